@@ -1,0 +1,70 @@
+"""Exact optimal transport on tiny inputs and the 1-D closed form. TEST INFRASTRUCTURE.
+
+  lp_permutations  Eq. (Da)-(Dd) for n = m <= 8 and uniform weights: the
+                   transport polytope's vertices are permutation matrices / n (Birkhoff),
+                   so W = min_sigma (1/n) sum_i c_{i sigma(i)}.
+  lp_linprog       Eq. (Da)-(Dd) for general weights with scipy's HiGHS LP solver as the
+                   library step.
+  w2_1d            d = 1, cost |x - y|^2: W_2^2 = int_0^1 |F^-1(t) - G^-1(t)|^2 dt
+                   (BJ north_star), evaluated exactly by merging the quantile step functions.
+"""
+from __future__ import annotations
+
+import itertools
+
+import numpy as np
+from scipy.optimize import linprog
+
+
+def cost_matrix(x, y):
+    x = np.asarray(x).reshape(len(x), -1)
+    y = np.asarray(y).reshape(len(y), -1)
+    return ((x[:, None, :] - y[None, :, :]) ** 2).sum(-1)
+
+
+def lp_permutations(x, y):
+    C = cost_matrix(x, y)
+    n = C.shape[0]
+    assert C.shape[1] == n and n <= 8
+    best = np.inf
+    for perm in itertools.permutations(range(n)):
+        v = C[np.arange(n), perm].sum() / n
+        best = min(best, v)
+    return best
+
+
+def lp_linprog(x, y, a, b):
+    C = cost_matrix(x, y)
+    n, m = C.shape
+    A_eq = np.zeros((n + m, n * m))
+    for i in range(n):
+        A_eq[i, i * m:(i + 1) * m] = 1.0
+    for j in range(m):
+        A_eq[n + j, j::m] = 1.0
+    b_eq = np.concatenate([a, b])
+    res = linprog(C.reshape(-1), A_eq=A_eq, b_eq=b_eq, bounds=(0, None), method="highs")
+    assert res.success, res.message
+    return float(res.fun), res.x.reshape(n, m)
+
+
+def w2_1d(x, a, y, b):
+    """int_0^1 |F^{-1}(t) - G^{-1}(t)|^2 dt for discrete measures on R."""
+    x = np.asarray(x).reshape(-1)
+    y = np.asarray(y).reshape(-1)
+    ix, iy = np.argsort(x, kind="stable"), np.argsort(y, kind="stable")
+    xs, as_ = x[ix], np.asarray(a)[ix]
+    ys, bs = y[iy], np.asarray(b)[iy]
+    Fa = np.cumsum(as_)
+    Fb = np.cumsum(bs)
+    Fa[-1] = 1.0
+    Fb[-1] = 1.0
+    cuts = np.unique(np.concatenate([[0.0], Fa, Fb]))
+    total = 0.0
+    for lo, hi in zip(cuts[:-1], cuts[1:]):
+        if hi <= lo:
+            continue
+        mid = 0.5 * (lo + hi)
+        qa = xs[min(np.searchsorted(Fa, mid), len(xs) - 1)]
+        qb = ys[min(np.searchsorted(Fb, mid), len(ys) - 1)]
+        total += (hi - lo) * (qa - qb) ** 2
+    return total
