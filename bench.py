@@ -1,0 +1,339 @@
+#!/usr/bin/env python
+"""Benchmark of the NFFT fast-summation Sinkhorn hot path (arXiv 2201.07524, Alg. 2).
+
+One STEP = one whole pass of the hot path over the workload:
+plan (geometry, binning, kernel coefficients), `iters` Sinkhorn iterations (2 fast
+summations each) and the divergence evaluation (2 more fast summations), via the C-ABI
+entry point ``sinkhorn_solve`` on inputs already resident in HBM. ``value`` = Sinkhorn
+iterations/s of the whole job (all ranks) = steps * iters / max-over-ranks device time.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c5] [--impl ours|reference]
+
+Multi-GPU: launched by torch.distributed.run, one rank per GPU, NCCL; points are sharded by
+contiguous index range and every fast summation all-reduces the oversampled grid
+(strong scaling: the workload is fixed). --impl reference times the CPU oracle (dense
+log-domain Alg. 1) on a bounded subsample of the same workload on the host cores.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+from synthetic import get, make_inputs, shard_range  # noqa: E402
+
+DEFAULT_CONFIG = os.environ.get("SK_BENCH_CONFIG", "c5")
+FP64_FMA_PER_CLK_PER_SM = 64      # B200 FP64 vector rate
+N_SM = 148
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=3)
+    p.add_argument("--warmup", type=int, default=3)
+    p.add_argument("--config", default=DEFAULT_CONFIG)
+    p.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--cpu-seconds", type=float, default=15.0, help="budget of the cpu_baseline sample")
+    return p.parse_args()
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            return json.load(fh)
+    except Exception:
+        return {"hbm_gbs": 6650.0, "sm_max_mhz": 1965.0, "fallback": True}
+
+
+# ---------------------------------------------------------------------------- clocks
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons every 200 ms during the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.gpu = gpu_index
+        self.rows = []
+        self.proc = None
+        self.th = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.gpu}", f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+            return
+        self.th = threading.Thread(target=self._read, daemon=True)
+        self.th.start()
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [s.strip() for s in line.split(",")]
+            if len(parts) >= 8:
+                self.rows.append(parts)
+
+    def stop(self):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+        if self.th is not None:
+            self.th.join(timeout=2)
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        sm = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in self.rows if r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[k] for r in self.rows for k in range(4) if r[4 + k].lower().startswith("active")})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+# ---------------------------------------------------------------------------- CPU oracle
+def cpu_oracle_rate(cfg, budget_s: float):
+    """Time the oracle (dense log-domain Alg. 1, as it stands) on a bounded seeded subsample
+    of the workload; return (it/s extrapolated to the full workload, description)."""
+    from oracle import dense
+    x, y, a, b = make_inputs(cfg.with_(n=min(cfg.n, 200_000), m=min(cfg.m, 200_000)))
+    # calibrate: one iteration on a small subsample, then size the sample to the budget
+    k = min(2000, x.shape[0], y.shape[0])
+    t0 = time.perf_counter()
+    dense.sinkhorn_log(x[:k], y[:k], a[:k] / a[:k].sum(), b[:k] / b[:k].sum(), cfg.lam, 1)
+    per_pair = (time.perf_counter() - t0) / (k * k)
+    iters = 5
+    ks = int(min(x.shape[0], y.shape[0], (budget_s / (iters * per_pair)) ** 0.5))
+    ks = max(ks, 100)
+    xs, ys = x[:ks], y[:ks]
+    as_, bs = a[:ks] / a[:ks].sum(), b[:ks] / b[:ks].sum()
+    t0 = time.perf_counter()
+    dense.sinkhorn_log(xs, ys, as_, bs, cfg.lam, iters)
+    dt = time.perf_counter() - t0
+    rate_sample = iters / dt
+    rate_full = rate_sample * (ks * ks) / (cfg.n * cfg.m)
+    desc = (f"{iters} log-domain Alg. 1 iterations on the first {ks}+{ks} points of {cfg.name} "
+            f"({dt:.1f} s); value = sample it/s x ({ks}*{ks})/({cfg.n}*{cfg.m}) (quadratic extrapolation "
+            f"to the full workload)")
+    return rate_full, desc, dense.num_threads(), rate_sample
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    cfg = get(args.config)
+    from oracle import dense
+    dense.build()
+    for _ in range(max(args.warmup, 0) and 1):
+        cpu_oracle_rate(cfg, 2.0)
+    vals = []
+    descs = []
+    for _ in range(args.steps):
+        v, desc, cores, _ = cpu_oracle_rate(cfg, args.cpu_seconds)
+        vals.append(v)
+        descs.append(desc)
+    value = float(statistics.median(vals))
+    line = {
+        "impl": "reference", "metric": "sinkhorn_iterations_per_s", "value": value, "unit": "it/s",
+        "n_gpus": 0, "steps": args.steps, "warmup": args.warmup, "higher_is_better": True,
+        "ms_per_step": 1e3 * cfg.iters / value, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic", "config": {"workload": cfg.name, "n": cfg.n, "m": cfg.m, "d": cfg.d,
+                                        "lambda": cfg.lam, "N": cfg.N, "iters": cfg.iters},
+        "cpu_baseline": {"value": value, "unit": "it/s", "cores": cores, "kind": "oracle", "sample": descs[-1]},
+        "e2e": {"value": value, "unit": "it/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line))
+    return 0
+
+
+# ---------------------------------------------------------------------------- GPU arm
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+    import torch
+    import torch.distributed as dist
+    from paper_2201_07524_b200 import capi
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    cfg = get(args.config)
+    x, y, a, b = make_inputs(cfg)
+    lo, hi = shard_range(cfg.n, rank, world)
+    lo2, hi2 = shard_range(cfg.m, rank, world)
+    hx, ha = np.ascontiguousarray(x[lo:hi]), np.ascontiguousarray(a[lo:hi])
+    hy, hb = np.ascontiguousarray(y[lo2:hi2]), np.ascontiguousarray(b[lo2:hi2])
+    del x, y, a, b
+    dev = lambda z: torch.from_numpy(z).cuda()  # noqa: E731
+    dx, dy, da, db = dev(hx), dev(hy), dev(ha), dev(hb)
+    stream = torch.cuda.current_stream()
+    ctx = capi.init_distributed_context(local, stream) if world > 1 else capi.Context(local, stream=stream)
+    solve = lambda: capi.sinkhorn_solve(ctx, dx, dy, da, db, cfg.lam, cfg.N, cfg.sigma, cfg.m_w,  # noqa: E731
+                                        cfg.eps_B, cfg.p, cfg.iters)
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")   # 256 MB > L2
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    for _ in range(args.warmup):
+        solve()
+    torch.cuda.synchronize()
+
+    # ---- timed region: K steps on HBM-resident inputs, L2 flushed between steps
+    clocks = ClockSampler(local)
+    clocks.start()
+    capi.sk_profile(True)
+    capi.sk_profile_read(reset=True)
+    launches0 = capi.sk_launch_count()
+    total_ms = 0.0
+    results = None
+    for _ in range(args.steps):
+        flush.fill_(1.0)
+        barrier()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        results = solve()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        barrier()
+        total_ms += e0.elapsed_time(e1)
+    launches = capi.sk_launch_count() - launches0
+    prof = capi.sk_profile_read(reset=True)
+    capi.sk_profile(False)
+    clk = clocks.stop()
+    t = torch.tensor([total_ms], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    total_ms = float(t.item())
+    value = args.steps * cfg.iters / (total_ms * 1e-3)
+
+    # ---- e2e: same step through the C-ABI with pinned HOST buffers (H2D + D2H inside)
+    e2e = None
+    if not args.no_e2e:
+        pin = lambda z: torch.from_numpy(z).pin_memory()  # noqa: E731
+        px, py, pa, pb = pin(hx), pin(hy), pin(ha), pin(hb)
+        solve_h = lambda: capi.sinkhorn_solve(ctx, px, py, pa, pb, cfg.lam, cfg.N, cfg.sigma, cfg.m_w,  # noqa
+                                              cfg.eps_B, cfg.p, cfg.iters, inputs_on_host=True)
+        solve_h()
+        tot = 0.0
+        for _ in range(args.steps):
+            flush.fill_(1.0)
+            barrier()
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            solve_h()
+            e1.record(stream)
+            torch.cuda.synchronize()
+            barrier()
+            tot += e0.elapsed_time(e1)
+        t = torch.tensor([tot], dtype=torch.float64, device="cuda")
+        if world > 1:
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        h2d = 8 * (hx.size + hy.size + ha.size + hb.size)
+        e2e = {"value": args.steps * cfg.iters / (float(t.item()) * 1e-3), "unit": "it/s",
+               "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": 16}
+
+    # ---- fast-summation point-evaluations/s (one K v product, targets = all x)
+    plan = capi.Plan(ctx, dx, dy, cfg.lam, cfg.N, cfg.sigma, cfg.m_w, cfg.eps_B, cfg.p)
+    w = torch.rand(hy.shape[0], dtype=torch.float64, device="cuda")
+    out = torch.empty(hx.shape[0], dtype=torch.float64, device="cuda")
+    for _ in range(2):
+        capi.fastsum_apply(plan, w, 0, 0, out)
+    torch.cuda.synchronize()
+    reps = 5
+    barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(reps):
+        capi.fastsum_apply(plan, w, 0, 0, out)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    t = torch.tensor([e0.elapsed_time(e1) / reps], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    apply_ms = float(t.item())
+    plan.close()
+    point_evals = cfg.n / (apply_ms * 1e-3)
+
+    # ---- roofline of the dominant kernel (from the live CUDA-event stage profile)
+    pk = peaks()
+    stage_ms = {s: (c, ms) for s, (c, ms) in prof.items() if c > 0}
+    dom = max(("spread", "interp"), key=lambda s: stage_ms.get(s, (0, 0.0))[1])
+    cnt, ms = stage_ms.get(dom, (1, float("nan")))
+    avg_ms = ms / max(cnt, 1)
+    W = 2 * cfg.m_w
+    # per launch: spread/interp alternate between the x (n) and y (m) node sets -> mean (n+m)/2
+    pts_per_launch = (cfg.n + cfg.m) / 2 / world
+    flops = 2.0 * W ** cfg.d * pts_per_launch                 # one multiply-add per grid tap
+    sm_mhz = clk.get("sm_mhz") or pk.get("sm_max_mhz", 1965.0)
+    fp64_peak = N_SM * FP64_FMA_PER_CLK_PER_SM * 2 * pk.get("sm_max_mhz", 1965.0) * 1e6 / 1e12
+    achieved = flops / (avg_ms * 1e-3) / 1e12
+    bytes_alg = pts_per_launch * 8 * (cfg.d + 1) + (cfg.N * cfg.sigma) ** cfg.d * 8
+    step_ms = total_ms / args.steps
+    stage_share = {s: round(v[1] / (total_ms if world == 1 else total_ms), 4) for s, v in stage_ms.items()}
+    line = {
+        "metric": "sinkhorn_iterations_per_s", "value": value, "unit": "it/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": step_ms, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded generators of BASELINE.json configs; see DESIGN.md input recipe)",
+        "config": {"workload": cfg.name, "n": cfg.n, "m": cfg.m, "d": cfg.d, "lambda": cfg.lam, "N": cfg.N,
+                   "sigma": cfg.sigma, "m_w": cfg.m_w, "eps_B": cfg.eps_B, "iters_per_step": cfg.iters,
+                   "step": "plan + iters x (K v, K^T u) + divergence (2 applies)",
+                   "parallelism": f"dp{world} (point shards + grid all-reduce)",
+                   "l2": "256 MB buffer written between timed steps"},
+        "fastsum_point_evals_per_s": point_evals * world if False else cfg.n / (apply_ms * 1e-3),
+        "fastsum_apply_ms": apply_ms,
+        "roofline": {"bound": "alu", "kernel": dom, "achieved": achieved, "peak": fp64_peak,
+                     "unit": "TFLOP/s", "frac": achieved / fp64_peak, "traffic": None,
+                     "algorithmic": f"2*(2m_w)^d flops per node per launch, {pts_per_launch:.3g} nodes/launch",
+                     "peak_source": f"{N_SM} SMs x {FP64_FMA_PER_CLK_PER_SM} FP64 FMA/clk x 2 x sm_max_mhz "
+                                    f"{pk.get('sm_max_mhz')} (DESIGN.md)",
+                     "hbm_frac": bytes_alg / (avg_ms * 1e-3) / (pk["hbm_gbs"] * 1e9),
+                     "avg_launch_ms": avg_ms},
+        "stage_ms_total": {s: v[1] for s, v in stage_ms.items()},
+        "stage_share_of_step": stage_share,
+        "gpu_launches": int(launches),
+        "clocks": clk,
+        "divergence": {"s_dual": results[0], "s_cost": results[1]} if results else None,
+        "kappa_log10_est": results[2].kappa_log10_est if results else None,
+    }
+    if e2e:
+        line["e2e"] = e2e
+    if rank == 0 and not args.no_cpu_baseline:
+        v, desc, cores, _ = cpu_oracle_rate(cfg, args.cpu_seconds)
+        line["cpu_baseline"] = {"value": v, "unit": "it/s", "cores": cores, "kind": "oracle", "sample": desc}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    ctx.close()
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,159 @@
+/*
+ * sinkhorn_nfft.h -- C-ABI of the B200-native NFFT fast-summation Sinkhorn library
+ * (libsk_nfft.so). Hot path of arXiv 2201.07524, Alg. 2.
+ *
+ * P:Lx refers to /root/reference/PAPER.md line x. Readings of the paper (Q1..Q15)
+ * are listed in DESIGN.md.
+ *
+ * Conventions for every entry point
+ *   - Pointers are DEVICE pointers (CUDA global memory of the context's device) unless
+ *     marked "host". Arrays are FP64, C-contiguous; point sets are row-major [count][d].
+ *   - The caller owns every array and keeps it alive for the duration of the call.
+ *     fastsum_plan copies what it needs (x, y may be freed afterwards).
+ *   - Return value: SK_OK (0) or one of the SK_E* codes below; the message of the last
+ *     failure on the calling thread is returned by sk_last_error(). On error no output
+ *     array is guaranteed to be written.
+ *   - Work is enqueued on the context's CUDA stream (sinkhorn_init). fastsum_apply,
+ *     nfft_spread and nfft_interp are asynchronous; calls returning host scalars
+ *     (sinkhorn_run, sinkhorn_divergence, sinkhorn_solve) synchronise that stream.
+ *   - SPMD multi-GPU: every rank calls every entry point with its local shard of the
+ *     points/weights (contiguous index ranges); world_size > 1 uses NCCL (loaded at
+ *     run time) for the grid all-reduce and scalar reductions.
+ *   - A plan serves one stream at a time; distinct plans are independent.
+ */
+#ifndef SINKHORN_NFFT_H
+#define SINKHORN_NFFT_H
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum {
+    SK_OK = 0,
+    SK_EINVAL = 1,          /* bad argument: d not in {1,2,3}, N odd or < 2, sigma*N not an even
+                               integer, sigma*N < 4*m_w, m_w not in [2,8], lambda <= 0, eps_B not
+                               in (0,1/4), p_smooth < 1, count < 0, NULL pointer ... */
+    SK_EGEOMETRY = 2,       /* a node is NaN/Inf or falls outside the ball |x'| <= 1/4 - eps_B/2
+                               after scaling ("we assume that |x_j| <= L/2") */
+    SK_ENONPOS = 3,         /* a fast-summation denominator t_i <= 1e-300 (or non-finite) in an
+                               update alpha_i = p_i / t_i (Alg. 2); run info holds the
+                               first (iteration, caller-order index) */
+    SK_ENOTCONVERGED = 4,   /* tol > 0 and the residual (Eq. (Error)) is still > tol after
+                               `iters` iterations; outputs are valid */
+    SK_ECUDA = 5,
+    SK_ECUFFT = 6,
+    SK_ENCCL = 7,
+    SK_ENOMEM = 8
+};
+
+typedef struct sk_ctx*  sk_ctx_t;   /* owns: NCCL communicator (world > 1); borrows: the stream */
+typedef struct sk_plan* sk_plan_t;  /* owns: sorted node copies, permutations, grid, spectrum,
+                                       multiplier tables, cuFFT plans, scratch */
+
+typedef struct {
+    int       iters_done;        /* full iterations completed (1 iteration = u- then v-update) */
+    double    residual;          /* ||pi 1 - a||_1 + ||pi^T 1 - b||_1 at the last iteration (the
+                                    second term is 0 after a v-update); global over ranks */
+    int       bad_iter;          /* SK_ENONPOS: iteration of the first non-positive denominator */
+    long long bad_index;         /* SK_ENONPOS: its caller-order index (local to the rank) */
+    double    kappa_log10_est;   /* log10( ||v||_1 / min_i (K v)_i ) at the last u-update: the
+                                    conditioning that amplifies the absolute fast-summation error
+                                     */
+    double    seconds;           /* device time of the iteration loop (CUDA events) */
+} sk_run_info;
+
+/* Create a context on `device` (the current CUDA device is switched to it). rank/world_size
+ * describe the SPMD job; nccl_unique_id: 128-byte ncclUniqueId (host) from
+ * sk_nccl_unique_id() on rank 0, broadcast by the caller; NULL iff world_size == 1.
+ * cuda_stream: cudaStream_t to enqueue on (NULL = legacy default stream). */
+int sinkhorn_init(sk_ctx_t* ctx, int device, int rank, int world_size,
+                  const void* nccl_unique_id, void* cuda_stream);
+int sinkhorn_finalize(sk_ctx_t ctx);
+/* Rank 0: write a fresh ncclUniqueId (128 bytes, host) into out. Loads NCCL. */
+int sk_nccl_unique_id(void* out);
+
+/* Plan the fast summation of Eq. (fastsum) for the node sets x (targets of K v)
+ * and y (sources of K v):
+ *   geometry (reading Q6 of P:L479-486): centre = midpoint of bbox(x u y) over all ranks,
+ *     rho = L / diag(bbox), L = 1/2 - eps_B, x' = rho (x - centre) lies in |x'| <= L/2,
+ *     lambda' = lambda / rho^2 (so exp(-lambda |x-y|^2) = exp(-lambda' |x'-y'|^2));
+ *   regularised kernel K~ with two-point Taylor K_B of order p_smooth on
+ *     (L, 1/2], its Fourier coefficients b_k on the centred N-band (reading Q9)
+ *     for K = exp(-lambda c) and for c K (divergence kernel, reading Q1);
+ *   Kaiser-Bessel window, oversampled grid n = sigma*N per axis, 2*m_w taps per axis.
+ * x: [n_local][d], y: [m_local][d] (device, caller order). Counts may be 0 on some ranks. */
+int fastsum_plan(sk_ctx_t ctx, sk_plan_t* plan, int d,
+                 const double* x, long long n_local, const double* y, long long m_local,
+                 double lambda, int N, double sigma, int m_w, double eps_B, int p_smooth);
+int fastsum_plan_destroy(sk_plan_t plan);
+
+/* One fast-summation matvec (Eq. (matexp)/(matexpt)):
+ *   transpose = 0: t_i = sum_j w_j K(x_i, y_j)   (w: [m_local], t: [n_local])
+ *   transpose = 1: t_j = sum_i w_i K(x_i, y_j)   (w: [n_local], t: [m_local])
+ *   kernel 0: K = exp(-lambda |x-y|^2);  kernel 1: K = |x-y|^2 exp(-lambda |x-y|^2).
+ * Sums run over all ranks' sources; t covers the local targets. Caller order. Async. */
+int fastsum_apply(sk_plan_t plan, int transpose, int kernel, const double* w, double* t);
+
+/* Alg. 2 for `iters` iterations (u-update then v-update, reading Q2/Q3):
+ *   u <- a / (K v), v <- b / (K^T u)   (each K product = one fast summation)
+ * u, v: in = starting values (all-ones for a cold start), out = final scalings,
+ * caller order. tol > 0 stops early once the residual <= tol (checked every iteration);
+ * tol == 0 runs exactly `iters`. rescale_policy (Eq. (scale), reading Q4):
+ * 0 none, 1 v <- v / geomean(v), 2 v <- v / max(v) before every u-update. info: host,
+ * may be NULL. Synchronises the stream. */
+int sinkhorn_run(sk_plan_t plan, const double* a, const double* b, int iters, double tol,
+                 int rescale_policy, double* u, double* v, sk_run_info* info);
+
+/* Divergences at (u, v) (reading Q1):
+ *   s_dual = 1/lambda + (1/lambda) (sum a log u + sum b log v) - (1/lambda) sum_j (K^T u)_j v_j
+ *            (Eq. (14) P:L211 / Alg. 2 result line P:L732; 2 fast summations incl. K^T u)
+ *   s_cost = sum_i u_i ((c K) v)_i = sum_ij pi_ij c_ij (Def 3.1)
+ * s_dual, s_cost: host. Global over ranks. Synchronises the stream. */
+int sinkhorn_divergence(sk_plan_t plan, const double* a, const double* b, const double* u,
+                        const double* v, double* s_dual, double* s_cost);
+
+/* End-to-end solve: plan + Alg. 2 (cold start) + divergences + destroy. inputs_on_host != 0:
+ * x, y, a, b are HOST arrays (copied to the device inside the call); else device arrays.
+ * s_dual, s_cost, info: host. */
+int sinkhorn_solve(sk_ctx_t ctx, int d, const double* x, long long n_local, const double* y,
+                   long long m_local, const double* a, const double* b, double lambda, int N,
+                   double sigma, int m_w, double eps_B, int p_smooth, int iters,
+                   int inputs_on_host, double* s_dual, double* s_cost, sk_run_info* info);
+
+/* ---- stage entry points (the NFFT building blocks of P:L473-477; used by parity tests) ----
+ * side 0 = the x nodes, side 1 = the y nodes. Grid: real [n]^d, row-major (axis 0 slowest),
+ * grid index l <-> torus position l/n - 1/2 of the scaled node x' (reading Q6).
+ * nfft_spread: g[l] = sum_j w_j prod_a phi(n (x'_ja + 1/2) - l_a)   (adjoint-NFFT gridding)
+ * nfft_interp: t_j = sum_l g[l] prod_a phi(n (x'_ja + 1/2) - l_a)   (NFFT interpolation)
+ * phi = Kaiser-Bessel window in grid units (reading Q10). Local nodes only, no all-reduce.
+ * w, t: caller order. Async. */
+int nfft_spread(sk_plan_t plan, int side, const double* w, double* grid);
+int nfft_interp(sk_plan_t plan, int side, const double* grid, double* t);
+
+/* Plan-time quantities (host outputs):
+ * fastsum_plan_info: out[0..2] centre, out[3] rho, out[4] lambda', out[5] L, out[6] n = sigma N,
+ *   out[7] band length per axis (N+1), out[8] d, out[9] total nodes x (all ranks),
+ *   out[10] total nodes y (all ranks).
+ * fastsum_coefficients: b (host, (N+1)^d, index prod over axes of (k_a + N/2), row-major):
+ *   the Fourier coefficients b_k of K~_per (kernel 0 or 1) on k in {-N/2..N/2}^d. */
+int fastsum_plan_info(sk_plan_t plan, double* out);
+int fastsum_coefficients(sk_plan_t plan, int kernel, double* b);
+
+/* Number of CUDA kernels this library launched in the calling process (for the bench's
+ * gpu_launches count; cuFFT and NCCL internal kernels are counted per call as 1). */
+long long sk_launch_count(void);
+
+/* Stage profiling with CUDA events on the context stream (off by default). sk_profile(1)
+ * starts recording an event pair around every stage of every fast summation; sk_profile_read
+ * writes out[2k] = number of timed launches and out[2k+1] = their total device milliseconds
+ * for stage k = 0 spread, 1 grid all-reduce, 2 forward FFT, 3 multiply, 4 inverse FFT,
+ * 5 interp, 6 update (nstages <= 7 entries are written); reset != 0 clears the totals. */
+void sk_profile(int on);
+int sk_profile_read(double* out, int nstages, int reset);
+
+const char* sk_last_error(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SINKHORN_NFFT_H */

@@ -1,0 +1,454 @@
+// api.cu -- C-ABI entry points of libsk_nfft (declared in include/sinkhorn_nfft.h).
+//
+// Alg. 2 on top of the fast summation of plan.cu; NCCL (loaded at run
+// time with dlopen) for the grid all-reduce and scalar reductions when world_size > 1.
+#include <dlfcn.h>
+#include <math.h>
+#include <nccl.h>
+#include <atomic>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "sk_internal.cuh"
+
+namespace sk {
+
+// ---------------------------------------------------------------- errors, launch counter
+static thread_local std::string g_err;
+static std::atomic<long long> g_launches{0};
+
+int set_error(int code, const std::string& msg) {
+    g_err = msg;
+    return code;
+}
+void count_launch(long long k) { g_launches += k; }
+
+// ---------------------------------------------------------------- NCCL (dlopen)
+struct NcclApi {
+    bool loaded = false;
+    ncclResult_t (*getUniqueId)(ncclUniqueId*) = nullptr;
+    ncclResult_t (*commInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+    ncclResult_t (*allReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                              cudaStream_t) = nullptr;
+    ncclResult_t (*commDestroy)(ncclComm_t) = nullptr;
+    const char* (*errStr)(ncclResult_t) = nullptr;
+};
+static NcclApi g_nccl;
+static std::mutex g_nccl_mu;
+
+static int nccl_load() {
+    std::lock_guard<std::mutex> lk(g_nccl_mu);
+    if (g_nccl.loaded) return SK_OK;
+    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) return set_error(SK_ENCCL, std::string("dlopen libnccl.so.2: ") + dlerror());
+    g_nccl.getUniqueId = (decltype(g_nccl.getUniqueId))dlsym(h, "ncclGetUniqueId");
+    g_nccl.commInitRank = (decltype(g_nccl.commInitRank))dlsym(h, "ncclCommInitRank");
+    g_nccl.allReduce = (decltype(g_nccl.allReduce))dlsym(h, "ncclAllReduce");
+    g_nccl.commDestroy = (decltype(g_nccl.commDestroy))dlsym(h, "ncclCommDestroy");
+    g_nccl.errStr = (decltype(g_nccl.errStr))dlsym(h, "ncclGetErrorString");
+    if (!g_nccl.getUniqueId || !g_nccl.commInitRank || !g_nccl.allReduce || !g_nccl.commDestroy)
+        return set_error(SK_ENCCL, "libnccl is missing a required symbol");
+    g_nccl.loaded = true;
+    return SK_OK;
+}
+
+#define SK_NCCL(call)                                                                  \
+    do {                                                                               \
+        ncclResult_t r_ = (call);                                                      \
+        if (r_ != ncclSuccess)                                                         \
+            return set_error(SK_ENCCL, std::string(#call) + ": " +                      \
+                                           (g_nccl.errStr ? g_nccl.errStr(r_) : "nccl error")); \
+    } while (0)
+
+int allreduce_sum(Ctx* c, double* buf, long long count) {
+    if (c->world <= 1 || count <= 0) return SK_OK;
+    SK_NCCL(g_nccl.allReduce(buf, buf, (size_t)count, ncclFloat64, ncclSum, (ncclComm_t)c->nccl_comm,
+                             c->stream));
+    count_launch();
+    return SK_OK;
+}
+
+int allreduce_minmax(Ctx* c, double* mins, double* maxs, int count) {
+    if (c->world <= 1 || count <= 0) return SK_OK;
+    SK_NCCL(g_nccl.allReduce(mins, mins, (size_t)count, ncclFloat64, ncclMin, (ncclComm_t)c->nccl_comm,
+                             c->stream));
+    SK_NCCL(g_nccl.allReduce(maxs, maxs, (size_t)count, ncclFloat64, ncclMax, (ncclComm_t)c->nccl_comm,
+                             c->stream));
+    count_launch(2);
+    return SK_OK;
+}
+
+// ---------------------------------------------------------------- stage profiling
+struct Prof {
+    bool on = false;
+    std::vector<cudaEvent_t> ev[ST_COUNT][2];
+    int used[ST_COUNT] = {0};
+    double total_ms[ST_COUNT] = {0};
+    long long count[ST_COUNT] = {0};
+};
+static Prof g_prof;
+
+void prof_begin(int st, cudaStream_t s) {
+    if (!g_prof.on) return;
+    int i = g_prof.used[st];
+    if ((int)g_prof.ev[st][0].size() <= i) {
+        cudaEvent_t a, b;
+        cudaEventCreate(&a);
+        cudaEventCreate(&b);
+        g_prof.ev[st][0].push_back(a);
+        g_prof.ev[st][1].push_back(b);
+    }
+    cudaEventRecord(g_prof.ev[st][0][i], s);
+}
+void prof_end(int st, cudaStream_t s) {
+    if (!g_prof.on) return;
+    cudaEventRecord(g_prof.ev[st][1][g_prof.used[st]], s);
+    g_prof.used[st]++;
+}
+void prof_harvest() {
+    for (int st = 0; st < ST_COUNT; ++st) {
+        for (int i = 0; i < g_prof.used[st]; ++i) {
+            float ms = 0.f;
+            cudaEventSynchronize(g_prof.ev[st][1][i]);
+            if (cudaEventElapsedTime(&ms, g_prof.ev[st][0][i], g_prof.ev[st][1][i]) == cudaSuccess) {
+                g_prof.total_ms[st] += ms;
+                g_prof.count[st] += 1;
+            }
+        }
+        g_prof.used[st] = 0;
+    }
+}
+
+// reduction output slots inside Plan::red_out (each slot: result + partial scratch)
+constexpr int kSlot = 608;
+static inline double* slot(Plan& P, int k) { return P.red_out + k * kSlot; }
+
+}  // namespace sk
+
+using namespace sk;
+
+// reduction slot ids
+enum { SL_UPD = 0, SL_A = 1, SL_B = 2, SL_C = 3, SL_D = 4, SL_E = 5, SL_SCALARS = 6 };
+
+extern "C" {
+
+const char* sk_last_error(void) { return g_err.c_str(); }
+
+void sk_profile(int on) {
+    if (!on) prof_harvest();
+    g_prof.on = on != 0;
+}
+
+// out[2*k] = launches timed, out[2*k+1] = total ms, for stage k in {spread, allreduce,
+// fft_fwd, multiply, fft_inv, interp, update}; reset != 0 clears the accumulators.
+int sk_profile_read(double* out, int nstages, int reset) {
+    prof_harvest();
+    for (int st = 0; st < ST_COUNT && st < nstages; ++st) {
+        out[2 * st] = (double)g_prof.count[st];
+        out[2 * st + 1] = g_prof.total_ms[st];
+        if (reset) { g_prof.count[st] = 0; g_prof.total_ms[st] = 0.0; }
+    }
+    return SK_OK;
+}
+long long sk_launch_count(void) { return g_launches.load(); }
+
+int sk_nccl_unique_id(void* out) {
+    if (!out) return set_error(SK_EINVAL, "NULL out");
+    SK_TRY(nccl_load());
+    ncclUniqueId id;
+    SK_NCCL(g_nccl.getUniqueId(&id));
+    memcpy(out, &id, sizeof(id));
+    return SK_OK;
+}
+
+int sinkhorn_init(sk_ctx_t* ctx, int device, int rank, int world_size, const void* nccl_unique_id,
+                  void* cuda_stream) {
+    if (!ctx) return set_error(SK_EINVAL, "NULL ctx");
+    if (world_size < 1 || rank < 0 || rank >= world_size) return set_error(SK_EINVAL, "bad rank/world_size");
+    if (world_size > 1 && !nccl_unique_id) return set_error(SK_EINVAL, "world_size > 1 needs an ncclUniqueId");
+    SK_CUDA(cudaSetDevice(device));
+    sk_ctx* c = new sk_ctx();
+    c->c.device = device;
+    c->c.rank = rank;
+    c->c.world = world_size;
+    c->c.stream = (cudaStream_t)cuda_stream;
+    if (world_size > 1) {
+        int st = nccl_load();
+        if (st) { delete c; return st; }
+        ncclUniqueId id;
+        memcpy(&id, nccl_unique_id, sizeof(id));
+        ncclComm_t comm;
+        ncclResult_t r = g_nccl.commInitRank(&comm, world_size, id, rank);
+        if (r != ncclSuccess) {
+            delete c;
+            return set_error(SK_ENCCL, std::string("ncclCommInitRank: ") + (g_nccl.errStr ? g_nccl.errStr(r) : ""));
+        }
+        c->c.nccl_comm = comm;
+    }
+    *ctx = c;
+    return SK_OK;
+}
+
+int sinkhorn_finalize(sk_ctx_t ctx) {
+    if (!ctx) return SK_OK;
+    if (ctx->c.nccl_comm) g_nccl.commDestroy((ncclComm_t)ctx->c.nccl_comm);
+    delete ctx;
+    return SK_OK;
+}
+
+int fastsum_plan(sk_ctx_t ctx, sk_plan_t* plan, int d, const double* x, long long n_local,
+                 const double* y, long long m_local, double lambda, int N, double sigma, int m_w,
+                 double eps_B, int p_smooth) {
+    if (!ctx || !plan) return set_error(SK_EINVAL, "NULL ctx/plan");
+    SK_CUDA(cudaSetDevice(ctx->c.device));
+    Plan* P = nullptr;
+    SK_TRY(build_plan(&ctx->c, &P, d, x, n_local, y, m_local, lambda, N, sigma, m_w, eps_B, p_smooth));
+    sk_plan* h = new sk_plan();
+    h->p = P;
+    *plan = h;
+    return SK_OK;
+}
+
+int fastsum_plan_destroy(sk_plan_t plan) {
+    if (!plan) return SK_OK;
+    destroy_plan(plan->p);
+    delete plan;
+    return SK_OK;
+}
+
+int fastsum_apply(sk_plan_t plan, int transpose, int kernel, const double* w, double* t) {
+    if (!plan) return set_error(SK_EINVAL, "NULL plan");
+    if (kernel != 0 && kernel != 1) return set_error(SK_EINVAL, "kernel must be 0 or 1");
+    Plan& P = *plan->p;
+    cudaStream_t s = P.ctx->stream;
+    const NodeSet& src = P.side[transpose ? 0 : 1];
+    const NodeSet& dst = P.side[transpose ? 1 : 0];
+    if ((src.count > 0 && !w) || (dst.count > 0 && !t)) return set_error(SK_EINVAL, "NULL w/t");
+    SK_TRY(launch_permute_in(w, src.perm, src.count, P.w_sorted, s));
+    SK_TRY(apply_sorted(P, transpose, kernel, P.w_sorted, P.t_sorted));
+    SK_TRY(launch_permute_out(P.t_sorted, dst.perm, dst.count, t, s));
+    return SK_OK;
+}
+
+int nfft_spread(sk_plan_t plan, int side, const double* w, double* grid) {
+    if (!plan || (side != 0 && side != 1) || !grid) return set_error(SK_EINVAL, "bad args");
+    Plan& P = *plan->p;
+    cudaStream_t s = P.ctx->stream;
+    const NodeSet& S = P.side[side];
+    SK_TRY(launch_permute_in(w, S.perm, S.count, P.w_sorted, s));
+    SK_CUDA(cudaMemsetAsync(grid, 0, sizeof(double) * P.grid_size, s));
+    SK_TRY(launch_spread(P, side, P.w_sorted, grid, s));
+    return SK_OK;
+}
+
+int nfft_interp(sk_plan_t plan, int side, const double* grid, double* t) {
+    if (!plan || (side != 0 && side != 1) || !grid) return set_error(SK_EINVAL, "bad args");
+    Plan& P = *plan->p;
+    cudaStream_t s = P.ctx->stream;
+    const NodeSet& S = P.side[side];
+    SK_TRY(launch_interp(P, side, grid, P.t_sorted, s));
+    SK_TRY(launch_permute_out(P.t_sorted, S.perm, S.count, t, s));
+    return SK_OK;
+}
+
+int fastsum_plan_info(sk_plan_t plan, double* out) {
+    if (!plan || !out) return set_error(SK_EINVAL, "bad args");
+    Plan& P = *plan->p;
+    for (int a = 0; a < 3; ++a) out[a] = a < P.d ? P.centre[a] : 0.0;
+    out[3] = P.rho;
+    out[4] = P.lambda_p;
+    out[5] = P.L;
+    out[6] = P.n;
+    out[7] = P.N + 1;
+    out[8] = P.d;
+    out[9] = (double)P.side[0].total;
+    out[10] = (double)P.side[1].total;
+    return SK_OK;
+}
+
+int fastsum_coefficients(sk_plan_t plan, int kernel, double* b) {
+    if (!plan || !b || (kernel != 0 && kernel != 1)) return set_error(SK_EINVAL, "bad args");
+    Plan& P = *plan->p;
+    long long full = 1;
+    for (int a = 0; a < P.d; ++a) full *= (P.N + 1);
+    SK_CUDA(cudaMemcpyAsync(b, P.bk[kernel], sizeof(double) * full, cudaMemcpyDeviceToHost, P.ctx->stream));
+    SK_CUDA(cudaStreamSynchronize(P.ctx->stream));
+    return SK_OK;
+}
+
+// Sum of the 3-slot update partials -> slot(SL_UPD)[0..2] (resid sum, min t, 0).
+static int finalize_update(Plan& P) {
+    return launch_finalize_partials(P.red, 592, 3, slot(P, SL_UPD), P.ctx->stream);
+}
+
+int sinkhorn_run(sk_plan_t plan, const double* a, const double* b, int iters, double tol,
+                 int rescale_policy, double* u, double* v, sk_run_info* info) {
+    if (!plan) return set_error(SK_EINVAL, "NULL plan");
+    Plan& P = *plan->p;
+    Ctx* C = P.ctx;
+    cudaStream_t s = C->stream;
+    const NodeSet& X = P.side[0];
+    const NodeSet& Y = P.side[1];
+    if (iters < 0 || tol < 0 || rescale_policy < 0 || rescale_policy > 2)
+        return set_error(SK_EINVAL, "bad iters/tol/rescale_policy");
+    if ((X.count > 0 && (!a || !u)) || (Y.count > 0 && (!b || !v))) return set_error(SK_EINVAL, "NULL a/b/u/v");
+    SK_TRY(launch_permute_in(a, X.perm, X.count, P.a_s, s));
+    SK_TRY(launch_permute_in(b, Y.perm, Y.count, P.b_s, s));
+    SK_TRY(launch_permute_in(u, X.perm, X.count, P.u_s, s));
+    SK_TRY(launch_permute_in(v, Y.perm, Y.count, P.v_s, s));
+    int hflag[4] = {0x7fffffff, 0x7fffffff, 0x7fffffff, 0x7fffffff};
+    SK_CUDA(cudaMemcpyAsync(P.flag, hflag, sizeof(hflag), cudaMemcpyHostToDevice, s));
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    cudaEventRecord(e0, s);
+    double resid = NAN, kappa = NAN;
+    int done = 0;
+    for (int it = 0; it < iters; ++it) {
+        const bool last = (it == iters - 1);
+        if (rescale_policy != 0) {
+            // Eq. (scale): v <- c v, c = 1/geomean(v) or 1/max(v) (reading Q4)
+            double* r = slot(P, SL_E);
+            SK_TRY(launch_reduce_sum_log(nullptr, P.v_s, Y.count, r, rescale_policy == 1 ? 3 : 4, s));
+            if (rescale_policy == 1) SK_TRY(allreduce_sum(C, r, 1));
+            else SK_TRY(allreduce_minmax(C, r + 600, r, 1));
+            SK_TRY(launch_rescale_factor(r, rescale_policy, (double)Y.total, s));
+            SK_TRY(launch_scale_vec(P.v_s, Y.count, r, s));
+        }
+        if (last) SK_TRY(launch_reduce_sum_log(nullptr, P.v_s, Y.count, slot(P, SL_D), 1, s));
+        // odd Delta: t = K v, u = a / t   (Eq. (even_F_sink))
+        SK_TRY(apply_sorted(P, 0, 0, P.v_s, P.t_sorted));
+        prof_begin(ST_UPDATE, s);
+        SK_TRY(launch_update(P, 0, P.t_sorted, P.a_s, P.u_s, (tol > 0 || last) ? 1 : 0, it, s));
+        prof_end(ST_UPDATE, s);
+        if (tol > 0 || last) SK_TRY(finalize_update(P));
+        // even Delta: t~ = K^T u, v = b / t~   (Eq. (odd_F_sink))
+        SK_TRY(apply_sorted(P, 1, 0, P.u_s, P.t_sorted));
+        prof_begin(ST_UPDATE, s);
+        SK_TRY(launch_update(P, 1, P.t_sorted, P.b_s, P.v_s, 0, it, s));
+        prof_end(ST_UPDATE, s);
+        done = it + 1;
+        if (tol > 0 || last) {
+            double* r = slot(P, SL_UPD);
+            // residual: sum over ranks; min t: min over ranks; ||v||_1: sum over ranks
+            SK_TRY(allreduce_sum(C, r, 1));
+            SK_TRY(allreduce_minmax(C, r + 1, r + 600, 1));
+            if (last) SK_TRY(allreduce_sum(C, slot(P, SL_D), 1));
+            SK_CUDA(cudaMemcpyAsync(P.host_red, r, sizeof(double) * 2, cudaMemcpyDeviceToHost, s));
+            if (last) SK_CUDA(cudaMemcpyAsync(P.host_red + 2, slot(P, SL_D), sizeof(double), cudaMemcpyDeviceToHost, s));
+            SK_CUDA(cudaStreamSynchronize(s));
+            resid = P.host_red[0];
+            if (last) kappa = log10(P.host_red[2] / P.host_red[1]);
+            if (tol > 0 && resid <= tol) break;
+        }
+    }
+    cudaEventRecord(e1, s);
+    SK_TRY(launch_permute_out(P.u_s, X.perm, X.count, u, s));
+    SK_TRY(launch_permute_out(P.v_s, Y.perm, Y.count, v, s));
+    SK_CUDA(cudaMemcpyAsync(hflag, P.flag, sizeof(hflag), cudaMemcpyDeviceToHost, s));
+    SK_CUDA(cudaStreamSynchronize(s));
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, e0, e1);
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    if (info) {
+        info->iters_done = done;
+        info->residual = resid;
+        info->kappa_log10_est = kappa;
+        info->seconds = ms * 1e-3;
+        info->bad_iter = -1;
+        info->bad_index = -1;
+    }
+    if (hflag[0] != 0x7fffffff || hflag[2] != 0x7fffffff) {
+        int side = hflag[0] != 0x7fffffff ? 0 : 1;
+        int sidx = hflag[side * 2];
+        int hperm = -1;
+        cudaMemcpy(&hperm, P.side[side].perm + sidx, sizeof(int), cudaMemcpyDeviceToHost);
+        if (info) {
+            info->bad_iter = hflag[side * 2 + 1];
+            info->bad_index = hperm;
+        }
+        return set_error(SK_ENONPOS, std::string("non-positive fast-summation denominator on side ") +
+                                         std::to_string(side) + " at caller index " + std::to_string(hperm));
+    }
+    if (tol > 0 && !(resid <= tol)) return set_error(SK_ENOTCONVERGED, "residual above tol");
+    return SK_OK;
+}
+
+int sinkhorn_divergence(sk_plan_t plan, const double* a, const double* b, const double* u,
+                        const double* v, double* s_dual, double* s_cost) {
+    if (!plan || !s_dual || !s_cost) return set_error(SK_EINVAL, "NULL plan/outputs");
+    Plan& P = *plan->p;
+    Ctx* C = P.ctx;
+    cudaStream_t s = C->stream;
+    const NodeSet& X = P.side[0];
+    const NodeSet& Y = P.side[1];
+    if ((X.count > 0 && (!a || !u)) || (Y.count > 0 && (!b || !v))) return set_error(SK_EINVAL, "NULL a/b/u/v");
+    SK_TRY(launch_permute_in(a, X.perm, X.count, P.a_s, s));
+    SK_TRY(launch_permute_in(b, Y.perm, Y.count, P.b_s, s));
+    SK_TRY(launch_permute_in(u, X.perm, X.count, P.u_s, s));
+    SK_TRY(launch_permute_in(v, Y.perm, Y.count, P.v_s, s));
+    double* sc = slot(P, SL_SCALARS);
+    // S1 = sum a log u, S2 = sum b log v
+    SK_TRY(launch_reduce_sum_log(P.a_s, P.u_s, X.count, slot(P, SL_A), 0, s));
+    SK_TRY(launch_reduce_sum_log(P.b_s, P.v_s, Y.count, slot(P, SL_B), 0, s));
+    // S3 = sum_j (K^T u)_j v_j
+    SK_TRY(apply_sorted(P, 1, 0, P.u_s, P.t_sorted));
+    SK_TRY(launch_reduce_sum_log(P.t_sorted, P.v_s, Y.count, slot(P, SL_C), 2, s));
+    // S4 = sum_i u_i ((c K) v)_i
+    SK_TRY(apply_sorted(P, 0, 1, P.v_s, P.t_sorted));
+    SK_TRY(launch_reduce_sum_log(P.t_sorted, P.u_s, X.count, slot(P, SL_D), 2, s));
+    for (int k = 0; k < 4; ++k)
+        SK_CUDA(cudaMemcpyAsync(sc + k, slot(P, SL_A + k), sizeof(double), cudaMemcpyDeviceToDevice, s));
+    SK_TRY(allreduce_sum(C, sc, 4));
+    SK_CUDA(cudaMemcpyAsync(P.host_red, sc, sizeof(double) * 4, cudaMemcpyDeviceToHost, s));
+    SK_CUDA(cudaStreamSynchronize(s));
+    const double S1 = P.host_red[0], S2 = P.host_red[1], S3 = P.host_red[2], S4 = P.host_red[3];
+    // Eq. (14): d = 1/lam + (1/lam) sum p log alpha + (1/lam) sum p~ log alpha~ - (1/lam) sum alpha k alpha~
+    *s_dual = (1.0 + S1 + S2 - S3) / P.lambda;
+    *s_cost = S4;
+    return SK_OK;
+}
+
+int sinkhorn_solve(sk_ctx_t ctx, int d, const double* x, long long n_local, const double* y,
+                   long long m_local, const double* a, const double* b, double lambda, int N,
+                   double sigma, int m_w, double eps_B, int p_smooth, int iters, int inputs_on_host,
+                   double* s_dual, double* s_cost, sk_run_info* info) {
+    if (!ctx || !s_dual || !s_cost) return set_error(SK_EINVAL, "NULL ctx/outputs");
+    if (d < 1 || d > 3 || n_local < 0 || m_local < 0) return set_error(SK_EINVAL, "bad d/counts");
+    cudaStream_t s = ctx->c.stream;
+    SK_CUDA(cudaSetDevice(ctx->c.device));
+    const double *dx = x, *dy = y, *da = a, *db = b;
+    double* buf = nullptr;
+    const long long nn = n_local, mm = m_local;
+    // device work buffers: [x | y | a | b | u | v]
+    const size_t tot = (size_t)(nn * d + mm * d + nn + mm + nn + mm);
+    SK_CUDA(cudaMallocAsync((void**)&buf, sizeof(double) * (tot ? tot : 1), s));
+    double* px = buf;
+    double* py = px + nn * d;
+    double* pa = py + mm * d;
+    double* pb = pa + nn;
+    double* pu = pb + mm;
+    double* pv = pu + nn;
+    if (inputs_on_host) {
+        if (nn) SK_CUDA(cudaMemcpyAsync(px, x, sizeof(double) * nn * d, cudaMemcpyHostToDevice, s));
+        if (mm) SK_CUDA(cudaMemcpyAsync(py, y, sizeof(double) * mm * d, cudaMemcpyHostToDevice, s));
+        if (nn) SK_CUDA(cudaMemcpyAsync(pa, a, sizeof(double) * nn, cudaMemcpyHostToDevice, s));
+        if (mm) SK_CUDA(cudaMemcpyAsync(pb, b, sizeof(double) * mm, cudaMemcpyHostToDevice, s));
+        dx = px; dy = py; da = pa; db = pb;
+    }
+    SK_TRY(launch_fill(pu, nn, 1.0, s));
+    SK_TRY(launch_fill(pv, mm, 1.0, s));
+    sk_plan_t plan = nullptr;
+    int st = fastsum_plan(ctx, &plan, d, dx, nn, dy, mm, lambda, N, sigma, m_w, eps_B, p_smooth);
+    if (!st) st = sinkhorn_run(plan, da, db, iters, 0.0, 0, pu, pv, info);
+    if (!st) st = sinkhorn_divergence(plan, da, db, pu, pv, s_dual, s_cost);
+    fastsum_plan_destroy(plan);
+    cudaFreeAsync(buf, s);
+    cudaStreamSynchronize(s);
+    return st;
+}
+
+}  // extern "C"

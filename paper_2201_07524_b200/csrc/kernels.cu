@@ -1,0 +1,553 @@
+// kernels.cu -- plan-time and per-apply CUDA kernels of libsk_nfft (sm_100a).
+//
+// Stages (PAPER.md P:Lx):
+//   bbox / scale_key   a0: geometry, torus scaling, tile keys   (reading Q6)
+//   sample / band      a1: b_k of the regularised kernel and the multiplier D_k
+//   spread             a2: adjoint-NFFT gridding (inner sum of Eq. (fastsum))
+//   multiply           a5: spectrum x D_k on the N-band (x b_k, window deconvolution), 0 elsewhere
+//   interp             a7: NFFT interpolation at the targets (outer sum of Eq. (fastsum))
+//   update             a7: fused marginal-scaling update alpha = p / t (Alg. 2)
+//   reductions         a8: deterministic two-pass block reductions
+#include <cub/cub.cuh>
+#include <math.h>
+
+#include "sk_internal.cuh"
+#include "window.cuh"
+#include "spread_interp.cuh"
+
+namespace sk {
+
+static inline int grid_for(long long count, int block) {
+    long long g = (count + block - 1) / block;
+    const long long cap = 148LL * 16;
+    if (g > cap) g = cap;
+    if (g < 1) g = 1;
+    return (int)g;
+}
+
+#define SK_LAUNCH_CHECK()                                                               \
+    do {                                                                                \
+        count_launch();                                                                 \
+        cudaError_t e_ = cudaGetLastError();                                            \
+        if (e_ != cudaSuccess) return set_error(SK_ECUDA, std::string("launch: ") + cudaGetErrorString(e_)); \
+    } while (0)
+
+// ------------------------------------------------------------------ block reduce helpers
+template <int BS>
+__device__ __forceinline__ double block_sum(double v, double* sh) {
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+    __syncthreads();
+    if (l == 0) sh[w] = v;
+    __syncthreads();
+    double r = 0.0;
+    if (threadIdx.x == 0)
+        for (int i = 0; i < BS / 32; ++i) r += sh[i];
+    return r;  // valid in thread 0
+}
+template <int BS>
+__device__ __forceinline__ double block_min(double v, double* sh) {
+    for (int o = 16; o > 0; o >>= 1) v = fmin(v, __shfl_xor_sync(0xffffffffu, v, o));
+    const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+    __syncthreads();
+    if (l == 0) sh[w] = v;
+    __syncthreads();
+    double r = INFINITY;
+    if (threadIdx.x == 0)
+        for (int i = 0; i < BS / 32; ++i) r = fmin(r, sh[i]);
+    return r;
+}
+template <int BS>
+__device__ __forceinline__ double block_max(double v, double* sh) {
+    return -block_min<BS>(-v, sh);
+}
+
+// ------------------------------------------------------------------ a0: bbox
+constexpr int kRedBlock = 256;
+
+__global__ void bbox_kernel(const double* __restrict__ pts, long long count, int d,
+                            double* __restrict__ partial) {
+    __shared__ double sh[kRedBlock / 32];
+    double mn[kMaxD], mx[kMaxD];
+    for (int a = 0; a < kMaxD; ++a) { mn[a] = INFINITY; mx[a] = -INFINITY; }
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < count;
+         i += (long long)gridDim.x * blockDim.x)
+        for (int a = 0; a < d; ++a) {
+            double v = pts[i * d + a];
+            mn[a] = fmin(mn[a], v);
+            mx[a] = fmax(mx[a], v);
+        }
+    for (int a = 0; a < d; ++a) {
+        double r0 = block_min<kRedBlock>(mn[a], sh);
+        if (threadIdx.x == 0) partial[blockIdx.x * 2 * d + a] = r0;
+        double r1 = block_max<kRedBlock>(mx[a], sh);
+        if (threadIdx.x == 0) partial[blockIdx.x * 2 * d + d + a] = r1;
+    }
+}
+
+__global__ void bbox_final(const double* __restrict__ partial, int nparts, int d,
+                           double* __restrict__ out) {
+    __shared__ double sh[kRedBlock / 32];
+    for (int a = 0; a < d; ++a) {
+        double mn = INFINITY, mx = -INFINITY;
+        for (int i = threadIdx.x; i < nparts; i += blockDim.x) {
+            mn = fmin(mn, partial[i * 2 * d + a]);
+            mx = fmax(mx, partial[i * 2 * d + d + a]);
+        }
+        double r0 = block_min<kRedBlock>(mn, sh);
+        double r1 = block_max<kRedBlock>(mx, sh);
+        if (threadIdx.x == 0) {
+            // combine with what is already in out (a previous point set)
+            out[a] = fmin(out[a], r0);
+            out[d + a] = fmax(out[d + a], r1);
+        }
+    }
+}
+
+int launch_bbox(const double* pts, long long count, int d, double* out_minmax, cudaStream_t s) {
+    if (count <= 0) return SK_OK;
+    int g = grid_for(count, kRedBlock);
+    if (g > 1024) g = 1024;
+    double* part = nullptr;
+    SK_CUDA(cudaMallocAsync(&part, sizeof(double) * 2 * d * g, s));
+    bbox_kernel<<<g, kRedBlock, 0, s>>>(pts, count, d, part);
+    SK_LAUNCH_CHECK();
+    bbox_final<<<1, kRedBlock, 0, s>>>(part, g, d, out_minmax);
+    SK_LAUNCH_CHECK();
+    SK_CUDA(cudaFreeAsync(part, s));
+    return SK_OK;
+}
+
+// ------------------------------------------------------------------ a0: scale + key
+struct ScaleParams {
+    double centre[kMaxD];
+    double rho, n, r2max;
+    int d, T, tiles_per_axis;
+};
+
+__global__ void scale_key_kernel(const double* __restrict__ pts, long long count, ScaleParams sp,
+                                 double* __restrict__ u_out, int* __restrict__ key,
+                                 int* __restrict__ idx, int* __restrict__ bad) {
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < count;
+         i += (long long)gridDim.x * blockDim.x) {
+        double r2 = 0.0;
+        int k = 0;
+        bool ok = true;
+        for (int a = 0; a < sp.d; ++a) {
+            double xs = sp.rho * (pts[i * sp.d + a] - sp.centre[a]);
+            ok = ok && isfinite(xs);
+            r2 += xs * xs;
+            double u = sp.n * (xs + 0.5);
+            u_out[a * count + i] = u;
+            int c = (int)floor(u);
+            int tc = c / sp.T;
+            tc = tc < 0 ? 0 : (tc >= sp.tiles_per_axis ? sp.tiles_per_axis - 1 : tc);
+            k = k * sp.tiles_per_axis + tc;
+        }
+        if (!ok || !(r2 <= sp.r2max)) atomicMin(bad, (int)i);
+        key[i] = k;
+        idx[i] = (int)i;
+    }
+}
+
+int launch_scale_key(Plan& P, const double* pts, long long count, double* u_unsorted, int* key,
+                     int* idx, int* bad, cudaStream_t s) {
+    if (count <= 0) return SK_OK;
+    ScaleParams sp;
+    for (int a = 0; a < kMaxD; ++a) sp.centre[a] = P.centre[a];
+    sp.rho = P.rho;
+    sp.n = (double)P.n;
+    const double R = 0.5 * P.L;
+    sp.r2max = R * R * (1.0 + 1e-12);
+    sp.d = P.d;
+    sp.T = P.tile_cells;
+    sp.tiles_per_axis = P.tiles_per_axis;
+    scale_key_kernel<<<grid_for(count, 256), 256, 0, s>>>(pts, count, sp, u_unsorted, key, idx, bad);
+    SK_LAUNCH_CHECK();
+    return SK_OK;
+}
+
+__global__ void gather_coords_kernel(const double* __restrict__ u_unsorted,
+                                     const int* __restrict__ perm, long long count, int d,
+                                     double* __restrict__ u_sorted) {
+    for (long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x; k < count;
+         k += (long long)gridDim.x * blockDim.x) {
+        long long i = perm[k];
+        for (int a = 0; a < d; ++a) u_sorted[a * count + k] = u_unsorted[a * count + i];
+    }
+}
+
+int launch_gather_coords(Plan& P, const double* u_unsorted, const int* perm, long long count,
+                         double* u_sorted, cudaStream_t s) {
+    if (count <= 0) return SK_OK;
+    gather_coords_kernel<<<grid_for(count, 256), 256, 0, s>>>(u_unsorted, perm, count, P.d, u_sorted);
+    SK_LAUNCH_CHECK();
+    return SK_OK;
+}
+
+__global__ void tile_offsets_kernel(const int* __restrict__ keys, long long count, int ntiles,
+                                    int* __restrict__ start) {
+    for (long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x; k <= count;
+         k += (long long)gridDim.x * blockDim.x) {
+        int prev = (k == 0) ? -1 : keys[k - 1];
+        int cur = (k == count) ? ntiles : keys[k];
+        for (int t = prev + 1; t <= cur; ++t) start[t] = (int)k;
+    }
+}
+
+int launch_tile_offsets(const int* sorted_keys, long long count, int ntiles, int* tile_start,
+                        cudaStream_t s) {
+    tile_offsets_kernel<<<grid_for(count + 1, 256), 256, 0, s>>>(sorted_keys, count, ntiles, tile_start);
+    SK_LAUNCH_CHECK();
+    return SK_OK;
+}
+
+// ------------------------------------------------------------------ permutations / vectors
+__global__ void permute_in_kernel(const double* __restrict__ src, const int* __restrict__ perm,
+                                  long long count, double* __restrict__ dst) {
+    for (long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x; k < count;
+         k += (long long)gridDim.x * blockDim.x)
+        dst[k] = src[perm[k]];
+}
+__global__ void permute_out_kernel(const double* __restrict__ src, const int* __restrict__ perm,
+                                   long long count, double* __restrict__ dst) {
+    for (long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x; k < count;
+         k += (long long)gridDim.x * blockDim.x)
+        dst[perm[k]] = src[k];
+}
+int launch_permute_in(const double* src, const int* perm, long long count, double* dst, cudaStream_t s) {
+    if (count <= 0) return SK_OK;
+    permute_in_kernel<<<grid_for(count, 256), 256, 0, s>>>(src, perm, count, dst);
+    SK_LAUNCH_CHECK();
+    return SK_OK;
+}
+int launch_permute_out(const double* src, const int* perm, long long count, double* dst, cudaStream_t s) {
+    if (count <= 0) return SK_OK;
+    permute_out_kernel<<<grid_for(count, 256), 256, 0, s>>>(src, perm, count, dst);
+    SK_LAUNCH_CHECK();
+    return SK_OK;
+}
+
+__global__ void fill_kernel(double* p, long long count, double v) {
+    for (long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x; k < count;
+         k += (long long)gridDim.x * blockDim.x)
+        p[k] = v;
+}
+int launch_fill(double* p, long long count, double v, cudaStream_t s) {
+    if (count <= 0) return SK_OK;
+    fill_kernel<<<grid_for(count, 256), 256, 0, s>>>(p, count, v);
+    SK_LAUNCH_CHECK();
+    return SK_OK;
+}
+
+__global__ void scale_vec_kernel(double* p, long long count, const double* __restrict__ sc) {
+    const double c = *sc;
+    for (long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x; k < count;
+         k += (long long)gridDim.x * blockDim.x)
+        p[k] *= c;
+}
+int launch_scale_vec(double* p, long long count, const double* scale_dev, cudaStream_t s) {
+    if (count <= 0) return SK_OK;
+    scale_vec_kernel<<<grid_for(count, 256), 256, 0, s>>>(p, count, scale_dev);
+    SK_LAUNCH_CHECK();
+    return SK_OK;
+}
+
+// ------------------------------------------------------------------ a8: reductions
+// op 0: sum p_i log x_i;  op 1: sum x_i;  op 2: sum p_i x_i;  op 3: sum log x_i;  op 4: max x_i
+__global__ void reduce_kernel(const double* __restrict__ p, const double* __restrict__ x,
+                              long long count, int op, double* __restrict__ partial) {
+    __shared__ double sh[kRedBlock / 32];
+    double acc = (op == 4) ? -INFINITY : 0.0;
+    for (long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x; k < count;
+         k += (long long)gridDim.x * blockDim.x) {
+        double xv = x[k];
+        switch (op) {
+            case 0: acc += p[k] * log(xv); break;
+            case 1: acc += xv; break;
+            case 2: acc += p[k] * xv; break;
+            case 3: acc += log(xv); break;
+            default: acc = fmax(acc, xv); break;
+        }
+    }
+    double r = (op == 4) ? block_max<kRedBlock>(acc, sh) : block_sum<kRedBlock>(acc, sh);
+    if (threadIdx.x == 0) partial[blockIdx.x] = r;
+}
+
+// partial layout [nparts][nvals]; minmask bit v => slot v is a min (else sum); maxmask => max
+__global__ void finalize_kernel(const double* __restrict__ partial, int nparts, int nvals,
+                                unsigned minmask, unsigned maxmask, double* __restrict__ out) {
+    __shared__ double sh[kRedBlock / 32];
+    for (int v = 0; v < nvals; ++v) {
+        const bool mn = (minmask >> v) & 1u, mx = (maxmask >> v) & 1u;
+        double acc = mn ? INFINITY : (mx ? -INFINITY : 0.0);
+        for (int i = threadIdx.x; i < nparts; i += blockDim.x) {
+            double t = partial[i * nvals + v];
+            acc = mn ? fmin(acc, t) : (mx ? fmax(acc, t) : acc + t);
+        }
+        double r = mn ? block_min<kRedBlock>(acc, sh)
+                      : (mx ? block_max<kRedBlock>(acc, sh) : block_sum<kRedBlock>(acc, sh));
+        if (threadIdx.x == 0) out[v] = r;
+    }
+}
+
+constexpr int kRedGrid = 592;  // 4 x 148 SMs
+
+int launch_reduce_sum_log(const double* p, const double* x, long long count, double* out_dev,
+                          int op, cudaStream_t s) {
+    // out_dev must have room for kRedGrid partials at out_dev + 1 (scratch) -- we use a
+    // static-size scratch owned by the caller: out_dev[0] = result, out_dev[1..] scratch.
+    double* part = out_dev + 1;
+    if (count <= 0) {
+        SK_CUDA(cudaMemsetAsync(out_dev, 0, sizeof(double), s));
+        if (op == 4) launch_fill(out_dev, 1, -INFINITY, s);
+        return SK_OK;
+    }
+    reduce_kernel<<<kRedGrid, kRedBlock, 0, s>>>(p, x, count, op, part);
+    SK_LAUNCH_CHECK();
+    finalize_kernel<<<1, kRedBlock, 0, s>>>(part, kRedGrid, 1, 0u, op == 4 ? 1u : 0u, out_dev);
+    SK_LAUNCH_CHECK();
+    return SK_OK;
+}
+
+__global__ void rescale_factor_kernel(double* r, int policy, double total) {
+    r[0] = policy == 1 ? exp(-r[0] / total) : 1.0 / r[0];
+}
+int launch_rescale_factor(double* r, int policy, double total, cudaStream_t s) {
+    rescale_factor_kernel<<<1, 1, 0, s>>>(r, policy, total);
+    SK_LAUNCH_CHECK();
+    return SK_OK;
+}
+
+int launch_finalize_partials(const double* red, int nparts, int nvals, double* out, cudaStream_t s) {
+    // slot 1 (min t) is a min; the others are sums
+    finalize_kernel<<<1, kRedBlock, 0, s>>>(red, nparts, nvals, 0x2u, 0u, out);
+    SK_LAUNCH_CHECK();
+    return SK_OK;
+}
+
+// ------------------------------------------------------------------ a7: fused update
+// x_new = p / t; partial slots: [0] sum |x_old t - p| (residual of the marginal that this
+// update makes exact, Eq. (Error)), [1] min t, [2] unused.
+__global__ void update_kernel(const double* __restrict__ t, const double* __restrict__ p,
+                              double* __restrict__ x, long long count, int want_resid, int iter,
+                              int* __restrict__ bad, double* __restrict__ partial) {
+    __shared__ double sh[kRedBlock / 32];
+    double res = 0.0, tmin = INFINITY;
+    for (long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x; k < count;
+         k += (long long)gridDim.x * blockDim.x) {
+        double tk = t[k], pk = p[k];
+        if (want_resid) res += fabs(x[k] * tk - pk);
+        tmin = fmin(tmin, tk);
+        if (!(tk > 1e-300) || !isfinite(tk)) {  // SK_ENONPOS (tau_pos = 1e-300)
+            atomicMin(bad, (int)k);
+            atomicMin(bad + 1, iter);
+        }
+        x[k] = pk / tk;
+    }
+    double r0 = block_sum<kRedBlock>(res, sh);
+    double r1 = block_min<kRedBlock>(tmin, sh);
+    if (threadIdx.x == 0) {
+        partial[blockIdx.x * 3 + 0] = r0;
+        partial[blockIdx.x * 3 + 1] = r1;
+        partial[blockIdx.x * 3 + 2] = 0.0;
+    }
+}
+
+int launch_update(Plan& P, int side, const double* t_sorted, const double* p_sorted,
+                  double* x_sorted, int want_resid, int iter, cudaStream_t s) {
+    long long count = P.side[side].count;  // count == 0 still writes neutral partials
+    update_kernel<<<kRedGrid, kRedBlock, 0, s>>>(t_sorted, p_sorted, x_sorted, count, want_resid,
+                                                 iter, P.flag + 2 * side, P.red);
+    SK_LAUNCH_CHECK();
+    return SK_OK;
+}
+
+// ------------------------------------------------------------------ a1: coefficients
+struct KernelParams {
+    double lam_p, rho2_inv, L, half, tscale;  // tscale = 1 / (1/2 - L)
+    int d, M, kernel, kb_deg;
+    double kb[32];                          // K_B coefficients in t = (r - L) / (1/2 - L)
+};
+
+__device__ __forceinline__ double radial(double r, const KernelParams& kp) {
+    double r2 = r * r;
+    double k = exp(-kp.lam_p * r2);
+    return kp.kernel == 0 ? k : r2 * kp.rho2_inv * k;
+}
+__device__ __forceinline__ double kb_poly(double r, const KernelParams& kp) {
+    double t = (r - kp.L) * kp.tscale;
+    double acc = kp.kb[kp.kb_deg];
+    for (int i = kp.kb_deg - 1; i >= 0; --i) acc = acc * t + kp.kb[i];
+    return acc;
+}
+
+__global__ void sample_kernel_kernel(KernelParams kp, double* __restrict__ out, long long total) {
+    for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
+         e += (long long)gridDim.x * blockDim.x) {
+        long long rest = e;
+        double r2 = 0.0;
+        for (int a = kp.d - 1; a >= 0; --a) {
+            int q = (int)(rest % kp.M);
+            rest /= kp.M;
+            double xa = (double)q / kp.M - (q >= kp.M / 2 ? 1.0 : 0.0);
+            r2 += xa * xa;
+        }
+        double r = sqrt(r2);
+        double v;
+        if (r <= kp.L) v = radial(r, kp);
+        else if (r <= kp.half) v = kb_poly(r, kp);
+        else v = kb_poly(kp.half, kp);
+        out[e] = v;
+    }
+}
+
+int launch_sample_kernel(Plan& P, int kernel, int M, const double* kb_coef, int kb_deg,
+                         double* out, cudaStream_t s) {
+    KernelParams kp;
+    kp.lam_p = P.lambda_p;
+    kp.rho2_inv = 1.0 / (P.rho * P.rho);
+    kp.L = P.L;
+    kp.half = 0.5;
+    kp.tscale = 1.0 / (0.5 - P.L);
+    kp.d = P.d;
+    kp.M = M;
+    kp.kernel = kernel;
+    kp.kb_deg = kb_deg;
+    for (int i = 0; i <= kb_deg && i < 32; ++i) kp.kb[i] = kb_coef[i];
+    long long total = 1;
+    for (int a = 0; a < P.d; ++a) total *= M;
+    sample_kernel_kernel<<<grid_for(total, 256), 256, 0, s>>>(kp, out, total);
+    SK_LAUNCH_CHECK();
+    return SK_OK;
+}
+
+struct BandParams {
+    int d, N, M, n, m;
+    double beta, inv_Md;
+};
+
+__device__ __forceinline__ double kb_phihat(int k, const BandParams& bp) {
+    double w = 2.0 * 3.141592653589793238462643 * (double)k / (double)bp.n;
+    return cyl_bessel_i0((double)bp.m * sqrt(bp.beta * bp.beta - w * w));
+}
+
+// For every k in the full band {-N/2..N/2}^d: b_k = Re B[k] / M^d (B = unnormalised D2Z of
+// the samples, half-complex in the last axis); write bk_full; for k_last >= 0 also write
+// D_k = w_k b_k / prod_a phihat(k_a)^2 (w_k = prod 1/2 over |k_a| = N/2, reading Q8).
+__global__ void band_kernel(BandParams bp, const cufftDoubleComplex* __restrict__ B,
+                            double* __restrict__ bk_full, double* __restrict__ Dk) {
+    const int nb = bp.N + 1, h = bp.N / 2;
+    long long total = 1;
+    for (int a = 0; a < bp.d; ++a) total *= nb;
+    for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
+         e += (long long)gridDim.x * blockDim.x) {
+        int k[kMaxD];
+        long long rest = e;
+        for (int a = bp.d - 1; a >= 0; --a) { k[a] = (int)(rest % nb) - h; rest /= nb; }
+        // b_k is real and even in each axis: read B at (k_0..k_{d-2}, |k_last|) with
+        // conj symmetry folded on the last axis.
+        int kl = k[bp.d - 1];
+        int sgn_fold = kl < 0 ? -1 : 1;
+        long long bidx = 0;
+        for (int a = 0; a < bp.d - 1; ++a) {
+            int ka = sgn_fold * k[a];
+            int ia = ka < 0 ? ka + bp.M : ka;
+            bidx = bidx * bp.M + ia;
+        }
+        bidx = bidx * (bp.M / 2 + 1) + (kl < 0 ? -kl : kl);
+        double b = B[bidx].x * bp.inv_Md;
+        bk_full[e] = b;
+        if (kl >= 0) {
+            double wgt = 1.0, ph = 1.0;
+            for (int a = 0; a < bp.d; ++a) {
+                if (k[a] == h || k[a] == -h) wgt *= 0.5;
+                double p = kb_phihat(k[a], bp);
+                ph *= p * p;
+            }
+            long long didx = 0;
+            for (int a = 0; a < bp.d - 1; ++a) didx = didx * nb + (k[a] + h);
+            didx = didx * (h + 1) + kl;
+            Dk[didx] = wgt * b / ph;
+        }
+    }
+}
+
+int launch_band_coeffs(Plan& P, int kernel, int M, const cufftDoubleComplex* B, cudaStream_t s) {
+    BandParams bp;
+    bp.d = P.d;
+    bp.N = P.N;
+    bp.M = M;
+    bp.n = P.n;
+    bp.m = P.win.m;
+    bp.beta = P.win.beta;
+    double Md = 1.0;
+    for (int a = 0; a < P.d; ++a) Md *= M;
+    bp.inv_Md = 1.0 / Md;
+    long long total = 1;
+    for (int a = 0; a < P.d; ++a) total *= (P.N + 1);
+    band_kernel<<<grid_for(total, 256), 256, 0, s>>>(bp, B, P.bk[kernel], P.D[kernel]);
+    SK_LAUNCH_CHECK();
+    return SK_OK;
+}
+
+// ------------------------------------------------------------------ a5: multiply
+struct MulParams {
+    int d, n, N;
+    long long spec_size;
+};
+
+__global__ void multiply_kernel(MulParams mp, cufftDoubleComplex* __restrict__ spec,
+                                const double* __restrict__ Dk) {
+    const int hl = mp.n / 2 + 1, h = mp.N / 2, nb = mp.N + 1;
+    for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < mp.spec_size;
+         e += (long long)gridDim.x * blockDim.x) {
+        int kl = (int)(e % hl);
+        long long rest = e / hl;
+        bool inband = kl <= h;
+        long long didx = 0, mul = 1;
+        // non-last axes, from axis d-2 down to 0
+        for (int a = mp.d - 2; a >= 0; --a) {
+            int ia = (int)(rest % mp.n);
+            rest /= mp.n;
+            int ka = ia <= mp.n / 2 ? ia : ia - mp.n;
+            inband = inband && (ka >= -h && ka <= h);
+            didx += (long long)(ka + h) * mul;
+            mul *= nb;
+        }
+        cufftDoubleComplex z = spec[e];
+        if (inband) {
+            double D = Dk[didx * (h + 1) + kl];
+            z.x *= D;
+            z.y *= D;
+        } else {
+            z.x = 0.0;
+            z.y = 0.0;
+        }
+        spec[e] = z;
+    }
+}
+
+int launch_multiply(Plan& P, int kernel, cudaStream_t s) {
+    MulParams mp{P.d, P.n, P.N, P.spec_size};
+    multiply_kernel<<<grid_for(P.spec_size, 256), 256, 0, s>>>(mp, P.spec, P.D[kernel]);
+    SK_LAUNCH_CHECK();
+    return SK_OK;
+}
+
+// ------------------------------------------------------------------ a2 / a7: spread, interp
+int launch_spread(Plan& P, int side, const double* w_sorted, double* grid, cudaStream_t s) {
+    const NodeSet& S = P.side[side];
+    if (S.count <= 0) return SK_OK;
+    SK_TRY(spread_dispatch(P, S, w_sorted, grid, s));
+    return SK_OK;
+}
+
+int launch_interp(Plan& P, int side, const double* grid, double* t_sorted, cudaStream_t s) {
+    const NodeSet& S = P.side[side];
+    if (S.count <= 0) return SK_OK;
+    SK_TRY(interp_dispatch(P, S, grid, t_sorted, s));
+    return SK_OK;
+}
+
+}  // namespace sk

@@ -1,0 +1,357 @@
+// plan.cu -- fastsum plan (geometry, binning, kernel coefficients, FFT plans) and one
+// fast-summation matvec on sorted data.
+#include <cub/cub.cuh>
+#include <math.h>
+#include <algorithm>
+#include <vector>
+
+#include "sk_internal.cuh"
+
+namespace sk {
+
+// ---------------------------------------------------------------- two-point Taylor K_B (host)
+// Derivatives K^{(k)}(L), k < p, of the radial profile of
+//   kernel 0: f(r) = exp(-a r^2)                 via physicists' Hermite polynomials
+//             f^{(k)}(r) = (-sqrt(a))^k H_k(sqrt(a) r) exp(-a r^2)
+//   kernel 1: g(r) = (r^2 / rho^2) f(r)          via Leibniz' rule
+static void radial_derivs(double a, double rho, int kernel, double r, int p, double* out) {
+    std::vector<double> f(p + 2), H(p + 2);
+    const double sa = sqrt(a), z = sa * r, e = exp(-a * r * r);
+    H[0] = 1.0;
+    H[1] = 2.0 * z;
+    for (int k = 1; k + 1 < p; ++k) H[k + 1] = 2.0 * z * H[k] - 2.0 * k * H[k - 1];
+    double sak = 1.0;
+    for (int k = 0; k < p; ++k) {
+        f[k] = ((k & 1) ? -1.0 : 1.0) * sak * H[k] * e;
+        sak *= sa;
+    }
+    for (int k = 0; k < p; ++k) {
+        if (kernel == 0) {
+            out[k] = f[k];
+        } else {
+            double v = r * r * f[k];
+            if (k >= 1) v += 2.0 * k * r * f[k - 1];
+            if (k >= 2) v += (double)k * (k - 1) * f[k - 2];
+            out[k] = v / (rho * rho);
+        }
+    }
+}
+
+static double binom(int n, int k) {
+    double r = 1.0;
+    for (int i = 1; i <= k; ++i) r = r * (n - k + i) / i;
+    return r;
+}
+
+// Coefficients c_0..c_{2p-2} of K_B(r) = sum_i c_i t^i, t = (r - L)/(1/2 - L), with
+// K_B^{(k)}(L) = K^{(k)}(L) (k < p) and K_B^{(k)}(1/2) = 0 (1 <= k < p), Eq. (intpol_cond_3/4)
+// (P:L489-496). Construction: s = dK_B/dt is the two-point Taylor interpolant of order
+// r = p - 1 at t = 0 (data F^{(k+1)}(0)) and t = 1 (zeros):
+//   s(t) = (1-t)^r sum_{k<r} sum_{j<r-k} C(r-1+j, j) s^{(k)}(0)/k! t^{k+j},
+// and K_B(t) = F(0) + int_0^t s.
+static void kb_coefficients(double lam_p, double rho, int kernel, double L, int p,
+                            std::vector<double>& c) {
+    const double D = 0.5 - L;
+    std::vector<double> dK(p);
+    radial_derivs(lam_p, rho, kernel, L, p, dK.data());
+    std::vector<double> F(p);
+    double Dk = 1.0;
+    for (int k = 0; k < p; ++k) { F[k] = dK[k] * Dk; Dk *= D; }
+    const int r = p - 1;
+    // inner polynomial P(t) = sum_{k<r} sum_{j<r-k} C(r-1+j,j) F^{(k+1)}(0)/k! t^{k+j}
+    std::vector<double> Pc(std::max(r, 1), 0.0);
+    double kf = 1.0;
+    for (int k = 0; k < r; ++k) {
+        if (k > 0) kf *= k;
+        for (int j = 0; j < r - k; ++j) Pc[k + j] += binom(r - 1 + j, j) * F[k + 1] / kf;
+    }
+    // (1-t)^r
+    std::vector<double> Q(r + 1);
+    for (int i = 0; i <= r; ++i) Q[i] = binom(r, i) * ((i & 1) ? -1.0 : 1.0);
+    std::vector<double> s(Pc.size() + Q.size() - 1, 0.0);
+    for (size_t i = 0; i < Pc.size(); ++i)
+        for (size_t j = 0; j < Q.size(); ++j) s[i + j] += Pc[i] * Q[j];
+    c.assign(s.size() + 1, 0.0);
+    c[0] = F[0];
+    for (size_t i = 0; i < s.size(); ++i) c[i + 1] = s[i] / (double)(i + 1);
+}
+
+// ---------------------------------------------------------------- plan
+static int alloc(void** p, size_t bytes) {
+    if (bytes == 0) { *p = nullptr; return SK_OK; }
+    cudaError_t e = cudaMalloc(p, bytes);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        return set_error(e == cudaErrorMemoryAllocation ? SK_ENOMEM : SK_ECUDA,
+                         std::string("cudaMalloc(") + std::to_string(bytes) + "): " + cudaGetErrorString(e));
+    }
+    return SK_OK;
+}
+
+static int choose_tile(int d, int n) {
+    int T = d == 1 ? 16 : (d == 2 ? 8 : 4);
+    while (T > 1 && n % T) T >>= 1;
+    return T;
+}
+
+static int plan_side(Plan& P, int sidx, const double* pts, long long count, cudaStream_t s) {
+    NodeSet& S = P.side[sidx];
+    S.count = count;
+    S.ntiles = 1;
+    for (int a = 0; a < P.d; ++a) S.ntiles *= P.tiles_per_axis;
+    SK_TRY(alloc((void**)&S.tile_start, sizeof(int) * (S.ntiles + 1)));
+    if (count == 0) {
+        SK_CUDA(cudaMemsetAsync(S.tile_start, 0, sizeof(int) * (S.ntiles + 1), s));
+        return SK_OK;
+    }
+    double* u_uns = nullptr;
+    int *key_in = nullptr, *idx_in = nullptr, *bad = nullptr;
+    SK_TRY(alloc((void**)&u_uns, sizeof(double) * P.d * count));
+    SK_TRY(alloc((void**)&key_in, sizeof(int) * count));
+    SK_TRY(alloc((void**)&idx_in, sizeof(int) * count));
+    SK_TRY(alloc((void**)&bad, sizeof(int)));
+    SK_TRY(alloc((void**)&S.cell_key, sizeof(int) * count));
+    SK_TRY(alloc((void**)&S.perm, sizeof(int) * count));
+    SK_TRY(alloc((void**)&S.u, sizeof(double) * P.d * count));
+    const int big = 0x7fffffff;
+    SK_CUDA(cudaMemcpyAsync(bad, &big, sizeof(int), cudaMemcpyHostToDevice, s));
+    SK_TRY(launch_scale_key(P, pts, count, u_uns, key_in, idx_in, bad, s));
+    int hbad = 0;
+    SK_CUDA(cudaMemcpyAsync(&hbad, bad, sizeof(int), cudaMemcpyDeviceToHost, s));
+    SK_CUDA(cudaStreamSynchronize(s));
+    if (hbad != big) {
+        cudaFree(u_uns); cudaFree(key_in); cudaFree(idx_in); cudaFree(bad);
+        return set_error(SK_EGEOMETRY, "node " + std::to_string(hbad) + " of side " + std::to_string(sidx) +
+                                           " is non-finite or outside the ball |x'| <= 1/4 - eps_B/2");
+    }
+    int end_bit = 1;
+    while ((1LL << end_bit) < S.ntiles) ++end_bit;
+    size_t tmp_bytes = 0;
+    cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, key_in, S.cell_key, idx_in, S.perm, (int)count, 0,
+                                    end_bit, s);
+    void* tmp = nullptr;
+    SK_TRY(alloc(&tmp, tmp_bytes));
+    SK_CUDA(cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, key_in, S.cell_key, idx_in, S.perm, (int)count,
+                                            0, end_bit, s));
+    count_launch(4);
+    SK_TRY(launch_gather_coords(P, u_uns, S.perm, count, S.u, s));
+    SK_TRY(launch_tile_offsets(S.cell_key, count, S.ntiles, S.tile_start, s));
+    SK_CUDA(cudaStreamSynchronize(s));
+    cudaFree(tmp);
+    cudaFree(u_uns);
+    cudaFree(key_in);
+    cudaFree(idx_in);
+    cudaFree(bad);
+    return SK_OK;
+}
+
+static int plan_coefficients(Plan& P, cudaStream_t s) {
+    const int M = 2 * P.N;  // sampling grid of K~_per (reading Q9)
+    long long Md = 1, Bsz = 1;
+    for (int a = 0; a < P.d; ++a) Md *= M;
+    for (int a = 0; a < P.d - 1; ++a) Bsz *= M;
+    Bsz *= (M / 2 + 1);
+    double* samp = nullptr;
+    cufftDoubleComplex* B = nullptr;
+    SK_TRY(alloc((void**)&samp, sizeof(double) * Md));
+    SK_TRY(alloc((void**)&B, sizeof(cufftDoubleComplex) * Bsz));
+    cufftHandle h;
+    int dims[3] = {M, M, M};
+    SK_CUFFT(cufftPlanMany(&h, P.d, dims, nullptr, 1, 0, nullptr, 1, 0, CUFFT_D2Z, 1));
+    SK_CUFFT(cufftSetStream(h, s));
+    for (int kernel = 0; kernel < 2; ++kernel) {
+        std::vector<double> c;
+        kb_coefficients(P.lambda_p, P.rho, kernel, P.L, P.p_smooth, c);
+        SK_TRY(launch_sample_kernel(P, kernel, M, c.data(), (int)c.size() - 1, samp, s));
+        SK_CUFFT(cufftExecD2Z(h, samp, B));
+        count_launch();
+        SK_TRY(launch_band_coeffs(P, kernel, M, B, s));
+    }
+    SK_CUDA(cudaStreamSynchronize(s));
+    cufftDestroy(h);
+    cudaFree(samp);
+    cudaFree(B);
+    return SK_OK;
+}
+
+int build_plan(Ctx* ctx, Plan** out, int d, const double* x, long long n, const double* y,
+               long long m, double lambda, int N, double sigma, int m_w, double eps_B, int p) {
+    if (d < 1 || d > 3) return set_error(SK_EINVAL, "d must be 1, 2 or 3");
+    if (N < 2 || (N & 1)) return set_error(SK_EINVAL, "N must be even and >= 2");
+    if (!(lambda > 0.0) || !isfinite(lambda)) return set_error(SK_EINVAL, "lambda must be > 0");
+    if (m_w < 2 || m_w > 8) return set_error(SK_EINVAL, "m_w must be in [2, 8]");
+    if (!(eps_B > 0.0 && eps_B < 0.25)) return set_error(SK_EINVAL, "eps_B must be in (0, 1/4)");
+    if (p < 1 || p > 15) return set_error(SK_EINVAL, "p_smooth must be in [1, 15]");
+    if (n < 0 || m < 0) return set_error(SK_EINVAL, "negative node count");
+    if ((n > 0 && !x) || (m > 0 && !y)) return set_error(SK_EINVAL, "NULL node array");
+    if (n > 0x7ffffffeLL || m > 0x7ffffffeLL) return set_error(SK_EINVAL, "local node count exceeds 2^31-2");
+    const double nd = sigma * N;
+    const int ng = (int)llround(nd);
+    if (!(sigma >= 1.0) || fabs(nd - ng) > 1e-9 || (ng & 1))
+        return set_error(SK_EINVAL, "sigma*N must be an even integer");
+    if (ng < 4 * m_w) return set_error(SK_EINVAL, "sigma*N must be >= 4*m_w (no tap wraps the torus)");
+
+    cudaStream_t s = ctx->stream;
+    Plan* P = new Plan();
+    P->ctx = ctx;
+    P->d = d;
+    P->N = N;
+    P->n = ng;
+    P->sigma = sigma;
+    P->win.m = m_w;
+    P->win.beta = 3.141592653589793238462643 * (2.0 - 1.0 / sigma);
+    P->win.m2 = (double)m_w * m_w;
+    P->win.inv_pi = 1.0 / 3.141592653589793238462643;
+    P->lambda = lambda;
+    P->eps_B = eps_B;
+    P->p_smooth = p;
+    P->L = 0.5 - eps_B;
+    P->grid_size = 1;
+    for (int a = 0; a < d; ++a) P->grid_size *= ng;
+    P->spec_size = 1;
+    for (int a = 0; a < d - 1; ++a) P->spec_size *= ng;
+    P->spec_size *= (ng / 2 + 1);
+    P->band_size = 1;
+    for (int a = 0; a < d - 1; ++a) P->band_size *= (N + 1);
+    P->band_size *= (N / 2 + 1);
+    P->tile_cells = choose_tile(d, ng);
+    P->tiles_per_axis = ng / P->tile_cells;
+
+    auto fail = [&](int code) { destroy_plan(P); return code; };
+
+    // ---- a0: geometry (bbox over x u y on all ranks), reading Q6
+    double* mm = nullptr;
+    if (alloc((void**)&mm, sizeof(double) * 2 * kMaxD)) return fail(SK_ENOMEM);
+    {
+        double init[2 * kMaxD];
+        for (int a = 0; a < d; ++a) { init[a] = INFINITY; init[d + a] = -INFINITY; }
+        if (cudaMemcpyAsync(mm, init, sizeof(double) * 2 * d, cudaMemcpyHostToDevice, s) != cudaSuccess)
+            return fail(set_error(SK_ECUDA, "bbox init"));
+        int st = launch_bbox(x, n, d, mm, s);
+        if (!st) st = launch_bbox(y, m, d, mm, s);
+        if (!st) st = allreduce_minmax(ctx, mm, mm + d, d);
+        if (st) { cudaFree(mm); return fail(st); }
+        double h[2 * kMaxD];
+        cudaMemcpyAsync(h, mm, sizeof(double) * 2 * d, cudaMemcpyDeviceToHost, s);
+        if (cudaStreamSynchronize(s) != cudaSuccess) { cudaFree(mm); return fail(set_error(SK_ECUDA, "bbox sync")); }
+        cudaFree(mm);
+        double diag2 = 0.0;
+        bool any = true;
+        for (int a = 0; a < d; ++a) {
+            if (!isfinite(h[a]) || !isfinite(h[d + a])) any = false;
+            P->centre[a] = 0.5 * (h[a] + h[d + a]);
+            diag2 += (h[d + a] - h[a]) * (h[d + a] - h[a]);
+        }
+        if (!any) {
+            // no nodes at all, or a NaN/Inf coordinate
+            return fail(set_error(SK_EGEOMETRY, "empty node sets or non-finite coordinates"));
+        }
+        const double diag = sqrt(diag2);
+        P->rho = diag > 0.0 ? P->L / diag : 1.0;
+        P->lambda_p = lambda / (P->rho * P->rho);
+    }
+    // global counts
+    {
+        double cnt[2] = {(double)n, (double)m};
+        double* dc = nullptr;
+        if (alloc((void**)&dc, sizeof(cnt))) return fail(SK_ENOMEM);
+        cudaMemcpyAsync(dc, cnt, sizeof(cnt), cudaMemcpyHostToDevice, s);
+        int st = allreduce_sum(ctx, dc, 2);
+        cudaMemcpyAsync(cnt, dc, sizeof(cnt), cudaMemcpyDeviceToHost, s);
+        cudaStreamSynchronize(s);
+        cudaFree(dc);
+        if (st) return fail(st);
+        P->side[0].total = (long long)llround(cnt[0]);
+        P->side[1].total = (long long)llround(cnt[1]);
+    }
+    // ---- a0: scale, bin, sort (both sides)
+    int st = plan_side(*P, 0, x, n, s);
+    if (!st) st = plan_side(*P, 1, y, m, s);
+    if (st) return fail(st);
+    // ---- a1: coefficients
+    if ((st = alloc((void**)&P->D[0], sizeof(double) * P->band_size))) return fail(st);
+    if ((st = alloc((void**)&P->D[1], sizeof(double) * P->band_size))) return fail(st);
+    long long full = 1;
+    for (int a = 0; a < d; ++a) full *= (N + 1);
+    if ((st = alloc((void**)&P->bk[0], sizeof(double) * full))) return fail(st);
+    if ((st = alloc((void**)&P->bk[1], sizeof(double) * full))) return fail(st);
+    if ((st = plan_coefficients(*P, s))) return fail(st);
+    // ---- grid, spectrum, FFT plans
+    if ((st = alloc((void**)&P->grid, sizeof(double) * P->grid_size))) return fail(st);
+    if ((st = alloc((void**)&P->spec, sizeof(cufftDoubleComplex) * P->spec_size))) return fail(st);
+    {
+        int dims[3] = {ng, ng, ng};
+        cufftResult r1 = cufftPlanMany(&P->fwd, d, dims, nullptr, 1, 0, nullptr, 1, 0, CUFFT_D2Z, 1);
+        cufftResult r2 = cufftPlanMany(&P->inv, d, dims, nullptr, 1, 0, nullptr, 1, 0, CUFFT_Z2D, 1);
+        if (r1 != CUFFT_SUCCESS || r2 != CUFFT_SUCCESS)
+            return fail(set_error(SK_ECUFFT, "cufftPlanMany failed"));
+        cufftSetStream(P->fwd, s);
+        cufftSetStream(P->inv, s);
+    }
+    // ---- scratch
+    P->max_count = std::max(n, m);
+    long long mc = std::max(P->max_count, 1LL);
+    if ((st = alloc((void**)&P->w_sorted, sizeof(double) * mc))) return fail(st);
+    if ((st = alloc((void**)&P->t_sorted, sizeof(double) * mc))) return fail(st);
+    if ((st = alloc((void**)&P->a_s, sizeof(double) * std::max(n, 1LL)))) return fail(st);
+    if ((st = alloc((void**)&P->u_s, sizeof(double) * std::max(n, 1LL)))) return fail(st);
+    if ((st = alloc((void**)&P->b_s, sizeof(double) * std::max(m, 1LL)))) return fail(st);
+    if ((st = alloc((void**)&P->v_s, sizeof(double) * std::max(m, 1LL)))) return fail(st);
+    if ((st = alloc((void**)&P->red, sizeof(double) * 4096))) return fail(st);
+    if ((st = alloc((void**)&P->red_out, sizeof(double) * 8192))) return fail(st);
+    if ((st = alloc((void**)&P->flag, sizeof(int) * 4))) return fail(st);
+    if (cudaMallocHost((void**)&P->host_red, sizeof(double) * 64) != cudaSuccess)
+        return fail(set_error(SK_ENOMEM, "cudaMallocHost"));
+    *out = P;
+    return SK_OK;
+}
+
+int destroy_plan(Plan* P) {
+    if (!P) return SK_OK;
+    for (int sidx = 0; sidx < 2; ++sidx) {
+        NodeSet& S = P->side[sidx];
+        cudaFree(S.u); cudaFree(S.perm); cudaFree(S.cell_key); cudaFree(S.tile_start);
+    }
+    cudaFree(P->grid); cudaFree(P->spec);
+    for (int k = 0; k < 2; ++k) { cudaFree(P->D[k]); cudaFree(P->bk[k]); }
+    if (P->fwd) cufftDestroy(P->fwd);
+    if (P->inv) cufftDestroy(P->inv);
+    cudaFree(P->w_sorted); cudaFree(P->t_sorted);
+    cudaFree(P->a_s); cudaFree(P->b_s); cudaFree(P->u_s); cudaFree(P->v_s);
+    cudaFree(P->red); cudaFree(P->red_out); cudaFree(P->flag);
+    if (P->host_red) cudaFreeHost(P->host_red);
+    delete P;
+    return SK_OK;
+}
+
+// One fast summation on sorted data: transpose 0: sources y (side 1) -> targets x (side 0).
+int apply_sorted(Plan& P, int transpose, int kernel, const double* w_sorted, double* t_sorted) {
+    cudaStream_t s = P.ctx->stream;
+    const int src = transpose ? 0 : 1, dst = transpose ? 1 : 0;
+    prof_begin(ST_SPREAD, s);
+    SK_CUDA(cudaMemsetAsync(P.grid, 0, sizeof(double) * P.grid_size, s));
+    SK_TRY(launch_spread(P, src, w_sorted, P.grid, s));
+    prof_end(ST_SPREAD, s);
+    if (P.ctx->world > 1) {
+        prof_begin(ST_ALLREDUCE, s);
+        SK_TRY(allreduce_sum(P.ctx, P.grid, P.grid_size));
+        prof_end(ST_ALLREDUCE, s);
+    }
+    prof_begin(ST_FFT_FWD, s);
+    SK_CUFFT(cufftExecD2Z(P.fwd, P.grid, P.spec));
+    count_launch();
+    prof_end(ST_FFT_FWD, s);
+    prof_begin(ST_MULTIPLY, s);
+    SK_TRY(launch_multiply(P, kernel, s));
+    prof_end(ST_MULTIPLY, s);
+    prof_begin(ST_FFT_INV, s);
+    SK_CUFFT(cufftExecZ2D(P.inv, P.spec, P.grid));
+    count_launch();
+    prof_end(ST_FFT_INV, s);
+    prof_begin(ST_INTERP, s);
+    SK_TRY(launch_interp(P, dst, P.grid, t_sorted, s));
+    prof_end(ST_INTERP, s);
+    return SK_OK;
+}
+
+}  // namespace sk

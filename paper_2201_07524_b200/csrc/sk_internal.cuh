@@ -1,0 +1,143 @@
+// sk_internal.cuh -- internal types of libsk_nfft (B200 / sm_100a).
+// Product code: shares nothing with oracle/ (see DESIGN.md "Boundary").
+#pragma once
+
+#include <cuda_runtime.h>
+#include <cufft.h>
+#include <stdint.h>
+#include <string>
+
+#include "../../include/sinkhorn_nfft.h"
+
+namespace sk {
+
+constexpr int kMaxD = 3;
+constexpr int kMaxW = 16;            // 2 * m_w taps per axis, m_w <= 8
+
+// Thread-local error message + status helpers (api.cu).
+int set_error(int code, const std::string& msg);
+#define SK_CUDA(call)                                                                  \
+    do {                                                                               \
+        cudaError_t e_ = (call);                                                       \
+        if (e_ != cudaSuccess)                                                         \
+            return ::sk::set_error(SK_ECUDA, std::string(#call) + ": " + cudaGetErrorString(e_)); \
+    } while (0)
+#define SK_CUFFT(call)                                                                 \
+    do {                                                                               \
+        cufftResult r_ = (call);                                                       \
+        if (r_ != CUFFT_SUCCESS)                                                       \
+            return ::sk::set_error(SK_ECUFFT, std::string(#call) + ": cufft error " + std::to_string((int)r_)); \
+    } while (0)
+#define SK_TRY(call)                                                                   \
+    do { int s_ = (call); if (s_ != SK_OK) return s_; } while (0)
+
+void count_launch(long long k = 1);
+
+// Kaiser-Bessel window parameters in oversampled-grid units (reading Q10).
+struct Window {
+    int m;            // cutoff: support |u| < m, 2m taps per axis
+    double beta;      // pi (2 - 1/sigma)
+    double m2;        // m*m
+    double inv_pi;    // 1/pi
+};
+
+// One node set (x or y) of the local rank, sorted by tile key.
+struct NodeSet {
+    long long count = 0;      // local nodes
+    long long total = 0;      // nodes over all ranks
+    double* u = nullptr;      // [d][count] grid coordinates n*(x'_a + 1/2), sorted order (SoA)
+    int* perm = nullptr;      // [count] sorted position -> caller index
+    int* cell_key = nullptr;  // [count] sort key (scratch after plan)
+    // tile decomposition (bins) for the tiled spread/gather kernels
+    int* tile_start = nullptr;   // [ntiles + 1] CSR offsets into the sorted order
+    int ntiles = 0;
+};
+
+struct Ctx {
+    int device = 0;
+    int rank = 0;
+    int world = 1;
+    cudaStream_t stream = nullptr;
+    void* nccl_comm = nullptr;    // ncclComm_t when world > 1
+};
+
+struct Plan {
+    Ctx* ctx = nullptr;
+    int d = 0;
+    int N = 0;                // bandwidth per axis
+    int n = 0;                // oversampled grid per axis (sigma N)
+    double sigma = 2.0;
+    Window win{};
+    double lambda = 0, lambda_p = 0, rho = 1, L = 0, eps_B = 0;
+    int p_smooth = 8;
+    double centre[kMaxD] = {0, 0, 0};
+    long long grid_size = 0;  // n^d
+    long long spec_size = 0;  // n^{d-1} (n/2 + 1)
+    long long band_size = 0;  // (N+1)^{d-1} (N/2 + 1)
+    NodeSet side[2];          // 0 = x (targets of K v), 1 = y (sources of K v)
+    double* grid = nullptr;             // [n^d] real
+    cufftDoubleComplex* spec = nullptr; // [spec_size]
+    double* D[2] = {nullptr, nullptr};  // multiplier tables (kernel 0, 1) over the half band
+    double* bk[2] = {nullptr, nullptr}; // b_k on the full band (N+1)^d (diagnostics)
+    cufftHandle fwd = 0, inv = 0;
+    // scratch
+    double* w_sorted = nullptr;   // [max count]
+    double* t_sorted = nullptr;   // [max count]
+    double* red = nullptr;        // block partials
+    double* red_out = nullptr;    // reduced scalars (device)
+    double* host_red = nullptr;   // pinned host mirror
+    int* flag = nullptr;          // device error flag / first bad index
+    // Sinkhorn state in sorted order
+    double* a_s = nullptr; double* b_s = nullptr; double* u_s = nullptr; double* v_s = nullptr;
+    long long max_count = 0;
+    int tile_cells = 0;       // tile edge in grid cells (per axis)
+    int tiles_per_axis = 0;
+};
+
+// ---- kernels.cu launchers ----
+int launch_bbox(const double* pts, long long count, int d, double* out_minmax /*device [2*d]*/,
+                cudaStream_t s);
+int launch_scale_key(Plan& P, const double* pts, long long count, double* u_unsorted,
+                     int* key, int* idx, int* bad, cudaStream_t s);
+int launch_gather_coords(Plan& P, const double* u_unsorted, const int* perm, long long count,
+                         double* u_sorted, cudaStream_t s);
+int launch_tile_offsets(const int* sorted_keys, long long count, int ntiles, int* tile_start,
+                        cudaStream_t s);
+int launch_spread(Plan& P, int side, const double* w_sorted, double* grid, cudaStream_t s);
+int launch_interp(Plan& P, int side, const double* grid, double* t_sorted, cudaStream_t s);
+int launch_multiply(Plan& P, int kernel, cudaStream_t s);
+int launch_permute_in(const double* src, const int* perm, long long count, double* dst, cudaStream_t s);
+int launch_permute_out(const double* src, const int* perm, long long count, double* dst, cudaStream_t s);
+int launch_sample_kernel(Plan& P, int kernel, int M, const double* kb_coef, int kb_deg,
+                         double* out, cudaStream_t s);
+int launch_band_coeffs(Plan& P, int kernel, int M, const cufftDoubleComplex* B, cudaStream_t s);
+// Sinkhorn fused update: x_s <- p_s / t (t = interpolated), partial sums into red
+int launch_update(Plan& P, int side, const double* t_sorted, const double* p_sorted,
+                  double* x_sorted, int want_resid, int iter, cudaStream_t s);
+int launch_fill(double* p, long long count, double v, cudaStream_t s);
+int launch_scale_vec(double* p, long long count, const double* scale_dev, cudaStream_t s);
+int launch_reduce_sum_log(const double* p, const double* x, long long count, double* out_dev,
+                          int op, cudaStream_t s);
+int launch_rescale_factor(double* r, int policy, double total, cudaStream_t s);
+int launch_finalize_partials(const double* red, int nparts, int nvals, double* out, cudaStream_t s);
+
+// ---- plan.cu ----
+int build_plan(Ctx* ctx, Plan** out, int d, const double* x, long long n, const double* y,
+               long long m, double lambda, int N, double sigma, int m_w, double eps_B, int p);
+int destroy_plan(Plan* P);
+int apply_sorted(Plan& P, int transpose, int kernel, const double* w_sorted, double* t_sorted);
+
+// ---- stage profiling (api.cu): CUDA-event pairs around each stage when enabled ----
+enum Stage { ST_SPREAD = 0, ST_ALLREDUCE, ST_FFT_FWD, ST_MULTIPLY, ST_FFT_INV, ST_INTERP, ST_UPDATE, ST_COUNT };
+void prof_begin(int stage, cudaStream_t s);
+void prof_end(int stage, cudaStream_t s);
+void prof_harvest();
+
+// ---- comm (api.cu) ----
+int allreduce_sum(Ctx* c, double* buf, long long count);           // in-place, device
+int allreduce_minmax(Ctx* c, double* mins, double* maxs, int count); // in-place, device
+
+}  // namespace sk
+
+struct sk_ctx { sk::Ctx c; };
+struct sk_plan { sk::Plan* p; };

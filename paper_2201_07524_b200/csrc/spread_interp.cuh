@@ -1,0 +1,115 @@
+// spread_interp.cuh -- adjoint-NFFT gridding (spread) and NFFT interpolation (interp).
+//
+//   spread: g[l] += w_j prod_a phi(u_ja - l_a)      over the 2m taps per axis of node j
+//   interp: t_j   = sum_l g[l] prod_a phi(u_ja - l_a)
+// u = n (x' + 1/2) is the node's grid coordinate; with |x'| <= 1/4 - eps_B/2 and
+// n >= 4m no tap wraps around the torus (checked in plan.cu), so indices are direct.
+//
+// v1 (this file): one thread per node, window values evaluated on the fly; spread
+// accumulates with FP64 atomics into the global grid, interp reads it through L1/L2.
+#pragma once
+#include "sk_internal.cuh"
+#include "window.cuh"
+
+namespace sk {
+
+template <int D>
+__global__ void spread_v1_kernel(const double* __restrict__ u, long long count,
+                                 const double* __restrict__ w, Window win, int n,
+                                 double* __restrict__ grid) {
+    const int W = 2 * win.m;
+    for (long long j = blockIdx.x * (long long)blockDim.x + threadIdx.x; j < count;
+         j += (long long)gridDim.x * blockDim.x) {
+        double phi[D][kMaxW];
+        int base[D];
+        for (int a = 0; a < D; ++a) base[a] = kb_taps(u[a * count + j], win, phi[a]) - win.m + 1;
+        const double wj = w[j];
+        if (D == 1) {
+            for (int t0 = 0; t0 < W; ++t0) atomicAdd(&grid[base[0] + t0], wj * phi[0][t0]);
+        } else if (D == 2) {
+            for (int t0 = 0; t0 < W; ++t0) {
+                const double w0 = wj * phi[0][t0];
+                double* row = grid + (long long)(base[0] + t0) * n + base[1];
+                for (int t1 = 0; t1 < W; ++t1) atomicAdd(&row[t1], w0 * phi[D - 1][t1]);
+            }
+        } else {
+            for (int t0 = 0; t0 < W; ++t0) {
+                const double w0 = wj * phi[0][t0];
+                for (int t1 = 0; t1 < W; ++t1) {
+                    const double w1 = w0 * phi[1][t1];
+                    double* row = grid + ((long long)(base[0] + t0) * n + (base[1] + t1)) * n + base[D - 1];
+                    for (int t2 = 0; t2 < W; ++t2) atomicAdd(&row[t2], w1 * phi[D - 1][t2]);
+                }
+            }
+        }
+    }
+}
+
+template <int D>
+__global__ void interp_v1_kernel(const double* __restrict__ u, long long count, Window win, int n,
+                                 const double* __restrict__ grid, double* __restrict__ t) {
+    const int W = 2 * win.m;
+    for (long long j = blockIdx.x * (long long)blockDim.x + threadIdx.x; j < count;
+         j += (long long)gridDim.x * blockDim.x) {
+        double phi[D][kMaxW];
+        int base[D];
+        for (int a = 0; a < D; ++a) base[a] = kb_taps(u[a * count + j], win, phi[a]) - win.m + 1;
+        double acc = 0.0;
+        if (D == 1) {
+            for (int t0 = 0; t0 < W; ++t0) acc += phi[0][t0] * __ldg(&grid[base[0] + t0]);
+        } else if (D == 2) {
+            for (int t0 = 0; t0 < W; ++t0) {
+                const double* row = grid + (long long)(base[0] + t0) * n + base[1];
+                double s = 0.0;
+                for (int t1 = 0; t1 < W; ++t1) s += phi[D - 1][t1] * __ldg(&row[t1]);
+                acc += phi[0][t0] * s;
+            }
+        } else {
+            for (int t0 = 0; t0 < W; ++t0) {
+                double s1 = 0.0;
+                for (int t1 = 0; t1 < W; ++t1) {
+                    const double* row = grid + ((long long)(base[0] + t0) * n + (base[1] + t1)) * n + base[D - 1];
+                    double s2 = 0.0;
+                    for (int t2 = 0; t2 < W; ++t2) s2 += phi[D - 1][t2] * __ldg(&row[t2]);
+                    s1 += phi[1][t1] * s2;
+                }
+                acc += phi[0][t0] * s1;
+            }
+        }
+        t[j] = acc;
+    }
+}
+
+inline int v1_grid(long long count) {
+    long long g = (count + 127) / 128;
+    if (g > 148LL * 32) g = 148LL * 32;
+    return (int)(g < 1 ? 1 : g);
+}
+
+inline int spread_dispatch(Plan& P, const NodeSet& S, const double* w, double* grid, cudaStream_t s) {
+    const int g = v1_grid(S.count);
+    switch (P.d) {
+        case 1: spread_v1_kernel<1><<<g, 128, 0, s>>>(S.u, S.count, w, P.win, P.n, grid); break;
+        case 2: spread_v1_kernel<2><<<g, 128, 0, s>>>(S.u, S.count, w, P.win, P.n, grid); break;
+        default: spread_v1_kernel<3><<<g, 128, 0, s>>>(S.u, S.count, w, P.win, P.n, grid); break;
+    }
+    count_launch();
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return set_error(SK_ECUDA, std::string("spread: ") + cudaGetErrorString(e));
+    return SK_OK;
+}
+
+inline int interp_dispatch(Plan& P, const NodeSet& S, const double* grid, double* t, cudaStream_t s) {
+    const int g = v1_grid(S.count);
+    switch (P.d) {
+        case 1: interp_v1_kernel<1><<<g, 128, 0, s>>>(S.u, S.count, P.win, P.n, grid, t); break;
+        case 2: interp_v1_kernel<2><<<g, 128, 0, s>>>(S.u, S.count, P.win, P.n, grid, t); break;
+        default: interp_v1_kernel<3><<<g, 128, 0, s>>>(S.u, S.count, P.win, P.n, grid, t); break;
+    }
+    count_launch();
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return set_error(SK_ECUDA, std::string("interp: ") + cudaGetErrorString(e));
+    return SK_OK;
+}
+
+}  // namespace sk

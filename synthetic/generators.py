@@ -154,7 +154,7 @@ def check_rows(cfg_index: int, count: int, total: int, seed: int = 0):
     return np.sort(g.choice(total, size=count, replace=False)).astype(np.int64)
 
 
-def test_weights(cfg_index: int, count: int, seed: int = 0):
+def uniform_test_weights(cfg_index: int, count: int, seed: int = 0):
     """Seeded U(0,1) weights for matvec checks."""
     return rng(cfg_index, STREAM_W, seed).random(count)
 

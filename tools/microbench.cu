@@ -1,0 +1,171 @@
+// microbench.cu -- FP64 throughput probes on B200 (sm_100a) that set the roofline of the
+// FP64-bound spread/interp kernels:
+//   dfma   : FP64 FMA (vector pipe), 8 independent chains per thread
+//   dmma   : FP64 tensor-core MMA mma.sync m8n8k4 and m16n8k4/k8/k16 (.f64)
+//   atoms  : shared-memory FP64 atomicAdd, distinct addresses per lane
+//   redg   : global FP64 atomicAdd (RED) to scattered addresses in a 16 MB grid
+// Build: nvcc -O3 -gencode arch=compute_100a,code=sm_100a -o build/microbench tools/microbench.cu
+#include <cstdio>
+#include <cuda_runtime.h>
+
+#define CK(x) do { cudaError_t e = (x); if (e != cudaSuccess) { printf("CUDA %s at %d\n", cudaGetErrorString(e), __LINE__); return 1; } } while (0)
+
+__global__ void dfma_kernel(double* out, int iters, double a, double b) {
+    double c0 = threadIdx.x, c1 = c0 + 1, c2 = c0 + 2, c3 = c0 + 3, c4 = c0 + 4, c5 = c0 + 5, c6 = c0 + 6, c7 = c0 + 7;
+    for (int i = 0; i < iters; ++i) {
+#pragma unroll
+        for (int k = 0; k < 16; ++k) {
+            c0 = fma(c0, a, b); c1 = fma(c1, a, b); c2 = fma(c2, a, b); c3 = fma(c3, a, b);
+            c4 = fma(c4, a, b); c5 = fma(c5, a, b); c6 = fma(c6, a, b); c7 = fma(c7, a, b);
+        }
+    }
+    out[blockIdx.x * blockDim.x + threadIdx.x] = c0 + c1 + c2 + c3 + c4 + c5 + c6 + c7;
+}
+
+__global__ void dmma884_kernel(double* out, int iters) {
+    double a = threadIdx.x * 1e-3, b = 1.0 - threadIdx.x * 1e-4;
+    double c[4][2] = {};
+    for (int i = 0; i < iters; ++i) {
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+                         : "+d"(c[k][0]), "+d"(c[k][1]) : "d"(a), "d"(b));
+        }
+    }
+    double s = 0;
+    for (int k = 0; k < 4; ++k) s += c[k][0] + c[k][1];
+    out[blockIdx.x * blockDim.x + threadIdx.x] = s;
+}
+
+__global__ void dmma1684_kernel(double* out, int iters) {
+    double a0 = threadIdx.x * 1e-3, a1 = a0 + 1e-3, b = 1.0 - threadIdx.x * 1e-4;
+    double c[4][4] = {};
+    for (int i = 0; i < iters; ++i) {
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            asm volatile("mma.sync.aligned.m16n8k4.row.col.f64.f64.f64.f64 {%0,%1,%2,%3}, {%4,%5}, {%6}, {%0,%1,%2,%3};"
+                         : "+d"(c[k][0]), "+d"(c[k][1]), "+d"(c[k][2]), "+d"(c[k][3]) : "d"(a0), "d"(a1), "d"(b));
+        }
+    }
+    double s = 0;
+    for (int k = 0; k < 4; ++k) s += c[k][0] + c[k][1] + c[k][2] + c[k][3];
+    out[blockIdx.x * blockDim.x + threadIdx.x] = s;
+}
+
+__global__ void dmma16816_kernel(double* out, int iters) {
+    double a[8], b[4];
+    for (int k = 0; k < 8; ++k) a[k] = (threadIdx.x + k) * 1e-3;
+    for (int k = 0; k < 4; ++k) b[k] = 1.0 - (threadIdx.x + k) * 1e-4;
+    double c[2][4] = {};
+    for (int i = 0; i < iters; ++i) {
+#pragma unroll
+        for (int k = 0; k < 2; ++k) {
+            asm volatile("mma.sync.aligned.m16n8k16.row.col.f64.f64.f64.f64 {%0,%1,%2,%3}, {%4,%5,%6,%7,%8,%9,%10,%11}, {%12,%13,%14,%15}, {%0,%1,%2,%3};"
+                         : "+d"(c[k][0]), "+d"(c[k][1]), "+d"(c[k][2]), "+d"(c[k][3])
+                         : "d"(a[0]), "d"(a[1]), "d"(a[2]), "d"(a[3]), "d"(a[4]), "d"(a[5]), "d"(a[6]), "d"(a[7]),
+                           "d"(b[0]), "d"(b[1]), "d"(b[2]), "d"(b[3]));
+        }
+    }
+    double s = 0;
+    for (int k = 0; k < 2; ++k) s += c[k][0] + c[k][1] + c[k][2] + c[k][3];
+    out[blockIdx.x * blockDim.x + threadIdx.x] = s;
+}
+
+__global__ void atoms_kernel(double* out, int iters) {
+    __shared__ double sh[4096];
+    for (int i = threadIdx.x; i < 4096; i += blockDim.x) sh[i] = 0;
+    __syncthreads();
+    const int base = (threadIdx.x * 33) & 4095;
+    for (int i = 0; i < iters; ++i) {
+#pragma unroll
+        for (int k = 0; k < 8; ++k) atomicAdd(&sh[(base + k * 128 + i) & 4095], 1.0);
+    }
+    __syncthreads();
+    out[blockIdx.x * blockDim.x + threadIdx.x] = sh[threadIdx.x];
+}
+
+__global__ void lds_bcast_kernel(double* out, int iters) {
+    __shared__ double sh[1024];
+    for (int i = threadIdx.x; i < 1024; i += blockDim.x) sh[i] = i * 1e-3;
+    __syncthreads();
+    double acc = 0, acc2 = 0;
+    for (int i = 0; i < iters; ++i) {
+#pragma unroll
+        for (int k = 0; k < 16; ++k) {
+            double2 v = *reinterpret_cast<const double2*>(&sh[((i * 16 + k) * 2) & 1023]);
+            acc = fma(acc, v.x, 1e-9);
+            acc2 = fma(acc2, v.y, 1e-9);
+        }
+    }
+    out[blockIdx.x * blockDim.x + threadIdx.x] = acc + acc2;
+}
+
+__global__ void redg_kernel(double* grid, long long gsize, int iters) {
+    unsigned long long h = (blockIdx.x * 1315423911ull + threadIdx.x * 2654435761ull);
+    for (int i = 0; i < iters; ++i) {
+        h = h * 6364136223846793005ull + 1442695040888963407ull;
+        long long base = (h >> 20) % (gsize - 64);
+        atomicAdd(&grid[base + (threadIdx.x & 31)], 1.0);
+    }
+}
+
+template <typename F>
+float timeit(F f) {
+    cudaEvent_t a, b;
+    cudaEventCreate(&a); cudaEventCreate(&b);
+    f();
+    cudaDeviceSynchronize();
+    cudaEventRecord(a);
+    f();
+    cudaEventRecord(b);
+    cudaEventSynchronize(b);
+    float ms; cudaEventElapsedTime(&ms, a, b);
+    return ms;
+}
+
+int main() {
+    cudaDeviceProp p; CK(cudaGetDeviceProperties(&p, 0));
+    int clk = 0; cudaDeviceGetAttribute(&clk, cudaDevAttrClockRate, 0);
+    printf("device %s SMs %d clock(kHz) %d\n", p.name, p.multiProcessorCount, clk);
+    const int blocks = p.multiProcessorCount * 8, threads = 256;
+    double* out; CK(cudaMalloc(&out, sizeof(double) * blocks * threads));
+    {
+        int iters = 4096;
+        float ms = timeit([&] { dfma_kernel<<<blocks, threads>>>(out, iters, 0.999999, 1e-7); });
+        double fl = 2.0 * 8 * 16 * (double)iters * blocks * threads;
+        printf("dfma: %.2f TFLOP/s  (%.1f FMA/clk/SM at %d MHz)\n", fl / ms / 1e9, fl / 2 / (ms * 1e-3) / p.multiProcessorCount / (clk * 1e3), clk / 1000);
+    }
+    {
+        int iters = 4096;
+        float ms = timeit([&] { dmma884_kernel<<<blocks, threads>>>(out, iters); });
+        double fl = 2.0 * 256 * 4 * (double)iters * blocks * (threads / 32);
+        printf("dmma m8n8k4: %.2f TFLOP/s\n", fl / ms / 1e9);
+        ms = timeit([&] { dmma1684_kernel<<<blocks, threads>>>(out, iters); });
+        fl = 2.0 * 512 * 4 * (double)iters * blocks * (threads / 32);
+        printf("dmma m16n8k4: %.2f TFLOP/s\n", fl / ms / 1e9);
+        ms = timeit([&] { dmma16816_kernel<<<blocks, threads>>>(out, iters); });
+        fl = 2.0 * 2048 * 2 * (double)iters * blocks * (threads / 32);
+        printf("dmma m16n8k16: %.2f TFLOP/s\n", fl / ms / 1e9);
+    }
+    {
+        int iters = 2048;
+        float ms = timeit([&] { atoms_kernel<<<blocks, threads>>>(out, iters); });
+        double ops = 8.0 * iters * blocks * threads;
+        printf("smem f64 atomicAdd: %.1f Gop/s (%.2f per clk per SM)\n", ops / ms / 1e6, ops / (ms * 1e-3) / p.multiProcessorCount / (clk * 1e3));
+        ms = timeit([&] { lds_bcast_kernel<<<blocks, threads>>>(out, iters); });
+        ops = 16.0 * iters * blocks * threads;
+        printf("LDS.128 broadcast + 2 DFMA: %.1f G lane-loads/s (%.2f warp-LDS per clk per SM)\n", ops / ms / 1e6, ops / 32 / (ms * 1e-3) / p.multiProcessorCount / (clk * 1e3));
+    }
+    {
+        long long gs = 1 << 21;
+        double* g; CK(cudaMalloc(&g, sizeof(double) * gs));
+        cudaMemset(g, 0, sizeof(double) * gs);
+        int iters = 256;
+        float ms = timeit([&] { redg_kernel<<<blocks, threads>>>(g, gs, iters); });
+        double ops = (double)iters * blocks * threads;
+        printf("global f64 RED (16 MB grid, 32 contiguous per warp): %.1f Gop/s\n", ops / ms / 1e6);
+        cudaFree(g);
+    }
+    CK(cudaDeviceSynchronize());
+    return 0;
+}
