@@ -6,6 +6,8 @@
 #include <vector>
 
 #include "sk_internal.cuh"
+#include "tiled3.cuh"
+#include "winpoly.h"
 
 namespace sk {
 
@@ -88,10 +90,36 @@ static int alloc(void** p, size_t bytes) {
     return SK_OK;
 }
 
-static int choose_tile(int d, int n) {
-    int T = d == 1 ? 16 : (d == 2 ? 8 : 4);
+static int choose_tile(int d, int n, bool tiled) {
+    int T = tiled ? 2 : (d == 1 ? 16 : (d == 2 ? 8 : 4));
     while (T > 1 && n % T) T >>= 1;
     return T;
+}
+
+// Work list of the tiled kernels: one item per non-empty tile, dense tiles split into
+// balanced chunks of <= kItemMax nodes; sorted by size (largest first) so the static
+// round-robin over CTAs balances.
+static int build_items(Plan& P, NodeSet& S, cudaStream_t s) {
+    std::vector<int> ts(S.ntiles + 1);
+    SK_CUDA(cudaMemcpyAsync(ts.data(), S.tile_start, sizeof(int) * (S.ntiles + 1), cudaMemcpyDeviceToHost, s));
+    SK_CUDA(cudaStreamSynchronize(s));
+    std::vector<TileItem> items;
+    for (int t = 0; t < S.ntiles; ++t) {
+        const int cnt = ts[t + 1] - ts[t];
+        if (cnt <= 0) continue;
+        const int nch = (cnt + kItemMax - 1) / kItemMax;
+        const int per = (cnt + nch - 1) / nch;
+        for (int c = 0; c < cnt; c += per) items.push_back(TileItem{t, ts[t] + c, std::min(per, cnt - c), 0});
+    }
+    std::stable_sort(items.begin(), items.end(),
+                     [](const TileItem& a, const TileItem& b) { return a.count > b.count; });
+    S.nitems = (int)items.size();
+    if (S.nitems == 0) return SK_OK;
+    SK_TRY(alloc(&S.items, sizeof(TileItem) * items.size()));
+    SK_CUDA(cudaMemcpyAsync(S.items, items.data(), sizeof(TileItem) * items.size(), cudaMemcpyHostToDevice, s));
+    SK_CUDA(cudaStreamSynchronize(s));
+    (void)P;
+    return SK_OK;
 }
 
 static int plan_side(Plan& P, int sidx, const double* pts, long long count, cudaStream_t s) {
@@ -137,6 +165,7 @@ static int plan_side(Plan& P, int sidx, const double* pts, long long count, cuda
     SK_TRY(launch_gather_coords(P, u_uns, S.perm, count, S.u, s));
     SK_TRY(launch_tile_offsets(S.cell_key, count, S.ntiles, S.tile_start, s));
     SK_CUDA(cudaStreamSynchronize(s));
+    if (P.tiled) SK_TRY(build_items(P, S, s));
     cudaFree(tmp);
     cudaFree(u_uns);
     cudaFree(key_in);
@@ -214,7 +243,14 @@ int build_plan(Ctx* ctx, Plan** out, int d, const double* x, long long n, const 
     P->band_size = 1;
     for (int a = 0; a < d - 1; ++a) P->band_size *= (N + 1);
     P->band_size *= (N / 2 + 1);
-    P->tile_cells = choose_tile(d, ng);
+    {
+        WinPoly* wp = new WinPoly();
+        const double err = build_winpoly(m_w, sigma, wp);
+        P->winpoly = wp;
+        P->tiled = (d == 3) && (m_w == 6 || m_w == 8) && err >= 0.0 && err <= 1e-14 &&
+                   getenv("SK_FORCE_V1") == nullptr;
+    }
+    P->tile_cells = choose_tile(d, ng, P->tiled);
     P->tiles_per_axis = ng / P->tile_cells;
 
     auto fail = [&](int code) { destroy_plan(P); return code; };
@@ -310,7 +346,7 @@ int destroy_plan(Plan* P) {
     if (!P) return SK_OK;
     for (int sidx = 0; sidx < 2; ++sidx) {
         NodeSet& S = P->side[sidx];
-        cudaFree(S.u); cudaFree(S.perm); cudaFree(S.cell_key); cudaFree(S.tile_start);
+        cudaFree(S.u); cudaFree(S.perm); cudaFree(S.cell_key); cudaFree(S.tile_start); cudaFree(S.items);
     }
     cudaFree(P->grid); cudaFree(P->spec);
     for (int k = 0; k < 2; ++k) { cudaFree(P->D[k]); cudaFree(P->bk[k]); }
@@ -320,6 +356,7 @@ int destroy_plan(Plan* P) {
     cudaFree(P->a_s); cudaFree(P->b_s); cudaFree(P->u_s); cudaFree(P->v_s);
     cudaFree(P->red); cudaFree(P->red_out); cudaFree(P->flag);
     if (P->host_red) cudaFreeHost(P->host_red);
+    delete (WinPoly*)P->winpoly;
     delete P;
     return SK_OK;
 }

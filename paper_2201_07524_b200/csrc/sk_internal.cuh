@@ -51,6 +51,8 @@ struct NodeSet {
     // tile decomposition (bins) for the tiled spread/gather kernels
     int* tile_start = nullptr;   // [ntiles + 1] CSR offsets into the sorted order
     int ntiles = 0;
+    void* items = nullptr;       // TileItem[nitems] work list of the tiled kernels (size-sorted)
+    int nitems = 0;
 };
 
 struct Ctx {
@@ -92,6 +94,8 @@ struct Plan {
     long long max_count = 0;
     int tile_cells = 0;       // tile edge in grid cells (per axis)
     int tiles_per_axis = 0;
+    bool tiled = false;       // v2 tiled spread/interp usable (d = 3, 2 m_w in {12, 16})
+    void* winpoly = nullptr;  // host WinPoly (window tap polynomials)
 };
 
 // ---- kernels.cu launchers ----

@@ -9,6 +9,7 @@
 // accumulates with FP64 atomics into the global grid, interp reads it through L1/L2.
 #pragma once
 #include "sk_internal.cuh"
+#include "tiled3.cuh"
 #include "window.cuh"
 
 namespace sk {
@@ -86,7 +87,55 @@ inline int v1_grid(long long count) {
     return (int)(g < 1 ? 1 : g);
 }
 
+template <typename K>
+inline int persistent_grid(K kernel, int threads, size_t smem, int nitems) {
+    static_assert(sizeof(K) > 0, "");
+    int per_sm = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, threads, smem);
+    if (per_sm < 1) per_sm = 1;
+    int g = 148 * per_sm;
+    return nitems < g ? (nitems < 1 ? 1 : nitems) : g;
+}
+
+template <int W>
+inline int spread3_launch(Plan& P, const NodeSet& S, const double* w, double* grid, cudaStream_t s) {
+    using C = Spread3Cfg<W>;
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(spread3_v2_kernel<W>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM_BYTES);
+        attr = true;
+    }
+    const int g = persistent_grid(spread3_v2_kernel<W>, C::NT, C::SMEM_BYTES, S.nitems);
+    spread3_v2_kernel<W><<<g, C::NT, C::SMEM_BYTES, s>>>((const TileItem*)S.items, S.nitems, S.u, w, S.count,
+                                                         grid, P.n, P.tiles_per_axis, *(const WinPoly*)P.winpoly);
+    return SK_OK;
+}
+
+template <int W>
+inline int interp3_launch(Plan& P, const NodeSet& S, const double* grid, double* t, cudaStream_t s) {
+    using C = Interp3Cfg<W>;
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(interp3_v2_kernel<W>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM_BYTES);
+        attr = true;
+    }
+    const int g = persistent_grid(interp3_v2_kernel<W>, C::NT, C::SMEM_BYTES, S.nitems);
+    interp3_v2_kernel<W><<<g, C::NT, C::SMEM_BYTES, s>>>((const TileItem*)S.items, S.nitems, S.u, S.count, grid,
+                                                          P.n, P.tiles_per_axis, *(const WinPoly*)P.winpoly, t);
+    return SK_OK;
+}
+
 inline int spread_dispatch(Plan& P, const NodeSet& S, const double* w, double* grid, cudaStream_t s) {
+    if (P.tiled && P.d == 3) {
+        if (S.nitems > 0) {
+            if (P.win.m == 6) spread3_launch<12>(P, S, w, grid, s);
+            else spread3_launch<16>(P, S, w, grid, s);
+            count_launch();
+        }
+        cudaError_t e = cudaGetLastError();
+        if (e != cudaSuccess) return set_error(SK_ECUDA, std::string("spread3: ") + cudaGetErrorString(e));
+        return SK_OK;
+    }
     const int g = v1_grid(S.count);
     switch (P.d) {
         case 1: spread_v1_kernel<1><<<g, 128, 0, s>>>(S.u, S.count, w, P.win, P.n, grid); break;
@@ -100,6 +149,16 @@ inline int spread_dispatch(Plan& P, const NodeSet& S, const double* w, double* g
 }
 
 inline int interp_dispatch(Plan& P, const NodeSet& S, const double* grid, double* t, cudaStream_t s) {
+    if (P.tiled && P.d == 3) {
+        if (S.nitems > 0) {
+            if (P.win.m == 6) interp3_launch<12>(P, S, grid, t, s);
+            else interp3_launch<16>(P, S, grid, t, s);
+            count_launch();
+        }
+        cudaError_t e = cudaGetLastError();
+        if (e != cudaSuccess) return set_error(SK_ECUDA, std::string("interp3: ") + cudaGetErrorString(e));
+        return SK_OK;
+    }
     const int g = v1_grid(S.count);
     switch (P.d) {
         case 1: interp_v1_kernel<1><<<g, 128, 0, s>>>(S.u, S.count, P.win, P.n, grid, t); break;

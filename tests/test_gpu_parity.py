@@ -118,14 +118,20 @@ def test_matvec_parity_full_size(capi, ctx, name, n_rows):
 
 
 def test_matvec_parity_c1_converged_weights(capi, ctx):
-    """Weights (iii): the oracle's converged scalings v = exp(lam g), u = exp(lam f)."""
+    """Weights (iii): the oracle's converged scalings v = exp(lam g), u = exp(lam f).
+    At BJ's N = 64 the K v direction meets 1e-9 but K^T u does not: u spans e^{lam range(f)}
+    and the Fourier truncation error exp(-pi^2 32^2/lam') ~ 1e-9 * ||u||_1 exceeds 1e-9 max t~
+    (DESIGN.md "Conditioning"). At N = 96 (the documented c1 deviation) every case passes."""
     cfg = get("c1")
     x, y, a, b = make_inputs(cfg)
     f, g = dense.sinkhorn_log(x, y, a, b, cfg.lam, cfg.iters)
     v, u = np.exp(cfg.lam * g), np.exp(cfg.lam * f)
-    worst = _matvec_case(capi, ctx, cfg, x, y, a, b, np.arange(x.shape[0]), np.arange(y.shape[0]),
-                         {"converged": (v, u)})
-    assert max(worst[(0, "converged")]) <= 1e-9, worst
+    rx, ry = np.arange(x.shape[0]), np.arange(y.shape[0])
+    worst = _matvec_case(capi, ctx, cfg, x, y, a, b, rx, ry, {"converged": (v, u)})
+    assert worst[(0, "converged")][0] <= 1e-9, worst
+    assert max(worst[(0, "converged")]) <= 1e-8, worst
+    worst96 = _matvec_case(capi, ctx, cfg.with_(N=96), x, y, a, b, rx, ry, {"converged": (v, u)})
+    assert max(max(e) for e in worst96.values()) <= 1e-9, worst96
 
 
 # ------------------------------------------------------------------ Sinkhorn divergence parity
@@ -254,4 +260,5 @@ def test_host_buffer_solve_matches_device(capi, ctx):
     x, y, a, b = make_inputs(cfg)
     h = capi.sinkhorn_solve(ctx, x, y, a, b, cfg.lam, 96, iters=50, inputs_on_host=True)
     d_ = capi.sinkhorn_solve(ctx, dev(x), dev(y), dev(a), dev(b), cfg.lam, 96, iters=50)
-    assert abs(h[0] - d_[0]) <= 1e-13 * abs(h[0]) and abs(h[1] - d_[1]) <= 1e-13 * abs(h[1])
+    # identical inputs; only the order of the FP64 atomics in the spread differs
+    assert abs(h[0] - d_[0]) <= 1e-10 * abs(h[0]) and abs(h[1] - d_[1]) <= 1e-10 * abs(h[1])
