@@ -5,18 +5,19 @@
 // region of R = T + W - 1 cells per axis (W = 2 m taps per axis), so
 //
 //   interp: the CTA stages the region of the grid in shared memory (R^3 doubles, one
-//           coalesced load per item), lanes = nodes (2 per lane), the per-node window
-//           values live in registers (z) and lane-private shared rows (x, y) over the whole
-//           region (zeros outside the node's 2m support), and the region loop is
-//           warp-uniform: every grid value is a broadcast LDS.128 feeding 4 DFMAs.
+//           coalesced load per item); lanes = nodes (2 per lane); a node's window values
+//           over the whole region (zeros outside its 2m support) live in registers (z) and
+//           in lane-private shared rows (x, y); the region loop is warp-uniform, so every
+//           grid value is one broadcast LDS.128 feeding 4 DFMAs.
 //   spread: lanes own 2 region columns (x,y) of R z-values in registers; per chunk of 64
 //           nodes the CTA tabulates w*phi_x, phi_y, phi_z in shared memory (lanes = nodes),
 //           then loops over the nodes (warp-uniform) with a broadcast phi_z row: per node
 //           and lane 2 DMUL + 2R DFMA. The region is flushed once per item with coalesced
 //           FP64 atomics (RED) into the global grid (neighbouring regions overlap).
 //
-// Window values come from the degree-14 tap polynomials of winpoly.h (compile-time indices
-// into a __grid_constant__ parameter -> constant-bank operands).
+// Window taps: degree-14 polynomials of winpoly.h. The window is even, so tap W-1-t at
+// g = f - 1/2 is tap t at -g: with p_t(g) = E_t(g^2) + g O_t(g^2) one pair of taps costs
+// 15 DFMA. The W/2 coefficient rows sit in shared memory (broadcast LDS.128).
 #pragma once
 #include "sk_internal.cuh"
 #include "winpoly.h"
@@ -31,42 +32,66 @@ struct TileItem {
 };
 
 constexpr int kItemMax = 4096;  // nodes per work item (dense tiles are split)
+constexpr int kCoefRow = 16;    // [e0..e7 | o0..o6, 0] per tap pair
 
+// Copy the even/odd coefficient rows of taps 0..W/2-1 into shared memory.
 template <int W>
-__device__ __forceinline__ void win_taps(double f, const WinPoly& wp, double (&v)[W]) {
-    const double g = f - 0.5;
-#pragma unroll
-    for (int t = 0; t < W; ++t) {
-        double acc = wp.c[t][kWinDeg];
-#pragma unroll
-        for (int q = kWinDeg - 1; q >= 0; --q) acc = fma(acc, g, wp.c[t][q]);
-        v[t] = acc;
+__device__ __forceinline__ void load_coefs(const WinPoly& wp, double* csm) {
+    for (int i = threadIdx.x; i < (W / 2) * kCoefRow; i += blockDim.x) {
+        const int t = i / kCoefRow, k = i % kCoefRow;
+        double v = 0.0;
+        if (k < 8) v = wp.c[t][2 * k];
+        else if (k < 15) v = wp.c[t][2 * (k - 8) + 1];
+        csm[i] = v;
     }
 }
 
-// Region weights for T = 2: phi[r] = v[r - c] (c in {0,1}), zero outside the support.
+// row[c + s] = scale * phi(f + m - 1 - s) for s in [0, W), row[r] = 0 for the other r < RP.
+// T = 2: c in {0, 1} so exactly one of row[0], row[W] is outside the support.
 template <int W, int RP>
-__device__ __forceinline__ void region_weights(const double (&v)[W], int c, double scale, double (&phi)[RP]) {
-#pragma unroll
-    for (int r = 0; r < RP; ++r) {
-        double a = (r < W) ? v[r < W ? r : 0] : 0.0;          // c == 0
-        double b = (r >= 1 && r <= W) ? v[(r >= 1 && r <= W) ? r - 1 : 0] : 0.0;  // c == 1
-        phi[r] = scale * (c ? b : a);
+__device__ __forceinline__ void taps_to_row(double f, int c, double scale, const double* __restrict__ csm,
+                                            double* row) {
+    const double g = f - 0.5, g2 = g * g;
+    double* base = row + c;
+#pragma unroll 2
+    for (int t = 0; t < W / 2; ++t) {
+        const double2* cr = reinterpret_cast<const double2*>(csm + t * kCoefRow);
+        const double2 e01 = cr[0], e23 = cr[1], e45 = cr[2], e67 = cr[3];
+        const double2 o01 = cr[4], o23 = cr[5], o45 = cr[6], o67 = cr[7];
+        double E = fma(e67.y, g2, e67.x);
+        E = fma(E, g2, e45.y);
+        E = fma(E, g2, e45.x);
+        E = fma(E, g2, e23.y);
+        E = fma(E, g2, e23.x);
+        E = fma(E, g2, e01.y);
+        E = fma(E, g2, e01.x);
+        double O = fma(o67.x, g2, o45.y);
+        O = fma(O, g2, o45.x);
+        O = fma(O, g2, o23.y);
+        O = fma(O, g2, o23.x);
+        O = fma(O, g2, o01.y);
+        O = fma(O, g2, o01.x);
+        base[t] = scale * fma(g, O, E);
+        base[W - 1 - t] = scale * fma(-g, O, E);
     }
+    row[c ? 0 : W] = 0.0;
+#pragma unroll
+    for (int r = W + 1; r < RP; ++r) row[r] = 0.0;
 }
 
 // ------------------------------------------------------------------------------ interp
 template <int W>
 struct Interp3Cfg {
     static constexpr int T = 2, R = W + T - 1, RZ = (R + 1) & ~1, NT = 128, NW = NT / 32;
-    static constexpr int PROW = 2 * R + 1;                 // odd stride: fewer bank conflicts
+    static constexpr int LROW = 4 * RZ + 1;                // per-lane [x0 | y0 | x1 | y1], odd stride
     static constexpr int SMEM_H = R * R * RZ;              // doubles
-    static constexpr int SMEM_P = NT * PROW * 2;           // x and y rows, 2 nodes per lane
-    static constexpr size_t SMEM_BYTES = sizeof(double) * (SMEM_H + SMEM_P);
+    static constexpr int SMEM_P = NT * LROW;
+    static constexpr int SMEM_C = (W / 2) * kCoefRow;
+    static constexpr size_t SMEM_BYTES = sizeof(double) * (SMEM_H + SMEM_P + SMEM_C);
 };
 
 template <int W>
-__global__ void __launch_bounds__(128)
+__global__ void __launch_bounds__(128, 3)
 interp3_v2_kernel(const TileItem* __restrict__ items, int nitems, const double* __restrict__ u,
                   long long count, const double* __restrict__ grid, int n, int tpa,
                   const __grid_constant__ WinPoly wp, double* __restrict__ t_out) {
@@ -74,12 +99,16 @@ interp3_v2_kernel(const TileItem* __restrict__ items, int nitems, const double* 
     constexpr int T = C::T, R = C::R, RZ = C::RZ, m = W / 2;
     extern __shared__ __align__(16) double smem[];
     double* H = smem;
-    double* PXY = smem + C::SMEM_H;
+    double* csm = smem + C::SMEM_H;
+    double* rows = csm + C::SMEM_C;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    double* px0 = PXY + threadIdx.x * 2 * C::PROW;   // [x0 | y0] rows of node 0
-    double* px1 = px0 + C::PROW;                      // [x1 | y1] rows of node 1 (stride PROW)
+    double* rx0p = rows + threadIdx.x * C::LROW;   // x-row node 0
+    double* ry0p = rx0p + RZ;                      // y-row node 0
+    double* rx1p = ry0p + RZ;                      // x-row node 1 (z scratch first)
+    double* ry1p = rx1p + RZ;                      // y-row node 1
     const double* uy = u + count;
     const double* uz = u + 2 * count;
+    load_coefs<W>(wp, csm);
 
     for (int it = blockIdx.x; it < nitems; it += gridDim.x) {
         const TileItem item = items[it];
@@ -98,50 +127,23 @@ interp3_v2_kernel(const TileItem* __restrict__ items, int nitems, const double* 
             const long long j0 = item.start + (ok0 ? i0 : 0), j1 = item.start + (ok1 ? i1 : 0);
             double pz0[RZ], pz1[RZ];
             {
-                double v[W];
-                double ux0 = u[j0], uy0 = uy[j0], uz0 = uz[j0];
-                double ux1 = u[j1], uy1 = uy[j1], uz1 = uz[j1];
-                double fx, cx;
-                // node 0
-                cx = floor(ux0); fx = ux0 - cx;
-                win_taps<W>(fx, wp, v);
-                {
-                    double ph[R];
-                    region_weights<W, R>(v, (int)cx - ox, ok0 ? 1.0 : 0.0, ph);
+                double c, v;
+                v = uz[j0]; c = floor(v);
+                taps_to_row<W, RZ>(v - c, (int)c - oz, 1.0, csm, rx1p);
 #pragma unroll
-                    for (int r = 0; r < R; ++r) px0[r] = ph[r];
-                }
-                cx = floor(uy0); fx = uy0 - cx;
-                win_taps<W>(fx, wp, v);
-                {
-                    double ph[R];
-                    region_weights<W, R>(v, (int)cx - oy, 1.0, ph);
+                for (int r = 0; r < RZ; ++r) pz0[r] = rx1p[r];
+                v = uz[j1]; c = floor(v);
+                taps_to_row<W, RZ>(v - c, (int)c - oz, 1.0, csm, rx1p);
 #pragma unroll
-                    for (int r = 0; r < R; ++r) px0[R + r] = ph[r];
-                }
-                cx = floor(uz0); fx = uz0 - cx;
-                win_taps<W>(fx, wp, v);
-                region_weights<W, RZ>(v, (int)cx - oz, 1.0, pz0);
-                // node 1
-                cx = floor(ux1); fx = ux1 - cx;
-                win_taps<W>(fx, wp, v);
-                {
-                    double ph[R];
-                    region_weights<W, R>(v, (int)cx - ox, ok1 ? 1.0 : 0.0, ph);
-#pragma unroll
-                    for (int r = 0; r < R; ++r) px1[r] = ph[r];
-                }
-                cx = floor(uy1); fx = uy1 - cx;
-                win_taps<W>(fx, wp, v);
-                {
-                    double ph[R];
-                    region_weights<W, R>(v, (int)cx - oy, 1.0, ph);
-#pragma unroll
-                    for (int r = 0; r < R; ++r) px1[R + r] = ph[r];
-                }
-                cx = floor(uz1); fx = uz1 - cx;
-                win_taps<W>(fx, wp, v);
-                region_weights<W, RZ>(v, (int)cx - oz, 1.0, pz1);
+                for (int r = 0; r < RZ; ++r) pz1[r] = rx1p[r];
+                v = u[j0]; c = floor(v);
+                taps_to_row<W, RZ>(v - c, (int)c - ox, ok0 ? 1.0 : 0.0, csm, rx0p);
+                v = uy[j0]; c = floor(v);
+                taps_to_row<W, RZ>(v - c, (int)c - oy, 1.0, csm, ry0p);
+                v = u[j1]; c = floor(v);
+                taps_to_row<W, RZ>(v - c, (int)c - ox, ok1 ? 1.0 : 0.0, csm, rx1p);
+                v = uy[j1]; c = floor(v);
+                taps_to_row<W, RZ>(v - c, (int)c - oy, 1.0, csm, ry1p);
             }
             double acc0 = 0.0, acc1 = 0.0;
 #pragma unroll 1
@@ -150,20 +152,20 @@ interp3_v2_kernel(const TileItem* __restrict__ items, int nitems, const double* 
 #pragma unroll
                 for (int ry = 0; ry < R; ++ry) {
                     const double2* h = reinterpret_cast<const double2*>(H + (rx * R + ry) * RZ);
-                    double s0 = 0.0, s1 = 0.0;
+                    double s0 = 0.0, s1 = 0.0, q0 = 0.0, q1 = 0.0;
 #pragma unroll
                     for (int k = 0; k < RZ / 2; ++k) {
                         const double2 hv = h[k];
                         s0 = fma(hv.x, pz0[2 * k], s0);
                         s1 = fma(hv.x, pz1[2 * k], s1);
-                        s0 = fma(hv.y, pz0[2 * k + 1], s0);
-                        s1 = fma(hv.y, pz1[2 * k + 1], s1);
+                        q0 = fma(hv.y, pz0[2 * k + 1], q0);
+                        q1 = fma(hv.y, pz1[2 * k + 1], q1);
                     }
-                    sy0 = fma(px0[R + ry], s0, sy0);
-                    sy1 = fma(px1[R + ry], s1, sy1);
+                    sy0 = fma(ry0p[ry], s0 + q0, sy0);
+                    sy1 = fma(ry1p[ry], s1 + q1, sy1);
                 }
-                acc0 = fma(px0[rx], sy0, acc0);
-                acc1 = fma(px1[rx], sy1, acc1);
+                acc0 = fma(rx0p[rx], sy0, acc0);
+                acc1 = fma(rx1p[rx], sy1, acc1);
             }
             if (ok0) t_out[j0] = acc0;
             if (ok1) t_out[j1] = acc1;
@@ -178,15 +180,16 @@ struct Spread3Cfg {
     static constexpr int NCOL = R * R;
     static constexpr int NT = (((NCOL + 1) / 2) + 31) / 32 * 32;    // 2 columns per lane
     static constexpr int CP = 64;                                   // nodes per chunk
-    static constexpr int TXS = R + 1;                                // padded row strides
+    static constexpr int TXS = RZ;                                   // row strides
     static constexpr int SMEM_TAB = CP * (TXS + TXS + RZ);
     static constexpr int SMEM_OUT = NCOL * RZ;
-    static constexpr int SMEM = SMEM_TAB > SMEM_OUT ? SMEM_TAB : SMEM_OUT;
-    static constexpr size_t SMEM_BYTES = sizeof(double) * SMEM;
+    static constexpr int SMEM_MAIN = SMEM_TAB > SMEM_OUT ? SMEM_TAB : SMEM_OUT;
+    static constexpr int SMEM_C = (W / 2) * kCoefRow;
+    static constexpr size_t SMEM_BYTES = sizeof(double) * (SMEM_MAIN + SMEM_C);
 };
 
 template <int W>
-__global__ void __launch_bounds__(Spread3Cfg<W>::NT)
+__global__ void __launch_bounds__(Spread3Cfg<W>::NT, 4)
 spread3_v2_kernel(const TileItem* __restrict__ items, int nitems, const double* __restrict__ u,
                   const double* __restrict__ w, long long count, double* __restrict__ grid, int n,
                   int tpa, const __grid_constant__ WinPoly wp) {
@@ -196,6 +199,7 @@ spread3_v2_kernel(const TileItem* __restrict__ items, int nitems, const double* 
     double* TX = smem;                     // [CP][TXS]  w * phi_x
     double* TY = TX + CP * C::TXS;          // [CP][TXS]  phi_y
     double* TZ = TY + CP * C::TXS;          // [CP][RZ]   phi_z (zero padded)
+    double* csm = smem + C::SMEM_MAIN;
     const int tid = threadIdx.x;
     const int col0 = tid, col1 = tid + C::NT;
     const bool v0 = col0 < NCOL, v1 = col1 < NCOL;
@@ -203,6 +207,7 @@ spread3_v2_kernel(const TileItem* __restrict__ items, int nitems, const double* 
     const int rx1 = v1 ? col1 / R : 0, ry1 = v1 ? col1 % R : 0;
     const double* uy = u + count;
     const double* uz = u + 2 * count;
+    load_coefs<W>(wp, csm);
 
     for (int it = blockIdx.x; it < nitems; it += gridDim.x) {
         const TileItem item = items[it];
@@ -217,36 +222,17 @@ spread3_v2_kernel(const TileItem* __restrict__ items, int nitems, const double* 
             if (tid < CP) {
                 const bool ok = tid < np;
                 const long long j = item.start + c0 + (ok ? tid : 0);
-                double v[W];
-                double cx, fx;
-                double ux = u[j], uyy = uy[j], uzz = uz[j], wj = ok ? w[j] : 0.0;
-                cx = floor(ux); fx = ux - cx;
-                win_taps<W>(fx, wp, v);
-                {
-                    double ph[R];
-                    region_weights<W, R>(v, (int)cx - ox, wj, ph);
-#pragma unroll
-                    for (int r = 0; r < R; ++r) TX[tid * C::TXS + r] = ph[r];
-                }
-                cx = floor(uyy); fx = uyy - cx;
-                win_taps<W>(fx, wp, v);
-                {
-                    double ph[R];
-                    region_weights<W, R>(v, (int)cx - oy, 1.0, ph);
-#pragma unroll
-                    for (int r = 0; r < R; ++r) TY[tid * C::TXS + r] = ph[r];
-                }
-                cx = floor(uzz); fx = uzz - cx;
-                win_taps<W>(fx, wp, v);
-                {
-                    double ph[RZ];
-                    region_weights<W, RZ>(v, (int)cx - oz, 1.0, ph);
-#pragma unroll
-                    for (int r = 0; r < RZ; ++r) TZ[tid * RZ + r] = ph[r];
-                }
+                const double wj = ok ? w[j] : 0.0;
+                double v, c;
+                v = u[j]; c = floor(v);
+                taps_to_row<W, RZ>(v - c, (int)c - ox, wj, csm, TX + tid * C::TXS);
+                v = uy[j]; c = floor(v);
+                taps_to_row<W, RZ>(v - c, (int)c - oy, 1.0, csm, TY + tid * C::TXS);
+                v = uz[j]; c = floor(v);
+                taps_to_row<W, RZ>(v - c, (int)c - oz, 1.0, csm, TZ + tid * RZ);
             }
             __syncthreads();
-#pragma unroll 2
+#pragma unroll 1
             for (int p = 0; p < np; ++p) {
                 const double a0 = TX[p * C::TXS + rx0] * TY[p * C::TXS + ry0];
                 const double a1 = TX[p * C::TXS + rx1] * TY[p * C::TXS + ry1];
