@@ -123,6 +123,7 @@ struct ScaleParams {
     double centre[kMaxD];
     double rho, n, r2max;
     int d, T, tiles_per_axis;
+    int cell_minor;   // 1: key = (tile << d) | cell-within-tile bits (T = 2): nodes sorted by cell
 };
 
 __global__ void scale_key_kernel(const double* __restrict__ pts, long long count, ScaleParams sp,
@@ -131,7 +132,7 @@ __global__ void scale_key_kernel(const double* __restrict__ pts, long long count
     for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < count;
          i += (long long)gridDim.x * blockDim.x) {
         double r2 = 0.0;
-        int k = 0;
+        int k = 0, sub = 0;
         bool ok = true;
         for (int a = 0; a < sp.d; ++a) {
             double xs = sp.rho * (pts[i * sp.d + a] - sp.centre[a]);
@@ -143,9 +144,10 @@ __global__ void scale_key_kernel(const double* __restrict__ pts, long long count
             int tc = c / sp.T;
             tc = tc < 0 ? 0 : (tc >= sp.tiles_per_axis ? sp.tiles_per_axis - 1 : tc);
             k = k * sp.tiles_per_axis + tc;
+            sub = sub * 2 + (c & 1);
         }
         if (!ok || !(r2 <= sp.r2max)) atomicMin(bad, (int)i);
-        key[i] = k;
+        key[i] = sp.cell_minor ? ((k << sp.d) | sub) : k;
         idx[i] = (int)i;
     }
 }
@@ -162,6 +164,7 @@ int launch_scale_key(Plan& P, const double* pts, long long count, double* u_unso
     sp.d = P.d;
     sp.T = P.tile_cells;
     sp.tiles_per_axis = P.tiles_per_axis;
+    sp.cell_minor = P.dmma ? 1 : 0;
     scale_key_kernel<<<grid_for(count, 256), 256, 0, s>>>(pts, count, sp, u_unsorted, key, idx, bad);
     SK_LAUNCH_CHECK();
     return SK_OK;

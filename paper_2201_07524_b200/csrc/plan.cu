@@ -7,6 +7,9 @@
 
 #include "sk_internal.cuh"
 #include "tiled3.cuh"
+#define SK_WORKLIST_ONLY
+#include "dmma3.cuh"
+#undef SK_WORKLIST_ONLY
 #include "winpoly.h"
 
 namespace sk {
@@ -122,6 +125,76 @@ static int build_items(Plan& P, NodeSet& S, cudaStream_t s) {
     return SK_OK;
 }
 
+// DMMA path: nodes are sorted by key = (2^3 super-tile << 3) | cell bits. Run-length encode
+// the keys (one run per non-empty cell) and build on the host
+//   batches: <= 32 nodes of one cell (interp work unit of a warp),
+//   segs:    <= kSegMax nodes of one cell (spread),
+//   sitems:  consecutive segs of one super-tile, <= kSpreadItemMax nodes (spread work unit of a
+//            warp, flushed once with coalesced atomics), sorted by size for balance.
+static int build_cell_lists(Plan& P, NodeSet& S, cudaStream_t s) {
+    const long long count = S.count;
+    int *d_unique = nullptr, *d_counts = nullptr, *d_nruns = nullptr;
+    SK_TRY(alloc((void**)&d_unique, sizeof(int) * count));
+    SK_TRY(alloc((void**)&d_counts, sizeof(int) * count));
+    SK_TRY(alloc((void**)&d_nruns, sizeof(int)));
+    size_t tb = 0;
+    cub::DeviceRunLengthEncode::Encode(nullptr, tb, S.cell_key, d_unique, d_counts, d_nruns, (int)count, s);
+    void* tmp = nullptr;
+    SK_TRY(alloc(&tmp, tb));
+    SK_CUDA(cub::DeviceRunLengthEncode::Encode(tmp, tb, S.cell_key, d_unique, d_counts, d_nruns, (int)count, s));
+    count_launch(2);
+    int nruns = 0;
+    SK_CUDA(cudaMemcpyAsync(&nruns, d_nruns, sizeof(int), cudaMemcpyDeviceToHost, s));
+    SK_CUDA(cudaStreamSynchronize(s));
+    std::vector<int> keys(nruns), cnts(nruns);
+    SK_CUDA(cudaMemcpyAsync(keys.data(), d_unique, sizeof(int) * nruns, cudaMemcpyDeviceToHost, s));
+    SK_CUDA(cudaMemcpyAsync(cnts.data(), d_counts, sizeof(int) * nruns, cudaMemcpyDeviceToHost, s));
+    SK_CUDA(cudaStreamSynchronize(s));
+    cudaFree(tmp); cudaFree(d_unique); cudaFree(d_counts); cudaFree(d_nruns);
+    const int d = P.d, n = P.n, tpa = P.tiles_per_axis;
+    std::vector<CellBatch> batches, segs;
+    std::vector<SpreadItem> items;
+    batches.reserve(count / 16 + nruns);
+    long long start = 0;
+    int cur_tile = -1;
+    for (int r = 0; r < nruns; ++r) {
+        const int key = keys[r], cnt = cnts[r];
+        const int tile = key >> d, sub = key & ((1 << d) - 1);
+        int tc[3], cc[3];
+        int rest = tile;
+        for (int a = d - 1; a >= 0; --a) { tc[a] = rest % tpa; rest /= tpa; }
+        int bits = sub;
+        for (int a = d - 1; a >= 0; --a) { cc[a] = 2 * tc[a] + (bits & 1); bits >>= 1; }
+        int cell = 0;
+        for (int a = 0; a < d; ++a) cell = cell * n + cc[a];
+        for (int b = 0; b < cnt; b += 32) batches.push_back(CellBatch{cell, (int)(start + b), std::min(32, cnt - b), 0});
+        for (int b = 0; b < cnt; b += kSegMax) {
+            const int c = std::min(kSegMax, cnt - b);
+            if (tile != cur_tile || items.back().count + c > kSpreadItemMax) {
+                items.push_back(SpreadItem{tile, (int)segs.size(), (int)segs.size(), 0});
+                cur_tile = tile;
+            }
+            segs.push_back(CellBatch{cell, (int)(start + b), c, 0});
+            items.back().seg_end = (int)segs.size();
+            items.back().count += c;
+        }
+        start += cnt;
+    }
+    std::stable_sort(items.begin(), items.end(),
+                     [](const SpreadItem& a, const SpreadItem& b) { return a.count > b.count; });
+    S.nbatches = (int)batches.size();
+    S.nsegs = (int)segs.size();
+    S.nsitems = (int)items.size();
+    SK_TRY(alloc(&S.batches, sizeof(CellBatch) * batches.size()));
+    SK_TRY(alloc(&S.segs, sizeof(CellBatch) * segs.size()));
+    SK_TRY(alloc(&S.sitems, sizeof(SpreadItem) * items.size()));
+    SK_CUDA(cudaMemcpyAsync(S.batches, batches.data(), sizeof(CellBatch) * batches.size(), cudaMemcpyHostToDevice, s));
+    SK_CUDA(cudaMemcpyAsync(S.segs, segs.data(), sizeof(CellBatch) * segs.size(), cudaMemcpyHostToDevice, s));
+    SK_CUDA(cudaMemcpyAsync(S.sitems, items.data(), sizeof(SpreadItem) * items.size(), cudaMemcpyHostToDevice, s));
+    SK_CUDA(cudaStreamSynchronize(s));
+    return SK_OK;
+}
+
 static int plan_side(Plan& P, int sidx, const double* pts, long long count, cudaStream_t s) {
     NodeSet& S = P.side[sidx];
     S.count = count;
@@ -152,8 +225,9 @@ static int plan_side(Plan& P, int sidx, const double* pts, long long count, cuda
         return set_error(SK_EGEOMETRY, "node " + std::to_string(hbad) + " of side " + std::to_string(sidx) +
                                            " is non-finite or outside the ball |x'| <= 1/4 - eps_B/2");
     }
+    const long long nkeys = P.dmma ? ((long long)S.ntiles << P.d) : S.ntiles;
     int end_bit = 1;
-    while ((1LL << end_bit) < S.ntiles) ++end_bit;
+    while ((1LL << end_bit) < nkeys) ++end_bit;
     size_t tmp_bytes = 0;
     cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, key_in, S.cell_key, idx_in, S.perm, (int)count, 0,
                                     end_bit, s);
@@ -163,9 +237,13 @@ static int plan_side(Plan& P, int sidx, const double* pts, long long count, cuda
                                             0, end_bit, s));
     count_launch(4);
     SK_TRY(launch_gather_coords(P, u_uns, S.perm, count, S.u, s));
-    SK_TRY(launch_tile_offsets(S.cell_key, count, S.ntiles, S.tile_start, s));
-    SK_CUDA(cudaStreamSynchronize(s));
-    if (P.tiled) SK_TRY(build_items(P, S, s));
+    if (P.dmma) {
+        SK_TRY(build_cell_lists(P, S, s));
+    } else {
+        SK_TRY(launch_tile_offsets(S.cell_key, count, S.ntiles, S.tile_start, s));
+        SK_CUDA(cudaStreamSynchronize(s));
+        if (P.tiled) SK_TRY(build_items(P, S, s));
+    }
     cudaFree(tmp);
     cudaFree(u_uns);
     cudaFree(key_in);
@@ -249,6 +327,7 @@ int build_plan(Ctx* ctx, Plan** out, int d, const double* x, long long n, const 
         P->winpoly = wp;
         P->tiled = (d == 3) && (m_w == 6 || m_w == 8) && err >= 0.0 && err <= 1e-14 &&
                    getenv("SK_FORCE_V1") == nullptr;
+        P->dmma = P->tiled && m_w == 6 && getenv("SK_NO_DMMA") == nullptr;
     }
     P->tile_cells = choose_tile(d, ng, P->tiled);
     P->tiles_per_axis = ng / P->tile_cells;
@@ -347,6 +426,7 @@ int destroy_plan(Plan* P) {
     for (int sidx = 0; sidx < 2; ++sidx) {
         NodeSet& S = P->side[sidx];
         cudaFree(S.u); cudaFree(S.perm); cudaFree(S.cell_key); cudaFree(S.tile_start); cudaFree(S.items);
+        cudaFree(S.batches); cudaFree(S.segs); cudaFree(S.sitems);
     }
     cudaFree(P->grid); cudaFree(P->spec);
     for (int k = 0; k < 2; ++k) { cudaFree(P->D[k]); cudaFree(P->bk[k]); }

@@ -53,6 +53,13 @@ struct NodeSet {
     int ntiles = 0;
     void* items = nullptr;       // TileItem[nitems] work list of the tiled kernels (size-sorted)
     int nitems = 0;
+    // DMMA path (d = 3, W = 12): per-cell work lists
+    void* batches = nullptr;     // CellBatch[nbatches]: <= 32 nodes of one cell (interp)
+    int nbatches = 0;
+    void* segs = nullptr;        // CellBatch[nsegs]: <= kSegMax nodes of one cell (spread)
+    int nsegs = 0;
+    void* sitems = nullptr;      // SpreadItem[nsitems]: segments of one 2^3 super-tile (spread)
+    int nsitems = 0;
 };
 
 struct Ctx {
@@ -95,6 +102,7 @@ struct Plan {
     int tile_cells = 0;       // tile edge in grid cells (per axis)
     int tiles_per_axis = 0;
     bool tiled = false;       // v2 tiled spread/interp usable (d = 3, 2 m_w in {12, 16})
+    bool dmma = false;        // FP64 tensor-core spread/interp (d = 3, 2 m_w = 12)
     void* winpoly = nullptr;  // host WinPoly (window tap polynomials)
 };
 

@@ -10,6 +10,7 @@
 #pragma once
 #include "sk_internal.cuh"
 #include "tiled3.cuh"
+#include "dmma3.cuh"
 #include "window.cuh"
 
 namespace sk {
@@ -126,6 +127,24 @@ inline int interp3_launch(Plan& P, const NodeSet& S, const double* grid, double*
 }
 
 inline int spread_dispatch(Plan& P, const NodeSet& S, const double* w, double* grid, cudaStream_t s) {
+    if (P.dmma) {
+        using C = SpreadDCfg;
+        static bool attr = false;
+        if (!attr) {
+            cudaFuncSetAttribute(spread3_dmma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM_BYTES);
+            attr = true;
+        }
+        if (S.nsitems > 0) {
+            const int g = persistent_grid(spread3_dmma_kernel, C::NT, C::SMEM_BYTES, (S.nsitems + C::NWARP - 1) / C::NWARP);
+            spread3_dmma_kernel<<<g, C::NT, C::SMEM_BYTES, s>>>((const SpreadItem*)S.sitems, S.nsitems,
+                                                                (const CellBatch*)S.segs, S.u, w, S.count, grid,
+                                                                P.n, *(const WinPoly*)P.winpoly);
+            count_launch();
+        }
+        cudaError_t e = cudaGetLastError();
+        if (e != cudaSuccess) return set_error(SK_ECUDA, std::string("spread3_dmma: ") + cudaGetErrorString(e));
+        return SK_OK;
+    }
     if (P.tiled && P.d == 3) {
         if (S.nitems > 0) {
             if (P.win.m == 6) spread3_launch<12>(P, S, w, grid, s);
@@ -149,6 +168,23 @@ inline int spread_dispatch(Plan& P, const NodeSet& S, const double* w, double* g
 }
 
 inline int interp_dispatch(Plan& P, const NodeSet& S, const double* grid, double* t, cudaStream_t s) {
+    if (P.dmma) {
+        using C = InterpDCfg;
+        static bool attr = false;
+        if (!attr) {
+            cudaFuncSetAttribute(interp3_dmma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM_BYTES);
+            attr = true;
+        }
+        if (S.nbatches > 0) {
+            const int g = persistent_grid(interp3_dmma_kernel, C::NT, C::SMEM_BYTES, (S.nbatches + C::NWARP - 1) / C::NWARP);
+            interp3_dmma_kernel<<<g, C::NT, C::SMEM_BYTES, s>>>((const CellBatch*)S.batches, S.nbatches, S.u, S.count,
+                                                                grid, P.n, *(const WinPoly*)P.winpoly, t);
+            count_launch();
+        }
+        cudaError_t e = cudaGetLastError();
+        if (e != cudaSuccess) return set_error(SK_ECUDA, std::string("interp3_dmma: ") + cudaGetErrorString(e));
+        return SK_OK;
+    }
     if (P.tiled && P.d == 3) {
         if (S.nitems > 0) {
             if (P.win.m == 6) interp3_launch<12>(P, S, grid, t, s);

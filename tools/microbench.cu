@@ -109,6 +109,54 @@ __global__ void redg_kernel(double* grid, long long gsize, int iters) {
     }
 }
 
+// half the warps DFMA, half DMMA: are the FP64 vector and tensor pipes additive?
+__global__ void mixed_kernel(double* out, int iters) {
+    const int warp = threadIdx.x >> 5;
+    if (warp & 1) {
+        double a = threadIdx.x * 1e-3, b = 1.0 - threadIdx.x * 1e-4;
+        double c[4][2] = {};
+        for (int i = 0; i < iters; ++i) {
+#pragma unroll
+            for (int k = 0; k < 4; ++k)
+                asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+                             : "+d"(c[k][0]), "+d"(c[k][1]) : "d"(a), "d"(b));
+        }
+        double s = 0;
+        for (int k = 0; k < 4; ++k) s += c[k][0] + c[k][1];
+        out[blockIdx.x * blockDim.x + threadIdx.x] = s;
+    } else {
+        double c0 = threadIdx.x, c1 = c0 + 1, c2 = c0 + 2, c3 = c0 + 3, c4 = c0 + 4, c5 = c0 + 5, c6 = c0 + 6, c7 = c0 + 7;
+        const double a = 0.999999, b = 1e-7;
+        for (int i = 0; i < iters; ++i) {
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {   // 32 DFMA per thread = 1024 FMA per warp ~ 4 DMMA
+                c0 = fma(c0, a, b); c1 = fma(c1, a, b); c2 = fma(c2, a, b); c3 = fma(c3, a, b);
+                c4 = fma(c4, a, b); c5 = fma(c5, a, b); c6 = fma(c6, a, b); c7 = fma(c7, a, b);
+            }
+        }
+        out[blockIdx.x * blockDim.x + threadIdx.x] = c0 + c1 + c2 + c3 + c4 + c5 + c6 + c7;
+    }
+}
+
+// LDS.128 broadcast throughput with 8 independent FMA chains per thread
+__global__ void lds_tp_kernel(double* out, int iters) {
+    __shared__ __align__(16) double sh[1024];
+    for (int i = threadIdx.x; i < 1024; i += blockDim.x) sh[i] = i * 1e-3;
+    __syncthreads();
+    double a[8] = {0, 1, 2, 3, 4, 5, 6, 7};
+    for (int i = 0; i < iters; ++i) {
+#pragma unroll
+        for (int k = 0; k < 16; ++k) {
+            double2 v = *reinterpret_cast<const double2*>(&sh[((i * 16 + k) * 2) & 1023]);
+            a[(2 * k) & 7] = fma(a[(2 * k) & 7], v.x, 1e-9);
+            a[(2 * k + 1) & 7] = fma(a[(2 * k + 1) & 7], v.y, 1e-9);
+        }
+    }
+    double s = 0;
+    for (int k = 0; k < 8; ++k) s += a[k];
+    out[blockIdx.x * blockDim.x + threadIdx.x] = s;
+}
+
 template <typename F>
 float timeit(F f) {
     cudaEvent_t a, b;
@@ -155,6 +203,17 @@ int main() {
         ms = timeit([&] { lds_bcast_kernel<<<blocks, threads>>>(out, iters); });
         ops = 16.0 * iters * blocks * threads;
         printf("LDS.128 broadcast + 2 DFMA: %.1f G lane-loads/s (%.2f warp-LDS per clk per SM)\n", ops / ms / 1e6, ops / 32 / (ms * 1e-3) / p.multiProcessorCount / (clk * 1e3));
+    }
+    {
+        int iters = 4096;
+        float ms = timeit([&] { mixed_kernel<<<blocks, threads>>>(out, iters); });
+        // per pair of warps: DMMA warp 4*256 FMA, DFMA warp 32*32 FMA per iteration
+        double fl = 2.0 * 1024 * (double)iters * blocks * (threads / 32);
+        printf("mixed DFMA+DMMA: %.2f TFLOP/s (additive pipes would give ~2x dfma)\n", fl / ms / 1e9);
+        ms = timeit([&] { lds_tp_kernel<<<blocks, threads>>>(out, iters); });
+        double ops = 16.0 * iters * blocks * (threads / 32);
+        printf("LDS.128 broadcast, 8 chains: %.2f warp-LDS per clk per SM, %.2f TFLOP/s\n",
+               ops / (ms * 1e-3) / p.multiProcessorCount / (clk * 1e3), ops * 32 * 4 / ms / 1e9);
     }
     {
         long long gs = 1 << 21;
