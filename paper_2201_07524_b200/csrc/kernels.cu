@@ -123,7 +123,8 @@ struct ScaleParams {
     double centre[kMaxD];
     double rho, n, r2max;
     int d, T, tiles_per_axis;
-    int cell_minor;   // 1: key = (tile << d) | cell-within-tile bits (T = 2): nodes sorted by cell
+    int cell_minor;   // 1: key = tile * T^d + cell-within-tile index: nodes sorted by cell
+    int Td;           // T^d
 };
 
 __global__ void scale_key_kernel(const double* __restrict__ pts, long long count, ScaleParams sp,
@@ -144,10 +145,10 @@ __global__ void scale_key_kernel(const double* __restrict__ pts, long long count
             int tc = c / sp.T;
             tc = tc < 0 ? 0 : (tc >= sp.tiles_per_axis ? sp.tiles_per_axis - 1 : tc);
             k = k * sp.tiles_per_axis + tc;
-            sub = sub * 2 + (c & 1);
+            sub = sub * sp.T + (c - tc * sp.T);
         }
         if (!ok || !(r2 <= sp.r2max)) atomicMin(bad, (int)i);
-        key[i] = sp.cell_minor ? ((k << sp.d) | sub) : k;
+        key[i] = sp.cell_minor ? k * sp.Td + sub : k;
         idx[i] = (int)i;
     }
 }
@@ -165,6 +166,8 @@ int launch_scale_key(Plan& P, const double* pts, long long count, double* u_unso
     sp.T = P.tile_cells;
     sp.tiles_per_axis = P.tiles_per_axis;
     sp.cell_minor = P.dmma ? 1 : 0;
+    sp.Td = 1;
+    for (int a = 0; a < P.d; ++a) sp.Td *= P.tile_cells;
     scale_key_kernel<<<grid_for(count, 256), 256, 0, s>>>(pts, count, sp, u_unsorted, key, idx, bad);
     SK_LAUNCH_CHECK();
     return SK_OK;

@@ -9,6 +9,7 @@
 #include "tiled3.cuh"
 #define SK_WORKLIST_ONLY
 #include "dmma3.cuh"
+#include "dmma2.cuh"
 #undef SK_WORKLIST_ONLY
 #include "winpoly.h"
 
@@ -151,7 +152,9 @@ static int build_cell_lists(Plan& P, NodeSet& S, cudaStream_t s) {
     SK_CUDA(cudaMemcpyAsync(cnts.data(), d_counts, sizeof(int) * nruns, cudaMemcpyDeviceToHost, s));
     SK_CUDA(cudaStreamSynchronize(s));
     cudaFree(tmp); cudaFree(d_unique); cudaFree(d_counts); cudaFree(d_nruns);
-    const int d = P.d, n = P.n, tpa = P.tiles_per_axis;
+    const int d = P.d, n = P.n, tpa = P.tiles_per_axis, T = P.tile_cells;
+    int Td = 1;
+    for (int a = 0; a < d; ++a) Td *= T;
     std::vector<CellBatch> batches, segs;
     std::vector<SpreadItem> items;
     batches.reserve(count / 16 + nruns);
@@ -159,12 +162,12 @@ static int build_cell_lists(Plan& P, NodeSet& S, cudaStream_t s) {
     int cur_tile = -1;
     for (int r = 0; r < nruns; ++r) {
         const int key = keys[r], cnt = cnts[r];
-        const int tile = key >> d, sub = key & ((1 << d) - 1);
+        const int tile = key / Td, sub = key % Td;
         int tc[3], cc[3];
         int rest = tile;
         for (int a = d - 1; a >= 0; --a) { tc[a] = rest % tpa; rest /= tpa; }
-        int bits = sub;
-        for (int a = d - 1; a >= 0; --a) { cc[a] = 2 * tc[a] + (bits & 1); bits >>= 1; }
+        int digits = sub;
+        for (int a = d - 1; a >= 0; --a) { cc[a] = T * tc[a] + digits % T; digits /= T; }
         int cell = 0;
         for (int a = 0; a < d; ++a) cell = cell * n + cc[a];
         for (int b = 0; b < cnt; b += 32) batches.push_back(CellBatch{cell, (int)(start + b), std::min(32, cnt - b), 0});
@@ -225,7 +228,9 @@ static int plan_side(Plan& P, int sidx, const double* pts, long long count, cuda
         return set_error(SK_EGEOMETRY, "node " + std::to_string(hbad) + " of side " + std::to_string(sidx) +
                                            " is non-finite or outside the ball |x'| <= 1/4 - eps_B/2");
     }
-    const long long nkeys = P.dmma ? ((long long)S.ntiles << P.d) : S.ntiles;
+    long long Td = 1;
+    for (int a = 0; a < P.d; ++a) Td *= P.tile_cells;
+    const long long nkeys = P.dmma ? (long long)S.ntiles * Td : S.ntiles;
     int end_bit = 1;
     while ((1LL << end_bit) < nkeys) ++end_bit;
     size_t tmp_bytes = 0;
@@ -327,9 +332,11 @@ int build_plan(Ctx* ctx, Plan** out, int d, const double* x, long long n, const 
         P->winpoly = wp;
         P->tiled = (d == 3) && (m_w == 6 || m_w == 8) && err >= 0.0 && err <= 1e-14 &&
                    getenv("SK_FORCE_V1") == nullptr;
-        P->dmma = P->tiled && m_w == 6 && getenv("SK_NO_DMMA") == nullptr;
+        P->dmma = ((P->tiled && m_w == 6) || (d == 2 && m_w == 8 && err >= 0.0 && err <= 1e-14)) &&
+                  getenv("SK_NO_DMMA") == nullptr && getenv("SK_FORCE_V1") == nullptr;
+        if (P->dmma && d == 2) P->tiled = false;
     }
-    P->tile_cells = choose_tile(d, ng, P->tiled);
+    P->tile_cells = P->dmma ? (d == 3 ? 2 : kSup2) : choose_tile(d, ng, P->tiled);
     P->tiles_per_axis = ng / P->tile_cells;
 
     auto fail = [&](int code) { destroy_plan(P); return code; };

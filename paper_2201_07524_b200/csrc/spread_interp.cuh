@@ -11,6 +11,7 @@
 #include "sk_internal.cuh"
 #include "tiled3.cuh"
 #include "dmma3.cuh"
+#include "dmma2.cuh"
 #include "window.cuh"
 
 namespace sk {
@@ -127,6 +128,24 @@ inline int interp3_launch(Plan& P, const NodeSet& S, const double* grid, double*
 }
 
 inline int spread_dispatch(Plan& P, const NodeSet& S, const double* w, double* grid, cudaStream_t s) {
+    if (P.dmma && P.d == 2) {
+        using C = Spread2Cfg;
+        static bool attr = false;
+        if (!attr) {
+            cudaFuncSetAttribute(spread2_dmma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM_BYTES);
+            attr = true;
+        }
+        if (S.nsitems > 0) {
+            const int g = persistent_grid(spread2_dmma_kernel, C::NT, C::SMEM_BYTES, (S.nsitems + C::NWARP - 1) / C::NWARP);
+            spread2_dmma_kernel<<<g, C::NT, C::SMEM_BYTES, s>>>((const SpreadItem*)S.sitems, S.nsitems,
+                                                                (const CellBatch*)S.segs, S.u, w, S.count, grid,
+                                                                P.n, *(const WinPoly*)P.winpoly);
+            count_launch();
+        }
+        cudaError_t e = cudaGetLastError();
+        if (e != cudaSuccess) return set_error(SK_ECUDA, std::string("spread2_dmma: ") + cudaGetErrorString(e));
+        return SK_OK;
+    }
     if (P.dmma) {
         using C = SpreadDCfg;
         static bool attr = false;
@@ -168,6 +187,23 @@ inline int spread_dispatch(Plan& P, const NodeSet& S, const double* w, double* g
 }
 
 inline int interp_dispatch(Plan& P, const NodeSet& S, const double* grid, double* t, cudaStream_t s) {
+    if (P.dmma && P.d == 2) {
+        using C = Interp2Cfg;
+        static bool attr = false;
+        if (!attr) {
+            cudaFuncSetAttribute(interp2_dmma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM_BYTES);
+            attr = true;
+        }
+        if (S.nbatches > 0) {
+            const int g = persistent_grid(interp2_dmma_kernel, C::NT, C::SMEM_BYTES, (S.nbatches + C::NWARP - 1) / C::NWARP);
+            interp2_dmma_kernel<<<g, C::NT, C::SMEM_BYTES, s>>>((const CellBatch*)S.batches, S.nbatches, S.u, S.count,
+                                                                grid, P.n, *(const WinPoly*)P.winpoly, t);
+            count_launch();
+        }
+        cudaError_t e = cudaGetLastError();
+        if (e != cudaSuccess) return set_error(SK_ECUDA, std::string("interp2_dmma: ") + cudaGetErrorString(e));
+        return SK_OK;
+    }
     if (P.dmma) {
         using C = InterpDCfg;
         static bool attr = false;
