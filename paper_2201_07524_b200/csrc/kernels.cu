@@ -556,4 +556,8 @@ int launch_interp(Plan& P, int side, const double* grid, double* t_sorted, cudaS
     return SK_OK;
 }
 
+int launch_taps(Plan& P, int side, cudaStream_t s) {
+    return taps_dispatch(P, P.side[side], s);
+}
+
 }  // namespace sk

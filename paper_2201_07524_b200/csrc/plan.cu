@@ -244,6 +244,8 @@ static int plan_side(Plan& P, int sidx, const double* pts, long long count, cuda
     SK_TRY(launch_gather_coords(P, u_uns, S.perm, count, S.u, s));
     if (P.dmma) {
         SK_TRY(build_cell_lists(P, S, s));
+        SK_TRY(alloc((void**)&S.taps, sizeof(double) * count * P.d * 2 * P.win.m));
+        SK_TRY(launch_taps(P, sidx, s));
     } else {
         SK_TRY(launch_tile_offsets(S.cell_key, count, S.ntiles, S.tile_start, s));
         SK_CUDA(cudaStreamSynchronize(s));
@@ -433,7 +435,7 @@ int destroy_plan(Plan* P) {
     for (int sidx = 0; sidx < 2; ++sidx) {
         NodeSet& S = P->side[sidx];
         cudaFree(S.u); cudaFree(S.perm); cudaFree(S.cell_key); cudaFree(S.tile_start); cudaFree(S.items);
-        cudaFree(S.batches); cudaFree(S.segs); cudaFree(S.sitems);
+        cudaFree(S.batches); cudaFree(S.segs); cudaFree(S.sitems); cudaFree(S.taps);
     }
     cudaFree(P->grid); cudaFree(P->spec);
     for (int k = 0; k < 2; ++k) { cudaFree(P->D[k]); cudaFree(P->bk[k]); }

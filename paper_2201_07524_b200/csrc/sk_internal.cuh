@@ -60,6 +60,7 @@ struct NodeSet {
     int nsegs = 0;
     void* sitems = nullptr;      // SpreadItem[nsitems]: segments of one 2^3 super-tile (spread)
     int nsitems = 0;
+    double* taps = nullptr;      // [count][d][2 m_w] window taps of every node (sorted order)
 };
 
 struct Ctx {
@@ -116,6 +117,7 @@ int launch_gather_coords(Plan& P, const double* u_unsorted, const int* perm, lon
 int launch_tile_offsets(const int* sorted_keys, long long count, int ntiles, int* tile_start,
                         cudaStream_t s);
 int launch_spread(Plan& P, int side, const double* w_sorted, double* grid, cudaStream_t s);
+int launch_taps(Plan& P, int side, cudaStream_t s);
 int launch_interp(Plan& P, int side, const double* grid, double* t_sorted, cudaStream_t s);
 int launch_multiply(Plan& P, int kernel, cudaStream_t s);
 int launch_permute_in(const double* src, const int* perm, long long count, double* dst, cudaStream_t s);

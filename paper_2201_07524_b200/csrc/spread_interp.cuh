@@ -127,6 +127,20 @@ inline int interp3_launch(Plan& P, const NodeSet& S, const double* grid, double*
     return SK_OK;
 }
 
+// Plan time (DMMA path): tabulate the d x 2m window taps of every node, [node][axis][2m].
+inline int taps_dispatch(Plan& P, NodeSet& S, cudaStream_t s) {
+    if (S.count <= 0) return SK_OK;
+    const WinPoly& wp = *(const WinPoly*)P.winpoly;
+    long long g = (S.count + 255) / 256;
+    if (g > 148LL * 8) g = 148LL * 8;
+    if (P.d == 3) taps_precompute_kernel<3, 12><<<(int)g, 256, 0, s>>>(S.u, S.count, wp, S.taps);
+    else taps_precompute_kernel<2, 16><<<(int)g, 256, 0, s>>>(S.u, S.count, wp, S.taps);
+    count_launch();
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return set_error(SK_ECUDA, std::string("taps: ") + cudaGetErrorString(e));
+    return SK_OK;
+}
+
 inline int spread_dispatch(Plan& P, const NodeSet& S, const double* w, double* grid, cudaStream_t s) {
     if (P.dmma && P.d == 2) {
         using C = Spread2Cfg;
@@ -138,8 +152,7 @@ inline int spread_dispatch(Plan& P, const NodeSet& S, const double* w, double* g
         if (S.nsitems > 0) {
             const int g = persistent_grid(spread2_dmma_kernel, C::NT, C::SMEM_BYTES, (S.nsitems + C::NWARP - 1) / C::NWARP);
             spread2_dmma_kernel<<<g, C::NT, C::SMEM_BYTES, s>>>((const SpreadItem*)S.sitems, S.nsitems,
-                                                                (const CellBatch*)S.segs, S.u, w, S.count, grid,
-                                                                P.n, *(const WinPoly*)P.winpoly);
+                                                                (const CellBatch*)S.segs, S.taps, w, grid, P.n);
             count_launch();
         }
         cudaError_t e = cudaGetLastError();
@@ -156,8 +169,7 @@ inline int spread_dispatch(Plan& P, const NodeSet& S, const double* w, double* g
         if (S.nsitems > 0) {
             const int g = persistent_grid(spread3_dmma_kernel, C::NT, C::SMEM_BYTES, (S.nsitems + C::NWARP - 1) / C::NWARP);
             spread3_dmma_kernel<<<g, C::NT, C::SMEM_BYTES, s>>>((const SpreadItem*)S.sitems, S.nsitems,
-                                                                (const CellBatch*)S.segs, S.u, w, S.count, grid,
-                                                                P.n, *(const WinPoly*)P.winpoly);
+                                                                (const CellBatch*)S.segs, S.taps, w, grid, P.n);
             count_launch();
         }
         cudaError_t e = cudaGetLastError();
@@ -196,8 +208,7 @@ inline int interp_dispatch(Plan& P, const NodeSet& S, const double* grid, double
         }
         if (S.nbatches > 0) {
             const int g = persistent_grid(interp2_dmma_kernel, C::NT, C::SMEM_BYTES, (S.nbatches + C::NWARP - 1) / C::NWARP);
-            interp2_dmma_kernel<<<g, C::NT, C::SMEM_BYTES, s>>>((const CellBatch*)S.batches, S.nbatches, S.u, S.count,
-                                                                grid, P.n, *(const WinPoly*)P.winpoly, t);
+            interp2_dmma_kernel<<<g, C::NT, C::SMEM_BYTES, s>>>((const CellBatch*)S.batches, S.nbatches, S.taps, grid, P.n, t);
             count_launch();
         }
         cudaError_t e = cudaGetLastError();
@@ -213,8 +224,7 @@ inline int interp_dispatch(Plan& P, const NodeSet& S, const double* grid, double
         }
         if (S.nbatches > 0) {
             const int g = persistent_grid(interp3_dmma_kernel, C::NT, C::SMEM_BYTES, (S.nbatches + C::NWARP - 1) / C::NWARP);
-            interp3_dmma_kernel<<<g, C::NT, C::SMEM_BYTES, s>>>((const CellBatch*)S.batches, S.nbatches, S.u, S.count,
-                                                                grid, P.n, *(const WinPoly*)P.winpoly, t);
+            interp3_dmma_kernel<<<g, C::NT, C::SMEM_BYTES, s>>>((const CellBatch*)S.batches, S.nbatches, S.taps, grid, P.n, t);
             count_launch();
         }
         cudaError_t e = cudaGetLastError();
