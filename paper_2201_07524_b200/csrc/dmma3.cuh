@@ -54,6 +54,15 @@ constexpr int kSpreadItemMax = 4096;
 
 #ifndef SK_WORKLIST_ONLY   // plan.cu only needs the work-list types above
 
+__device__ __forceinline__ void prefetch_l2(const void* p) {
+    asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
+}
+// warp-cooperative L2 prefetch of [p, p + bytes)
+__device__ __forceinline__ void prefetch_range(const void* p, long long bytes, int lane) {
+    const char* c = reinterpret_cast<const char*>(p);
+    for (long long off = (long long)lane * 128; off < bytes; off += 32 * 128) prefetch_l2(c + off);
+}
+
 // ------------------------------------------------------------------------------ taps
 // out[node][a][t] = phi(f_a + m - 1 - t), f_a = frac(u_a), t < W (even/odd tap polynomials).
 template <int D, int W>
@@ -100,6 +109,10 @@ interp3_dmma_kernel(const CellBatch* __restrict__ batches, int nbatches, const d
         const int cz = B.cell % n, cy = (B.cell / n) % n, cx = B.cell / n / n;
         const double* T0 = taps + (long long)B.start * TS;
         const int last = B.count - 1;
+        if (bi + nw < nbatches) {   // next batch of this warp: stream its taps into L2
+            const CellBatch Bn = batches[bi + nw];
+            prefetch_range(taps + (long long)Bn.start * TS, (long long)Bn.count * TS * 8, lane);
+        }
         // B fragments: phi_z of node 8 nt + g at tz = 4 s + q
         double bf[KS][4];
 #pragma unroll
@@ -217,19 +230,51 @@ spread3_dmma_kernel(const SpreadItem* __restrict__ items, int nitems, const Cell
             const double* T0 = taps + (long long)seg.start * TS;
             const double* w0 = w + seg.start;
             const int nks = (seg.count + 3) >> 2;
-#pragma unroll 1
-            for (int s = 0; s < nks; ++s) {
+            // the taps stream from HBM once per apply: keep L2 two 32-node chunks ahead
+            prefetch_range(T0, (long long)min(seg.count, 64) * TS * 8, lane);
+            if (lane < 4) prefetch_l2(w0 + 16 * lane);
+            // B[k = q][n = g] of n-tile nt is column 8 nt + g = (ty, tz) = divmod(8 nt + g, 12):
+            // tz cycles with period 3 in nt, so a lane needs only phi_z at 3 positions and the
+            // node's 12 phi_y values -> 12 loads per k-step instead of 36.
+            const int z1 = (8 + g) % W;
+            // operands of k-step s: w*phi_x (A, 2 rows), phi_y[0..12), phi_z at {g, z1, 4+g}
+            auto load_ops = [&](int s, double& wv, double& x0, double& x1, double2 (&yy)[6], double (&zz)[3]) {
                 const int jr = 4 * s + q;                            // node of this lane's A/B
                 const bool ok = jr < seg.count;
                 const double* tr = T0 + (ok ? jr : 0) * TS;
-                const double wj = ok ? __ldg(w0 + jr) : 0.0;
-                const double a0 = wj * __ldg(tr + g);                   // A[tx = g][k = q]
-                const double a1 = (8 + g < W) ? wj * __ldg(tr + 8 + g) : 0.0;  // A[tx = 8 + g][k = q]
+                wv = ok ? __ldg(w0 + jr) : 0.0;
+                x0 = __ldg(tr + g);
+                x1 = (8 + g < W) ? __ldg(tr + 8 + g) : 0.0;
+                const double2* y2 = reinterpret_cast<const double2*>(tr + W);
+#pragma unroll
+                for (int i = 0; i < 6; ++i) yy[i] = __ldg(y2 + i);
+                zz[0] = __ldg(tr + 2 * W + g);
+                zz[1] = __ldg(tr + 2 * W + z1);
+                zz[2] = __ldg(tr + 2 * W + 4 + g);
+            };
+            double wn, x0n, x1n, zn[3];
+            double2 yn[6];
+            load_ops(0, wn, x0n, x1n, yn, zn);
+#pragma unroll 1
+            for (int s = 0; s < nks; ++s) {
+                if ((s & 7) == 0 && 4 * s + 64 < seg.count) {
+                    const int n0 = 4 * s + 64, n1 = min(seg.count, 4 * s + 96);
+                    prefetch_range(T0 + (long long)n0 * TS, (long long)(n1 - n0) * TS * 8, lane);
+                    if (lane < 2) prefetch_l2(w0 + n0 + 16 * lane);
+                }
+                const double a0 = wn * x0n, a1 = wn * x1n;           // A[tx = g | 8 + g][k = q]
+                double yv[W], zv[3];
+#pragma unroll
+                for (int i = 0; i < 6; ++i) { yv[2 * i] = yn[i].x; yv[2 * i + 1] = yn[i].y; }
+                zv[0] = zn[0]; zv[1] = zn[1]; zv[2] = zn[2];
+                if (s + 1 < nks) load_ops(s + 1, wn, x0n, x1n, yn, zn);   // software pipeline
 #pragma unroll
                 for (int nt = 0; nt < NTILE; ++nt) {
-                    // B[k = q][n = g]: column 8 nt + g = (ty, tz) pair
-                    const int col = 8 * nt + g;
-                    const double b = __ldg(tr + W + col / W) * __ldg(tr + 2 * W + col % W);
+                    // column 8 nt + g: ty = (8 nt + g) / 12 (compile-time up to g < 4 vs >= 4)
+                    const int k3 = nt / 3, r3 = nt % 3;
+                    const int ty = (r3 == 0) ? 2 * k3 : ((r3 == 1) ? 2 * k3 + (g >= 4 ? 1 : 0) : 2 * k3 + 1);
+                    const double yvv = (r3 == 1) ? (g >= 4 ? yv[2 * k3 + 1] : yv[2 * k3]) : yv[ty];
+                    const double b = yvv * zv[r3];
                     dmma884(acc[0][nt][0], acc[0][nt][1], a0, b);
                     dmma884(acc[1][nt][0], acc[1][nt][1], a1, b);
                 }

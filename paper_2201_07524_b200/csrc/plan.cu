@@ -160,6 +160,10 @@ static int build_cell_lists(Plan& P, NodeSet& S, cudaStream_t s) {
     batches.reserve(count / 16 + nruns);
     long long start = 0;
     int cur_tile = -1;
+    // spread work-unit size: enough items to keep ~4 per resident warp busy (148 SMs x 8
+    // warps), at most kSpreadItemMax nodes (one region flush per item)
+    const int item_max = (int)std::max(128LL, std::min((long long)kSpreadItemMax, count / 4736));
+    const int seg_max = std::min(kSegMax, item_max);
     for (int r = 0; r < nruns; ++r) {
         const int key = keys[r], cnt = cnts[r];
         const int tile = key / Td, sub = key % Td;
@@ -171,9 +175,9 @@ static int build_cell_lists(Plan& P, NodeSet& S, cudaStream_t s) {
         int cell = 0;
         for (int a = 0; a < d; ++a) cell = cell * n + cc[a];
         for (int b = 0; b < cnt; b += 32) batches.push_back(CellBatch{cell, (int)(start + b), std::min(32, cnt - b), 0});
-        for (int b = 0; b < cnt; b += kSegMax) {
-            const int c = std::min(kSegMax, cnt - b);
-            if (tile != cur_tile || items.back().count + c > kSpreadItemMax) {
+        for (int b = 0; b < cnt; b += seg_max) {
+            const int c = std::min(seg_max, cnt - b);
+            if (tile != cur_tile || items.back().count + c > item_max) {
                 items.push_back(SpreadItem{tile, (int)segs.size(), (int)segs.size(), 0});
                 cur_tile = tile;
             }
