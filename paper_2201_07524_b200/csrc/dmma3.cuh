@@ -103,14 +103,18 @@ interp3_dmma_kernel(const CellBatch* __restrict__ batches, int nbatches, const d
     const int g = lane >> 2, q = lane & 3;
     const long long n2 = (long long)n * n;
     const int gw = blockIdx.x * C::NWARP + warp, nw = gridDim.x * C::NWARP;
+    // contiguous slice of the cell-sorted batch list per warp: consecutive batches of one
+    // cell reuse its 12^3 grid block from L1, and the taps stream sequentially
+    const int per = (nbatches + nw - 1) / nw;
+    const int b_lo = gw * per, b_hi = min(nbatches, b_lo + per);
 
-    for (int bi = gw; bi < nbatches; bi += nw) {
+    for (int bi = b_lo; bi < b_hi; ++bi) {
         const CellBatch B = batches[bi];
         const int cz = B.cell % n, cy = (B.cell / n) % n, cx = B.cell / n / n;
         const double* T0 = taps + (long long)B.start * TS;
         const int last = B.count - 1;
-        if (bi + nw < nbatches) {   // next batch of this warp: stream its taps into L2
-            const CellBatch Bn = batches[bi + nw];
+        if (bi + 1 < b_hi) {   // next batch of this warp: stream its taps into L2
+            const CellBatch Bn = batches[bi + 1];
             prefetch_range(taps + (long long)Bn.start * TS, (long long)Bn.count * TS * 8, lane);
         }
         // B fragments: phi_z of node 8 nt + g at tz = 4 s + q
@@ -121,53 +125,53 @@ interp3_dmma_kernel(const CellBatch* __restrict__ batches, int nbatches, const d
 #pragma unroll
             for (int s = 0; s < KS; ++s) bf[s][nt] = __ldg(tz + 4 * s + q);
         }
-        // phi_y of node 8 nt + 2 q + e at ty = 8 h + g (rows ty >= W are padding)
-        double fy[4][2][2];
-#pragma unroll
-        for (int nt = 0; nt < 4; ++nt)
-#pragma unroll
-            for (int e = 0; e < 2; ++e) {
-                const double* ty = T0 + min(8 * nt + 2 * q + e, last) * TS + W;
-                fy[nt][e][0] = __ldg(ty + g);
-                fy[nt][e][1] = (8 + g < W) ? __ldg(ty + 8 + g) : 0.0;
-            }
+        // Rows of the DMMA are the flattened (tx, ty) pairs r = 8 mt + g, mt < 18 (no padding).
+        // For lane row g, ty = r % 12 cycles with period 3 in mt through {g, (8+g)%12, 4+g},
+        // so phi_y of the lane's 8 nodes lives in registers at just those 3 positions.
+        const int ty1 = (8 + g) % W, txo1 = (g >= 4) ? 1 : 0;
+        double yv[4][2][3];
         const double* txp[4][2];
 #pragma unroll
         for (int nt = 0; nt < 4; ++nt)
 #pragma unroll
-            for (int e = 0; e < 2; ++e) txp[nt][e] = T0 + min(8 * nt + 2 * q + e, last) * TS;
+            for (int e = 0; e < 2; ++e) {
+                const double* tr = T0 + min(8 * nt + 2 * q + e, last) * TS;
+                txp[nt][e] = tr;
+                yv[nt][e][0] = __ldg(tr + W + g);
+                yv[nt][e][1] = __ldg(tr + W + ty1);
+                yv[nt][e][2] = __ldg(tr + W + 4 + g);
+            }
         double acc[4][2];
 #pragma unroll
         for (int nt = 0; nt < 4; ++nt) acc[nt][0] = acc[nt][1] = 0.0;
         const double* Hb = grid + (long long)(cx - m + 1) * n2 + (long long)(cy - m + 1) * n + (cz - m + 1) + q;
-        const long long rowh1 = (8 + g < W) ? (long long)(8 + g) * n : 0;
-        const long long rowh0 = (long long)g * n;
-#pragma unroll 2
-        for (int tx = 0; tx < W; ++tx) {
-            const double* Hx = Hb + (long long)tx * n2;
-            double a0[KS], a1[KS];
+        const long long ry[3] = {(long long)g * n, (long long)ty1 * n, (long long)(4 + g) * n};
+#pragma unroll 1
+        for (int k = 0; k < W / 2; ++k) {
 #pragma unroll
-            for (int s = 0; s < KS; ++s) {
-                a0[s] = __ldg(Hx + rowh0 + 4 * s);
-                a1[s] = (8 + g < W) ? __ldg(Hx + rowh1 + 4 * s) : 0.0;
+            for (int r3 = 0; r3 < 3; ++r3) {
+                const int tx = 2 * k + (r3 == 0 ? 0 : (r3 == 2 ? 1 : txo1));
+                const double* Hrow = Hb + (long long)tx * n2 + ry[r3];
+                double a[KS];
+#pragma unroll
+                for (int s = 0; s < KS; ++s) a[s] = __ldg(Hrow + 4 * s);
+                double xw[4][2];
+#pragma unroll
+                for (int nt = 0; nt < 4; ++nt)
+#pragma unroll
+                    for (int e = 0; e < 2; ++e) xw[nt][e] = __ldg(txp[nt][e] + tx) * yv[nt][e][r3];
+                double d[4][2];
+#pragma unroll
+                for (int nt = 0; nt < 4; ++nt) d[nt][0] = d[nt][1] = 0.0;
+#pragma unroll
+                for (int s = 0; s < KS; ++s)
+#pragma unroll
+                    for (int nt = 0; nt < 4; ++nt) dmma884(d[nt][0], d[nt][1], a[s], bf[s][nt]);
+#pragma unroll
+                for (int nt = 0; nt < 4; ++nt)
+#pragma unroll
+                    for (int e = 0; e < 2; ++e) acc[nt][e] = fma(xw[nt][e], d[nt][e], acc[nt][e]);
             }
-            double d0[4][2], d1[4][2];
-#pragma unroll
-            for (int nt = 0; nt < 4; ++nt) d0[nt][0] = d0[nt][1] = d1[nt][0] = d1[nt][1] = 0.0;
-#pragma unroll
-            for (int s = 0; s < KS; ++s)
-#pragma unroll
-                for (int nt = 0; nt < 4; ++nt) {
-                    dmma884(d0[nt][0], d0[nt][1], a0[s], bf[s][nt]);
-                    dmma884(d1[nt][0], d1[nt][1], a1[s], bf[s][nt]);
-                }
-#pragma unroll
-            for (int nt = 0; nt < 4; ++nt)
-#pragma unroll
-                for (int e = 0; e < 2; ++e) {
-                    const double sy = fma(fy[nt][e][1], d1[nt][e], fy[nt][e][0] * d0[nt][e]);
-                    acc[nt][e] = fma(__ldg(txp[nt][e] + tx), sy, acc[nt][e]);
-                }
         }
         // sum over the 8 rows g held by lanes q, q+4, ..., q+28
 #pragma unroll
