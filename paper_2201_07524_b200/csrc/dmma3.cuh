@@ -89,12 +89,15 @@ taps_precompute_kernel(const double* __restrict__ u, long long count, const __gr
 }
 
 // ------------------------------------------------------------------------------ interp
+#ifndef SK_INTERP3_MINB
+#define SK_INTERP3_MINB 3
+#endif
 struct InterpDCfg {
     static constexpr int W = 12, KS = W / 4, NT = 128, NWARP = NT / 32, TS = 3 * W;
     static constexpr size_t SMEM_BYTES = 0;
 };
 
-__global__ void __launch_bounds__(128, 3)
+__global__ void __launch_bounds__(128, SK_INTERP3_MINB)
 interp3_dmma_kernel(const CellBatch* __restrict__ batches, int nbatches, const double* __restrict__ taps,
                     const double* __restrict__ grid, int n, double* __restrict__ t_out) {
     using C = InterpDCfg;
@@ -148,30 +151,37 @@ interp3_dmma_kernel(const CellBatch* __restrict__ batches, int nbatches, const d
         const long long ry[3] = {(long long)g * n, (long long)ty1 * n, (long long)(4 + g) * n};
 #pragma unroll 1
         for (int k = 0; k < W / 2; ++k) {
+            // three m-tiles (one period of ty) per step, their DMMAs interleaved s-major so
+            // 12 independent accumulations separate dependent DMMAs
+            int txr[3];
+            txr[0] = 2 * k;
+            txr[1] = 2 * k + txo1;
+            txr[2] = 2 * k + 1;
+            double a[3][KS];
 #pragma unroll
             for (int r3 = 0; r3 < 3; ++r3) {
-                const int tx = 2 * k + (r3 == 0 ? 0 : (r3 == 2 ? 1 : txo1));
-                const double* Hrow = Hb + (long long)tx * n2 + ry[r3];
-                double a[KS];
+                const double* Hrow = Hb + (long long)txr[r3] * n2 + ry[r3];
 #pragma unroll
-                for (int s = 0; s < KS; ++s) a[s] = __ldg(Hrow + 4 * s);
-                double xw[4][2];
-#pragma unroll
-                for (int nt = 0; nt < 4; ++nt)
-#pragma unroll
-                    for (int e = 0; e < 2; ++e) xw[nt][e] = __ldg(txp[nt][e] + tx) * yv[nt][e][r3];
-                double d[4][2];
-#pragma unroll
-                for (int nt = 0; nt < 4; ++nt) d[nt][0] = d[nt][1] = 0.0;
-#pragma unroll
-                for (int s = 0; s < KS; ++s)
-#pragma unroll
-                    for (int nt = 0; nt < 4; ++nt) dmma884(d[nt][0], d[nt][1], a[s], bf[s][nt]);
-#pragma unroll
-                for (int nt = 0; nt < 4; ++nt)
-#pragma unroll
-                    for (int e = 0; e < 2; ++e) acc[nt][e] = fma(xw[nt][e], d[nt][e], acc[nt][e]);
+                for (int s = 0; s < KS; ++s) a[r3][s] = __ldg(Hrow + 4 * s);
             }
+            double d[3][4][2];
+#pragma unroll
+            for (int r3 = 0; r3 < 3; ++r3)
+#pragma unroll
+                for (int nt = 0; nt < 4; ++nt) d[r3][nt][0] = d[r3][nt][1] = 0.0;
+#pragma unroll
+            for (int s = 0; s < KS; ++s)
+#pragma unroll
+                for (int r3 = 0; r3 < 3; ++r3)
+#pragma unroll
+                    for (int nt = 0; nt < 4; ++nt) dmma884(d[r3][nt][0], d[r3][nt][1], a[r3][s], bf[s][nt]);
+#pragma unroll
+            for (int r3 = 0; r3 < 3; ++r3)
+#pragma unroll
+                for (int nt = 0; nt < 4; ++nt)
+#pragma unroll
+                    for (int e = 0; e < 2; ++e)
+                        acc[nt][e] = fma(__ldg(txp[nt][e] + txr[r3]) * yv[nt][e][r3], d[r3][nt][e], acc[nt][e]);
         }
         // sum over the 8 rows g held by lanes q, q+4, ..., q+28
 #pragma unroll
