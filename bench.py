@@ -296,6 +296,14 @@ def main():
     bytes_alg = pts_per_launch * 8 * (cfg.d + 1) + (cfg.N * cfg.sigma) ** cfg.d * 8
     step_ms = total_ms / args.steps
     stage_share = {s: round(v[1] / (total_ms if world == 1 else total_ms), 4) for s, v in stage_ms.items()}
+    traffic, traffic_src = None, None
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as fh:
+            tr = json.load(fh).get(cfg.name, {}).get(dom)
+        if tr and world == 1:
+            traffic, traffic_src = float(tr["bytes_per_launch"]), tr["measured"]
+    except (OSError, ValueError, KeyError):
+        pass
     line = {
         "metric": "sinkhorn_iterations_per_s", "value": value, "unit": "it/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": step_ms, "higher_is_better": True,
@@ -306,10 +314,11 @@ def main():
                    "step": "plan + iters x (K v, K^T u) + divergence (2 applies)",
                    "parallelism": f"dp{world} (point shards + grid all-reduce)",
                    "l2": "256 MB buffer written between timed steps"},
-        "fastsum_point_evals_per_s": point_evals * world if False else cfg.n / (apply_ms * 1e-3),
+        "fastsum_point_evals_per_s": point_evals,   # all n targets of one K v, max-over-ranks time
         "fastsum_apply_ms": apply_ms,
         "roofline": {"bound": "alu", "kernel": dom, "achieved": achieved, "peak": fp64_peak,
-                     "unit": "TFLOP/s", "frac": achieved / fp64_peak, "traffic": None,
+                     "unit": "TFLOP/s", "frac": achieved / fp64_peak, "traffic": traffic,
+                     "traffic_source": traffic_src,
                      "algorithmic": f"2*(2m_w)^d flops per node per launch, {pts_per_launch:.3g} nodes/launch",
                      "peak_source": f"{N_SM} SMs x {FP64_FMA_PER_CLK_PER_SM} FP64 FMA/clk x 2 x sm_max_mhz "
                                     f"{pk.get('sm_max_mhz')} (DESIGN.md)",

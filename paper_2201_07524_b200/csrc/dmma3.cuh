@@ -17,9 +17,11 @@
 // d x W window values once (taps_precompute_kernel, [node][axis][W] FP64 in HBM, c5: 52 GB)
 // and the kernels load fragments straight from it (L1/L2): no per-apply window evaluation.
 //
-// Row padding: M = 16 rows per tx (ty padded 12 -> 16) for interp and M = 16 tx rows for
-// spread, i.e. 75% of the DMMA work is useful; in exchange the interp epilogue keeps the
-// per-node phi_y in registers and the spread forms its operands with one DMUL each.
+// DMMA shapes: interp rows are the 144 flattened (tx, ty) pairs (18 m-tiles, K = tz = 12:
+// no padding); a lane's row g meets only 3 distinct ty values, so phi_y of its 8 nodes stays
+// in registers. Spread rows are tx padded 12 -> 16 (75% useful DMMA work); a lane's 18
+// B-operand columns (ty, tz) meet only 3 distinct tz, so each k-step loads 12 phi_y + 3 phi_z
+// values and forms the 18 products with one DMUL each.
 //
 // Fragment layouts (m8n8k4, f64): g = lane/4, q = lane%4
 //   A[8x4]: a = A[g][q];  B[4x8]: b = B[q][g];  C[8x8]: c0, c1 = C[g][2q], C[g][2q+1]
