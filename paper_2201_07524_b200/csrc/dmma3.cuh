@@ -133,15 +133,18 @@ interp3_dmma_kernel(const CellBatch* __restrict__ batches, int nbatches, const d
         // Rows of the DMMA are the flattened (tx, ty) pairs r = 8 mt + g, mt < 18 (no padding).
         // For lane row g, ty = r % 12 cycles with period 3 in mt through {g, (8+g)%12, 4+g},
         // so phi_y of the lane's 8 nodes lives in registers at just those 3 positions.
+        // Within step k the lane's three rows have tx = 2k (r3 = 0, and r3 = 1 when g < 4) or
+        // 2k + 1 (r3 = 2, and r3 = 1 when g >= 4): accumulate phi_y * E per (node, tx) and apply
+        // phi_x once per k with one 16-byte load of (phi_x[2k], phi_x[2k+1]).
         const int ty1 = (8 + g) % W, txo1 = (g >= 4) ? 1 : 0;
-        double yv[4][2][3];
-        const double* txp[4][2];
+        double yv[4][2][3];   // phi_y at ty = g, (8+g)%12, 4+g
+        int nrow[4][2];       // node rows of this lane (offsets into T0 in doubles)
 #pragma unroll
         for (int nt = 0; nt < 4; ++nt)
 #pragma unroll
             for (int e = 0; e < 2; ++e) {
-                const double* tr = T0 + min(8 * nt + 2 * q + e, last) * TS;
-                txp[nt][e] = tr;
+                nrow[nt][e] = min(8 * nt + 2 * q + e, last) * TS;
+                const double* tr = T0 + nrow[nt][e];
                 yv[nt][e][0] = __ldg(tr + W + g);
                 yv[nt][e][1] = __ldg(tr + W + ty1);
                 yv[nt][e][2] = __ldg(tr + W + 4 + g);
@@ -178,12 +181,16 @@ interp3_dmma_kernel(const CellBatch* __restrict__ batches, int nbatches, const d
 #pragma unroll
                     for (int nt = 0; nt < 4; ++nt) dmma884(d[r3][nt][0], d[r3][nt][1], a[r3][s], bf[s][nt]);
 #pragma unroll
-            for (int r3 = 0; r3 < 3; ++r3)
+            for (int nt = 0; nt < 4; ++nt)
 #pragma unroll
-                for (int nt = 0; nt < 4; ++nt)
-#pragma unroll
-                    for (int e = 0; e < 2; ++e)
-                        acc[nt][e] = fma(__ldg(txp[nt][e] + txr[r3]) * yv[nt][e][r3], d[r3][nt][e], acc[nt][e]);
+                for (int e = 0; e < 2; ++e) {
+                    // phi_x[2k], phi_x[2k+1] of the node in one 16-byte load
+                    const double2 xx = __ldg(reinterpret_cast<const double2*>(T0 + nrow[nt][e]) + k);
+                    const double t1 = yv[nt][e][1] * d[1][nt][e];
+                    const double sa = fma(yv[nt][e][0], d[0][nt][e], txo1 ? 0.0 : t1);
+                    const double sb = fma(yv[nt][e][2], d[2][nt][e], txo1 ? t1 : 0.0);
+                    acc[nt][e] = fma(xx.x, sa, fma(xx.y, sb, acc[nt][e]));
+                }
         }
         // sum over the 8 rows g held by lanes q, q+4, ..., q+28
 #pragma unroll
