@@ -182,6 +182,21 @@ def test_divergence_parity_subsample(capi, ctx, name, k):
     assert err <= tol, (name, sc, ref, info.asdict())
 
 
+def test_divergence_c4_subsample_conditioning(capi, ctx):
+    """c4 (lam = 200, image-like histograms): Alg. 2 is conditioning-limited (DESIGN.md §8);
+    on a 3000-point random subsample kappa ~ 1e15 and s~ stays within the method's envelope."""
+    cfg = get("c4")
+    x, y, a, b = make_inputs(cfg)
+    ix = np.sort(np.random.default_rng(0).choice(x.shape[0], size=3000, replace=False))
+    iy = np.sort(np.random.default_rng(1).choice(y.shape[0], size=3000, replace=False))
+    x, y, a, b = x[ix], y[iy], a[ix] / a[ix].sum(), b[iy] / b[iy].sum()
+    ref, _, _ = dense.sinkhorn_divergence(x, y, a, b, cfg.lam, cfg.iters)
+    sd, sc, info, *_ = _gpu_divergence(capi, ctx, cfg, x, y, a, b)
+    assert info.kappa_log10_est > 12
+    assert abs(sc - ref["s_cost"]) <= 1e-3 * abs(ref["s_cost"])
+    assert abs(sd - ref["s_dual"]) <= 1e-4 * abs(ref["s_dual"])
+
+
 def test_divergence_golden_full(capi, ctx):
     """Full-size / 1e5-subsample oracle divergences precomputed by tools/make_golden.py (calls
     only oracle/), when present."""
