@@ -96,7 +96,8 @@ taps_precompute_kernel(const double* __restrict__ u, long long count, const __gr
 #endif
 struct InterpDCfg {
     static constexpr int W = 12, KS = W / 4, NT = 128, NWARP = NT / 32, TS = 3 * W;
-    static constexpr size_t SMEM_BYTES = 0;
+    static constexpr int XS = W + 2;                          // phi_x row stride (doubles)
+    static constexpr size_t SMEM_BYTES = sizeof(double) * NWARP * 32 * XS;
 };
 
 __global__ void __launch_bounds__(128, SK_INTERP3_MINB)
@@ -108,6 +109,8 @@ interp3_dmma_kernel(const CellBatch* __restrict__ batches, int nbatches, const d
     const int g = lane >> 2, q = lane & 3;
     const long long n2 = (long long)n * n;
     const int gw = blockIdx.x * C::NWARP + warp, nw = gridDim.x * C::NWARP;
+    extern __shared__ __align__(16) double smem[];
+    double* XT = smem + warp * 32 * C::XS;        // [node][XS] phi_x rows of the current batch
     // contiguous slice of the cell-sorted batch list per warp: consecutive batches of one
     // cell reuse its 12^3 grid block from L1, and the taps stream sequentially
     const int per = (nbatches + nw - 1) / nw;
@@ -138,13 +141,18 @@ interp3_dmma_kernel(const CellBatch* __restrict__ batches, int nbatches, const d
         // phi_x once per k with one 16-byte load of (phi_x[2k], phi_x[2k+1]).
         const int ty1 = (8 + g) % W, txo1 = (g >= 4) ? 1 : 0;
         double yv[4][2][3];   // phi_y at ty = g, (8+g)%12, 4+g
-        int nrow[4][2];       // node rows of this lane (offsets into T0 in doubles)
+        {   // stage the batch's phi_x rows (lane = node) in this warp's shared table
+            const double2* src = reinterpret_cast<const double2*>(T0 + min(lane, last) * TS);
+            double2* dst = reinterpret_cast<double2*>(XT + lane * C::XS);
+#pragma unroll
+            for (int i = 0; i < W / 2; ++i) dst[i] = __ldg(src + i);
+        }
+        __syncwarp();
 #pragma unroll
         for (int nt = 0; nt < 4; ++nt)
 #pragma unroll
             for (int e = 0; e < 2; ++e) {
-                nrow[nt][e] = min(8 * nt + 2 * q + e, last) * TS;
-                const double* tr = T0 + nrow[nt][e];
+                const double* tr = T0 + min(8 * nt + 2 * q + e, last) * TS;
                 yv[nt][e][0] = __ldg(tr + W + g);
                 yv[nt][e][1] = __ldg(tr + W + ty1);
                 yv[nt][e][2] = __ldg(tr + W + 4 + g);
@@ -185,7 +193,7 @@ interp3_dmma_kernel(const CellBatch* __restrict__ batches, int nbatches, const d
 #pragma unroll
                 for (int e = 0; e < 2; ++e) {
                     // phi_x[2k], phi_x[2k+1] of the node in one 16-byte load
-                    const double2 xx = __ldg(reinterpret_cast<const double2*>(T0 + nrow[nt][e]) + k);
+                    const double2 xx = reinterpret_cast<const double2*>(XT + (8 * nt + 2 * q + e) * C::XS)[k];
                     const double t1 = yv[nt][e][1] * d[1][nt][e];
                     const double sa = fma(yv[nt][e][0], d[0][nt][e], txo1 ? 0.0 : t1);
                     const double sb = fma(yv[nt][e][2], d[2][nt][e], txo1 ? t1 : 0.0);
@@ -212,6 +220,7 @@ interp3_dmma_kernel(const CellBatch* __restrict__ batches, int nbatches, const d
                     if (p < B.count) t_out[B.start + p] = acc[nt][e];
                 }
         }
+        __syncwarp();   // XT is rewritten by the next batch
     }
 }
 
