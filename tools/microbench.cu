@@ -157,6 +157,99 @@ __global__ void lds_tp_kernel(double* out, int iters) {
     out[blockIdx.x * blockDim.x + threadIdx.x] = s;
 }
 
+// the spread3 inner-loop mix: per k-step 18 products (DMUL) feeding 36 DMMAs into 36
+// independent accumulators (72 doubles/lane), 2 warps x 2 CTAs per SMSP-quad like the kernel
+template <bool WITH_DMUL>
+__global__ void __launch_bounds__(128, 2) spreadmix_kernel(double* out, int iters) {
+    double acc[2][18][2];
+#pragma unroll
+    for (int i = 0; i < 2; ++i)
+#pragma unroll
+        for (int j = 0; j < 18; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+    double y = 1.0 + threadIdx.x * 1e-6, z = 1.0 - threadIdx.x * 1e-6, a0 = 1e-3, a1 = 2e-3;
+    for (int it = 0; it < iters; ++it) {
+#pragma unroll
+        for (int j = 0; j < 18; ++j) {
+            const double b = WITH_DMUL ? y * (z + j) : y + j;
+            asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+                : "+d"(acc[0][j][0]), "+d"(acc[0][j][1]) : "d"(a0), "d"(b));
+            asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+                : "+d"(acc[1][j][0]), "+d"(acc[1][j][1]) : "d"(a1), "d"(b));
+        }
+        y *= 0.9999999;
+    }
+    double s = 0;
+#pragma unroll
+    for (int i = 0; i < 2; ++i)
+#pragma unroll
+        for (int j = 0; j < 18; ++j) s += acc[i][j][0] + acc[i][j][1];
+    out[blockIdx.x * blockDim.x + threadIdx.x] = s;
+}
+
+// operand-order variants of the spread mix: ORDER 0 = (a0,b_j),(a1,b_j) pairs; 1 = all a0 then
+// all a1 (A reused, B changes every DMMA); 2 = b_j varies but computed without DMUL chains
+template <int ORDER>
+__global__ void __launch_bounds__(128, 2) spreadorder_kernel(double* out, int iters) {
+    double acc[2][18][2];
+#pragma unroll
+    for (int i = 0; i < 2; ++i)
+#pragma unroll
+        for (int j = 0; j < 18; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+    double y = 1.0 + threadIdx.x * 1e-6, a0 = 1e-3, a1 = 2e-3;
+    double b[18];
+    for (int it = 0; it < iters; ++it) {
+#pragma unroll
+        for (int j = 0; j < 18; ++j) b[j] = y + j;
+        if (ORDER == 1) {
+#pragma unroll
+            for (int j = 0; j < 18; ++j)
+                asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+                    : "+d"(acc[0][j][0]), "+d"(acc[0][j][1]) : "d"(a0), "d"(b[j]));
+#pragma unroll
+            for (int j = 0; j < 18; ++j)
+                asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+                    : "+d"(acc[1][j][0]), "+d"(acc[1][j][1]) : "d"(a1), "d"(b[j]));
+        } else {
+#pragma unroll
+            for (int j = 0; j < 18; ++j) {
+                asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+                    : "+d"(acc[0][j][0]), "+d"(acc[0][j][1]) : "d"(a0), "d"(b[j]));
+                asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+                    : "+d"(acc[1][j][0]), "+d"(acc[1][j][1]) : "d"(a1), "d"(b[j]));
+            }
+        }
+        y *= 0.9999999;
+    }
+    double s = 0;
+#pragma unroll
+    for (int i = 0; i < 2; ++i)
+#pragma unroll
+        for (int j = 0; j < 18; ++j) s += acc[i][j][0] + acc[i][j][1];
+    out[blockIdx.x * blockDim.x + threadIdx.x] = s;
+}
+
+// accumulator-count sweep: NACC independent m8n8k4 accumulators per lane, same A/B
+template <int NACC>
+__global__ void __launch_bounds__(128, 2) accsweep_kernel(double* out, int iters) {
+    double acc[NACC][2];
+#pragma unroll
+    for (int j = 0; j < NACC; ++j) acc[j][0] = acc[j][1] = 0.0;
+    double a = 1e-3 + threadIdx.x * 1e-9, b = 1.0;
+    for (int it = 0; it < iters; ++it) {
+#pragma unroll
+        for (int r = 0; r < 36 / NACC; ++r)
+#pragma unroll
+            for (int j = 0; j < NACC; ++j)
+                asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+                    : "+d"(acc[j][0]), "+d"(acc[j][1]) : "d"(a), "d"(b));
+        b *= 0.9999999;
+    }
+    double s = 0;
+#pragma unroll
+    for (int j = 0; j < NACC; ++j) s += acc[j][0] + acc[j][1];
+    out[blockIdx.x * blockDim.x + threadIdx.x] = s;
+}
+
 template <typename F>
 float timeit(F f) {
     cudaEvent_t a, b;
@@ -214,6 +307,29 @@ int main() {
         double ops = 16.0 * iters * blocks * (threads / 32);
         printf("LDS.128 broadcast, 8 chains: %.2f warp-LDS per clk per SM, %.2f TFLOP/s\n",
                ops / (ms * 1e-3) / p.multiProcessorCount / (clk * 1e3), ops * 32 * 4 / ms / 1e9);
+    }
+    {
+        int iters = 2048;
+        const int g2 = p.multiProcessorCount * 2;
+        float ms = timeit([&] { spreadmix_kernel<true><<<g2, 128>>>(out, iters); });
+        double fl = 2.0 * 256 * 36 * (double)iters * g2 * 4;
+        printf("spread mix (36 DMMA + 18 DMUL, 8 warps/SM): %.2f TFLOP/s\n", fl / ms / 1e9);
+        ms = timeit([&] { spreadmix_kernel<false><<<g2, 128>>>(out, iters); });
+        printf("spread mix without DMUL (36 DMMA, 8 warps/SM): %.2f TFLOP/s\n", fl / ms / 1e9);
+        ms = timeit([&] { spreadmix_kernel<true><<<g2 * 2, 128>>>(out, iters); });
+        printf("spread mix, 16 warps/SM: %.2f TFLOP/s\n", 2 * fl / ms / 1e9);
+        ms = timeit([&] { spreadorder_kernel<0><<<g2, 128>>>(out, iters); });
+        printf("spread order 0 (pairs, b precomputed): %.2f TFLOP/s\n", fl / ms / 1e9);
+        ms = timeit([&] { spreadorder_kernel<1><<<g2, 128>>>(out, iters); });
+        printf("spread order 1 (A-major): %.2f TFLOP/s\n", fl / ms / 1e9);
+        ms = timeit([&] { accsweep_kernel<4><<<g2, 128>>>(out, iters); });
+        printf("36 DMMA/iter, 4 accumulators, 8 warps/SM: %.2f TFLOP/s\n", fl / ms / 1e9);
+        ms = timeit([&] { accsweep_kernel<12><<<g2, 128>>>(out, iters); });
+        printf("36 DMMA/iter, 12 accumulators, 8 warps/SM: %.2f TFLOP/s\n", fl / ms / 1e9);
+        ms = timeit([&] { accsweep_kernel<36><<<g2, 128>>>(out, iters); });
+        printf("36 DMMA/iter, 36 accumulators, 8 warps/SM: %.2f TFLOP/s\n", fl / ms / 1e9);
+        ms = timeit([&] { accsweep_kernel<4><<<g2 * 4, 128>>>(out, iters); });
+        printf("36 DMMA/iter, 4 accumulators, 32 warps/SM: %.2f TFLOP/s\n", 4 * fl / ms / 1e9);
     }
     {
         long long gs = 1 << 21;

@@ -30,7 +30,16 @@ def main():
     x, y, a, b = make_inputs(cfg)
     ctx = capi.Context(0)
     t = lambda z: torch.from_numpy(np.ascontiguousarray(z)).cuda()  # noqa: E731
-    P = capi.Plan(ctx, t(x), t(y), cfg.lam, cfg.N, cfg.sigma, cfg.m_w, cfg.eps_B, cfg.p)
+    import time
+    dx, dy = t(x), t(y)
+    for rep in range(2):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        P = capi.Plan(ctx, dx, dy, cfg.lam, cfg.N, cfg.sigma, cfg.m_w, cfg.eps_B, cfg.p)
+        torch.cuda.synchronize()
+        print(f"plan {rep}: {1e3 * (time.perf_counter() - t0):.1f} ms")
+        if rep == 0:
+            P.close()
     w_y, w_x = t(b), t(a)
     capi.fastsum_apply(P, w_y, 0, 0)
     torch.cuda.synchronize()
