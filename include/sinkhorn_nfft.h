@@ -151,6 +151,11 @@ long long sk_launch_count(void);
 void sk_profile(int on);
 int sk_profile_read(double* out, int nstages, int reset);
 
+/* Device memory of destroyed plans is cached by the library and reused (best fit, ordered on
+ * the allocating stream with events); this returns every cached block to the driver. Call it
+ * after fastsum_plan_destroy when the memory is needed elsewhere. */
+void sk_release_cache(void);
+
 const char* sk_last_error(void);
 
 #ifdef __cplusplus

@@ -64,6 +64,7 @@ _sig = {
     "fastsum_plan_info": ([_vp, _dp], _i),
     "fastsum_coefficients": ([_vp, _i, _dp], _i),
     "sk_launch_count": ([], _ll),
+    "sk_release_cache": ([], None),
     "sk_profile": ([_i], None),
     "sk_profile_read": ([_dp, _i, _i], _i),
     "sk_last_error": ([], ctypes.c_char_p),

@@ -6,6 +6,7 @@
 #include <math.h>
 #include <nccl.h>
 #include <atomic>
+#include <map>
 #include <mutex>
 #include <string>
 #include <vector>
@@ -23,6 +24,85 @@ int set_error(int code, const std::string& msg) {
     return code;
 }
 void count_launch(long long k) { g_launches += k; }
+
+// ---------------------------------------------------------------- caching device allocator
+// Plans allocate tens of GB (c5: sorted nodes, 52 GB of window taps, grids); cudaMalloc /
+// cudaFree of such blocks costs tens of ms and synchronises the device. Freed blocks are kept
+// per process and reused best-fit (size in [req, 2 req)); a block freed on stream A carries
+// an event that a later user on stream B waits for, so reuse is stream-ordered. On OOM the
+// cache is released and the allocation retried.
+struct CachedBlock {
+    void* p;
+    size_t bytes;
+    cudaEvent_t ready;
+    int device;
+};
+static std::mutex g_alloc_mu;
+static std::multimap<size_t, CachedBlock> g_cache;
+static std::map<void*, std::pair<size_t, int>> g_live;   // ptr -> (bytes, device)
+
+static size_t round_bytes(size_t b) {
+    const size_t g = b >= (1u << 20) ? (2u << 20) : 512;
+    return (b + g - 1) / g * g;
+}
+
+void dev_cache_release() {
+    std::lock_guard<std::mutex> lk(g_alloc_mu);
+    for (auto& kv : g_cache) {
+        cudaEventSynchronize(kv.second.ready);
+        cudaEventDestroy(kv.second.ready);
+        cudaFree(kv.second.p);
+    }
+    g_cache.clear();
+}
+
+int dev_alloc(void** out, size_t bytes, cudaStream_t s) {
+    *out = nullptr;
+    if (bytes == 0) return SK_OK;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    const size_t want = round_bytes(bytes);
+    {
+        std::lock_guard<std::mutex> lk(g_alloc_mu);
+        for (auto it = g_cache.lower_bound(want); it != g_cache.end() && it->first < 2 * want; ++it) {
+            if (it->second.device != dev) continue;
+            CachedBlock blk = it->second;
+            g_cache.erase(it);
+            cudaStreamWaitEvent(s, blk.ready, 0);
+            cudaEventDestroy(blk.ready);
+            g_live[blk.p] = {blk.bytes, dev};
+            *out = blk.p;
+            return SK_OK;
+        }
+    }
+    cudaError_t e = cudaMalloc(out, want);
+    if (e == cudaErrorMemoryAllocation) {
+        cudaGetLastError();
+        dev_cache_release();
+        e = cudaMalloc(out, want);
+    }
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        *out = nullptr;
+        return set_error(e == cudaErrorMemoryAllocation ? SK_ENOMEM : SK_ECUDA,
+                         std::string("cudaMalloc(") + std::to_string(bytes) + "): " + cudaGetErrorString(e));
+    }
+    std::lock_guard<std::mutex> lk(g_alloc_mu);
+    g_live[*out] = {want, dev};
+    return SK_OK;
+}
+
+void dev_free(void* p, cudaStream_t s) {
+    if (!p) return;
+    std::lock_guard<std::mutex> lk(g_alloc_mu);
+    auto it = g_live.find(p);
+    if (it == g_live.end()) return;
+    CachedBlock blk{p, it->second.first, nullptr, it->second.second};
+    g_live.erase(it);
+    cudaEventCreateWithFlags(&blk.ready, cudaEventDisableTiming);
+    cudaEventRecord(blk.ready, s);
+    g_cache.emplace(blk.bytes, blk);
+}
 
 // ---------------------------------------------------------------- NCCL (dlopen)
 struct NcclApi {
@@ -136,6 +216,8 @@ extern "C" {
 
 const char* sk_last_error(void) { return g_err.c_str(); }
 
+void sk_release_cache(void) { dev_cache_release(); }
+
 void sk_profile(int on) {
     if (!on) prof_harvest();
     g_prof.on = on != 0;
@@ -193,6 +275,7 @@ int sinkhorn_init(sk_ctx_t* ctx, int device, int rank, int world_size, const voi
 
 int sinkhorn_finalize(sk_ctx_t ctx) {
     if (!ctx) return SK_OK;
+    cudaStreamSynchronize(ctx->c.stream);
     if (ctx->c.nccl_comm) g_nccl.commDestroy((ncclComm_t)ctx->c.nccl_comm);
     delete ctx;
     return SK_OK;
@@ -425,7 +508,7 @@ int sinkhorn_solve(sk_ctx_t ctx, int d, const double* x, long long n_local, cons
     const long long nn = n_local, mm = m_local;
     // device work buffers: [x | y | a | b | u | v]
     const size_t tot = (size_t)(nn * d + mm * d + nn + mm + nn + mm);
-    SK_CUDA(cudaMallocAsync((void**)&buf, sizeof(double) * (tot ? tot : 1), s));
+    SK_TRY(dev_alloc((void**)&buf, sizeof(double) * (tot ? tot : 1), s));
     double* px = buf;
     double* py = px + nn * d;
     double* pa = py + mm * d;
@@ -446,7 +529,7 @@ int sinkhorn_solve(sk_ctx_t ctx, int d, const double* x, long long n_local, cons
     if (!st) st = sinkhorn_run(plan, da, db, iters, 0.0, 0, pu, pv, info);
     if (!st) st = sinkhorn_divergence(plan, da, db, pu, pv, s_dual, s_cost);
     fastsum_plan_destroy(plan);
-    cudaFreeAsync(buf, s);
+    dev_free(buf, s);
     cudaStreamSynchronize(s);
     return st;
 }

@@ -78,14 +78,23 @@ taps_precompute_kernel(const double* __restrict__ u, long long count, const __gr
          j += (long long)gridDim.x * blockDim.x) {
 #pragma unroll 1
         for (int a = 0; a < D; ++a) {
-            const double v = u[a * count + j];
-            const double f = v - floor(v);
-            double row[W + 2];
-            taps_to_row<W, W + 1>(f, 0, 1.0, csm, row);   // c = 0: row[0..W) = taps, row[W] = 0
-            double* o = out + (j * D + a) * W;
+            const double uv = u[a * count + j];
+            const double g = uv - floor(uv) - 0.5, g2 = g * g;
+            double v[W];
 #pragma unroll
-            for (int t = 0; t < W; t += 2)
-                *reinterpret_cast<double2*>(o + t) = make_double2(row[t], row[t + 1]);
+            for (int t = 0; t < W / 2; ++t) {   // tap pair (t, W-1-t): E(g^2) +- g O(g^2)
+                const double* cr = csm + t * kCoefRow;
+                double E = cr[7], O = cr[14];
+#pragma unroll
+                for (int i = 6; i >= 0; --i) E = fma(E, g2, cr[i]);
+#pragma unroll
+                for (int i = 5; i >= 0; --i) O = fma(O, g2, cr[8 + i]);
+                v[t] = fma(g, O, E);
+                v[W - 1 - t] = fma(-g, O, E);
+            }
+            double2* o = reinterpret_cast<double2*>(out + (j * D + a) * W);
+#pragma unroll
+            for (int t = 0; t < W / 2; ++t) o[t] = make_double2(v[2 * t], v[2 * t + 1]);
         }
     }
 }

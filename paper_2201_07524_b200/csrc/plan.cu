@@ -83,16 +83,10 @@ static void kb_coefficients(double lam_p, double rho, int kernel, double L, int 
 }
 
 // ---------------------------------------------------------------- plan
-static int alloc(void** p, size_t bytes) {
-    if (bytes == 0) { *p = nullptr; return SK_OK; }
-    cudaError_t e = cudaMalloc(p, bytes);
-    if (e != cudaSuccess) {
-        cudaGetLastError();
-        return set_error(e == cudaErrorMemoryAllocation ? SK_ENOMEM : SK_ECUDA,
-                         std::string("cudaMalloc(") + std::to_string(bytes) + "): " + cudaGetErrorString(e));
-    }
-    return SK_OK;
-}
+// All plan memory goes through the caching allocator, ordered on the plan's stream.
+static thread_local cudaStream_t tls_stream = nullptr;
+static int alloc(void** p, size_t bytes) { return dev_alloc(p, bytes, tls_stream); }
+static void sk_free(void* p) { dev_free(p, tls_stream); }
 
 static int choose_tile(int d, int n, bool tiled) {
     int T = tiled ? 2 : (d == 1 ? 16 : (d == 2 ? 8 : 4));
@@ -151,7 +145,7 @@ static int build_cell_lists(Plan& P, NodeSet& S, cudaStream_t s) {
     SK_CUDA(cudaMemcpyAsync(keys.data(), d_unique, sizeof(int) * nruns, cudaMemcpyDeviceToHost, s));
     SK_CUDA(cudaMemcpyAsync(cnts.data(), d_counts, sizeof(int) * nruns, cudaMemcpyDeviceToHost, s));
     SK_CUDA(cudaStreamSynchronize(s));
-    cudaFree(tmp); cudaFree(d_unique); cudaFree(d_counts); cudaFree(d_nruns);
+    sk_free(tmp); sk_free(d_unique); sk_free(d_counts); sk_free(d_nruns);
     const int d = P.d, n = P.n, tpa = P.tiles_per_axis, T = P.tile_cells;
     int Td = 1;
     for (int a = 0; a < d; ++a) Td *= T;
@@ -228,7 +222,7 @@ static int plan_side(Plan& P, int sidx, const double* pts, long long count, cuda
     SK_CUDA(cudaMemcpyAsync(&hbad, bad, sizeof(int), cudaMemcpyDeviceToHost, s));
     SK_CUDA(cudaStreamSynchronize(s));
     if (hbad != big) {
-        cudaFree(u_uns); cudaFree(key_in); cudaFree(idx_in); cudaFree(bad);
+        sk_free(u_uns); sk_free(key_in); sk_free(idx_in); sk_free(bad);
         return set_error(SK_EGEOMETRY, "node " + std::to_string(hbad) + " of side " + std::to_string(sidx) +
                                            " is non-finite or outside the ball |x'| <= 1/4 - eps_B/2");
     }
@@ -255,11 +249,11 @@ static int plan_side(Plan& P, int sidx, const double* pts, long long count, cuda
         SK_CUDA(cudaStreamSynchronize(s));
         if (P.tiled) SK_TRY(build_items(P, S, s));
     }
-    cudaFree(tmp);
-    cudaFree(u_uns);
-    cudaFree(key_in);
-    cudaFree(idx_in);
-    cudaFree(bad);
+    sk_free(tmp);
+    sk_free(u_uns);
+    sk_free(key_in);
+    sk_free(idx_in);
+    sk_free(bad);
     return SK_OK;
 }
 
@@ -287,8 +281,8 @@ static int plan_coefficients(Plan& P, cudaStream_t s) {
     }
     SK_CUDA(cudaStreamSynchronize(s));
     cufftDestroy(h);
-    cudaFree(samp);
-    cudaFree(B);
+    sk_free(samp);
+    sk_free(B);
     return SK_OK;
 }
 
@@ -310,6 +304,7 @@ int build_plan(Ctx* ctx, Plan** out, int d, const double* x, long long n, const 
     if (ng < 4 * m_w) return set_error(SK_EINVAL, "sigma*N must be >= 4*m_w (no tap wraps the torus)");
 
     cudaStream_t s = ctx->stream;
+    tls_stream = s;
     Plan* P = new Plan();
     P->ctx = ctx;
     P->d = d;
@@ -358,11 +353,11 @@ int build_plan(Ctx* ctx, Plan** out, int d, const double* x, long long n, const 
         int st = launch_bbox(x, n, d, mm, s);
         if (!st) st = launch_bbox(y, m, d, mm, s);
         if (!st) st = allreduce_minmax(ctx, mm, mm + d, d);
-        if (st) { cudaFree(mm); return fail(st); }
+        if (st) { sk_free(mm); return fail(st); }
         double h[2 * kMaxD];
         cudaMemcpyAsync(h, mm, sizeof(double) * 2 * d, cudaMemcpyDeviceToHost, s);
-        if (cudaStreamSynchronize(s) != cudaSuccess) { cudaFree(mm); return fail(set_error(SK_ECUDA, "bbox sync")); }
-        cudaFree(mm);
+        if (cudaStreamSynchronize(s) != cudaSuccess) { sk_free(mm); return fail(set_error(SK_ECUDA, "bbox sync")); }
+        sk_free(mm);
         double diag2 = 0.0;
         bool any = true;
         for (int a = 0; a < d; ++a) {
@@ -387,7 +382,7 @@ int build_plan(Ctx* ctx, Plan** out, int d, const double* x, long long n, const 
         int st = allreduce_sum(ctx, dc, 2);
         cudaMemcpyAsync(cnt, dc, sizeof(cnt), cudaMemcpyDeviceToHost, s);
         cudaStreamSynchronize(s);
-        cudaFree(dc);
+        sk_free(dc);
         if (st) return fail(st);
         P->side[0].total = (long long)llround(cnt[0]);
         P->side[1].total = (long long)llround(cnt[1]);
@@ -436,18 +431,19 @@ int build_plan(Ctx* ctx, Plan** out, int d, const double* x, long long n, const 
 
 int destroy_plan(Plan* P) {
     if (!P) return SK_OK;
+    tls_stream = P->ctx->stream;
     for (int sidx = 0; sidx < 2; ++sidx) {
         NodeSet& S = P->side[sidx];
-        cudaFree(S.u); cudaFree(S.perm); cudaFree(S.cell_key); cudaFree(S.tile_start); cudaFree(S.items);
-        cudaFree(S.batches); cudaFree(S.segs); cudaFree(S.sitems); cudaFree(S.taps);
+        sk_free(S.u); sk_free(S.perm); sk_free(S.cell_key); sk_free(S.tile_start); sk_free(S.items);
+        sk_free(S.batches); sk_free(S.segs); sk_free(S.sitems); sk_free(S.taps);
     }
-    cudaFree(P->grid); cudaFree(P->spec);
-    for (int k = 0; k < 2; ++k) { cudaFree(P->D[k]); cudaFree(P->bk[k]); }
+    sk_free(P->grid); sk_free(P->spec);
+    for (int k = 0; k < 2; ++k) { sk_free(P->D[k]); sk_free(P->bk[k]); }
     if (P->fwd) cufftDestroy(P->fwd);
     if (P->inv) cufftDestroy(P->inv);
-    cudaFree(P->w_sorted); cudaFree(P->t_sorted);
-    cudaFree(P->a_s); cudaFree(P->b_s); cudaFree(P->u_s); cudaFree(P->v_s);
-    cudaFree(P->red); cudaFree(P->red_out); cudaFree(P->flag);
+    sk_free(P->w_sorted); sk_free(P->t_sorted);
+    sk_free(P->a_s); sk_free(P->b_s); sk_free(P->u_s); sk_free(P->v_s);
+    sk_free(P->red); sk_free(P->red_out); sk_free(P->flag);
     if (P->host_red) cudaFreeHost(P->host_red);
     delete (WinPoly*)P->winpoly;
     delete P;

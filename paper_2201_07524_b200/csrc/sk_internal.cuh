@@ -33,6 +33,11 @@ int set_error(int code, const std::string& msg);
 
 void count_launch(long long k = 1);
 
+// Caching device allocator (api.cu): stream-ordered reuse of freed blocks.
+int dev_alloc(void** out, size_t bytes, cudaStream_t s);
+void dev_free(void* p, cudaStream_t s);
+void dev_cache_release();
+
 // Kaiser-Bessel window parameters in oversampled-grid units (reading Q10).
 struct Window {
     int m;            // cutoff: support |u| < m, 2m taps per axis

@@ -271,9 +271,11 @@ def test_errors(capi, ctx):
 
 
 def test_host_buffer_solve_matches_device(capi, ctx):
-    cfg = get("c1")
+    cfg = get("c3").with_(n=20000, m=15000)
     x, y, a, b = make_inputs(cfg)
-    h = capi.sinkhorn_solve(ctx, x, y, a, b, cfg.lam, 96, iters=50, inputs_on_host=True)
-    d_ = capi.sinkhorn_solve(ctx, dev(x), dev(y), dev(a), dev(b), cfg.lam, 96, iters=50)
-    # identical inputs; only the order of the FP64 atomics in the spread differs
-    assert abs(h[0] - d_[0]) <= 1e-10 * abs(h[0]) and abs(h[1] - d_[1]) <= 1e-10 * abs(h[1])
+    a, b = a / a.sum(), b / b.sum()
+    h = capi.sinkhorn_solve(ctx, x, y, a, b, cfg.lam, cfg.N, cfg.sigma, cfg.m_w, iters=30, inputs_on_host=True)
+    d_ = capi.sinkhorn_solve(ctx, dev(x), dev(y), dev(a), dev(b), cfg.lam, cfg.N, cfg.sigma, cfg.m_w, iters=30)
+    # identical inputs; only the order of the FP64 atomics in the spread flush differs
+    # (well-conditioned workload, kappa ~ 10^1.6, so rounding is not amplified)
+    assert abs(h[0] - d_[0]) <= 1e-12 * abs(h[0]) and abs(h[1] - d_[1]) <= 1e-12 * abs(h[1])
