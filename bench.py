@@ -113,7 +113,14 @@ def cpu_oracle_rate(cfg, budget_s: float):
     """Time the oracle (dense log-domain Alg. 1, as it stands) on a bounded seeded subsample
     of the workload; return (it/s extrapolated to the full workload, description)."""
     from oracle import dense
-    x, y, a, b = make_inputs(cfg.with_(n=min(cfg.n, 200_000), m=min(cfg.m, 200_000)))
+    if cfg.x_dist == "jitter_grid":      # grid generators need the full K x K grid
+        x, y, a, b = make_inputs(cfg)
+        rng = np.random.default_rng(0)
+        ix = rng.permutation(x.shape[0])[:200_000]
+        iy = rng.permutation(y.shape[0])[:200_000]
+        x, y, a, b = x[ix], y[iy], a[ix], b[iy]
+    else:
+        x, y, a, b = make_inputs(cfg.with_(n=min(cfg.n, 200_000), m=min(cfg.m, 200_000)))
     # calibrate: one iteration on a small subsample, then size the sample to the budget
     k = min(2000, x.shape[0], y.shape[0])
     t0 = time.perf_counter()
