@@ -331,6 +331,7 @@ def main():
                                     f"{pk.get('sm_max_mhz')} (DESIGN.md)",
                      "hbm_frac": bytes_alg / (avg_ms * 1e-3) / (pk["hbm_gbs"] * 1e9),
                      "avg_launch_ms": avg_ms},
+        "plan_ms_per_step": stage_ms.get("plan", (0, 0.0))[1] / args.steps,
         "stage_ms_total": {s: v[1] for s, v in stage_ms.items()},
         "stage_share_of_step": stage_share,
         "gpu_launches": int(launches),

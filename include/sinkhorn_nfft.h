@@ -133,7 +133,9 @@ int nfft_interp(sk_plan_t plan, int side, const double* grid, double* t);
 /* Plan-time quantities (host outputs):
  * fastsum_plan_info: out[0..2] centre, out[3] rho, out[4] lambda', out[5] L, out[6] n = sigma N,
  *   out[7] band length per axis (N+1), out[8] d, out[9] total nodes x (all ranks),
- *   out[10] total nodes y (all ranks).
+ *   out[10] total nodes y (all ranks), out[11..13] first grid index of the exchange box per
+ *   axis, out[14..16] its extent per axis (the cells any node window touches; only this box
+ *   is all-reduced across ranks), out[17] box cells. out must hold 18 doubles.
  * fastsum_coefficients: b (host, (N+1)^d, index prod over axes of (k_a + N/2), row-major):
  *   the Fourier coefficients b_k of K~_per (kernel 0 or 1) on k in {-N/2..N/2}^d. */
 int fastsum_plan_info(sk_plan_t plan, double* out);

@@ -105,7 +105,7 @@ def sk_launch_count() -> int:
     return int(_lib.sk_launch_count())
 
 
-STAGES = ("spread", "allreduce", "fft_fwd", "multiply", "fft_inv", "interp", "update")
+STAGES = ("spread", "allreduce", "fft_fwd", "multiply", "fft_inv", "interp", "update", "plan")
 
 
 def sk_profile(on: bool) -> None:
@@ -192,10 +192,12 @@ class Plan:
             pass
 
     def info(self) -> dict:
-        out = (ctypes.c_double * 16)()
+        out = (ctypes.c_double * 18)()
         _check(_lib.fastsum_plan_info(self.handle, out))
         return dict(centre=list(out[0:3]), rho=out[3], lambda_p=out[4], L=out[5], n_grid=out[6],
-                    band=out[7], d=out[8], total_x=out[9], total_y=out[10])
+                    band=out[7], d=out[8], total_x=out[9], total_y=out[10],
+                    box_lo=[int(v) for v in out[11:14]], box_n=[int(v) for v in out[14:17]],
+                    box_size=int(out[17]))
 
     def coefficients(self, kernel: int = 0):
         import numpy as np

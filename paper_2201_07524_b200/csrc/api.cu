@@ -6,6 +6,9 @@
 #include <math.h>
 #include <nccl.h>
 #include <atomic>
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <map>
 #include <mutex>
 #include <string>
@@ -201,6 +204,16 @@ void prof_harvest() {
     }
 }
 
+void plan_trace(const char* phase, cudaStream_t s) {
+    static const bool on = getenv("SK_PLAN_TRACE") != nullptr;
+    if (!on) return;
+    static auto t0 = std::chrono::steady_clock::now();
+    cudaStreamSynchronize(s);
+    const auto t = std::chrono::steady_clock::now();
+    fprintf(stderr, "[plan] %-28s %9.2f ms\n", phase, std::chrono::duration<double, std::milli>(t - t0).count());
+    t0 = t;
+}
+
 // reduction output slots inside Plan::red_out (each slot: result + partial scratch)
 constexpr int kSlot = 608;
 static inline double* slot(Plan& P, int k) { return P.red_out + k * kSlot; }
@@ -224,7 +237,7 @@ void sk_profile(int on) {
 }
 
 // out[2*k] = launches timed, out[2*k+1] = total ms, for stage k in {spread, allreduce,
-// fft_fwd, multiply, fft_inv, interp, update}; reset != 0 clears the accumulators.
+// fft_fwd, multiply, fft_inv, interp, update, plan}; reset != 0 clears the accumulators.
 int sk_profile_read(double* out, int nstages, int reset) {
     prof_harvest();
     for (int st = 0; st < ST_COUNT && st < nstages; ++st) {
@@ -348,6 +361,11 @@ int fastsum_plan_info(sk_plan_t plan, double* out) {
     out[8] = P.d;
     out[9] = (double)P.side[0].total;
     out[10] = (double)P.side[1].total;
+    for (int a = 0; a < 3; ++a) {
+        out[11 + a] = a < P.d ? P.box_lo[a] : 0.0;
+        out[14 + a] = a < P.d ? P.box_n[a] : 1.0;
+    }
+    out[17] = (double)P.box_size;
     return SK_OK;
 }
 
@@ -525,7 +543,9 @@ int sinkhorn_solve(sk_ctx_t ctx, int d, const double* x, long long n_local, cons
     SK_TRY(launch_fill(pu, nn, 1.0, s));
     SK_TRY(launch_fill(pv, mm, 1.0, s));
     sk_plan_t plan = nullptr;
+    prof_begin(ST_PLAN, s);
     int st = fastsum_plan(ctx, &plan, d, dx, nn, dy, mm, lambda, N, sigma, m_w, eps_B, p_smooth);
+    prof_end(ST_PLAN, s);
     if (!st) st = sinkhorn_run(plan, da, db, iters, 0.0, 0, pu, pv, info);
     if (!st) st = sinkhorn_divergence(plan, da, db, pu, pv, s_dual, s_cost);
     fastsum_plan_destroy(plan);

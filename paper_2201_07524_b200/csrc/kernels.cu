@@ -239,6 +239,43 @@ __global__ void fill_kernel(double* p, long long count, double v) {
          k += (long long)gridDim.x * blockDim.x)
         p[k] = v;
 }
+// ------------------------------------------------------------------ a3: box pack / unpack
+struct BoxParams { long long lo_off; long long stride[kMaxD]; int dims[kMaxD]; int d; };
+
+template <int DIR>
+__global__ void box_copy_kernel(double* __restrict__ grid, double* __restrict__ buf, long long total,
+                                BoxParams bp) {
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
+         i += (long long)gridDim.x * blockDim.x) {
+        long long rest = i, off = bp.lo_off;
+        for (int a = bp.d - 1; a >= 0; --a) {
+            off += (rest % bp.dims[a]) * bp.stride[a];
+            rest /= bp.dims[a];
+        }
+        if (DIR == 0) buf[i] = grid[off];
+        else grid[off] = buf[i];
+    }
+}
+
+int launch_box_copy(const Plan& P, double* grid, double* buf, int dir, cudaStream_t s) {
+    if (P.box_size <= 0) return SK_OK;
+    BoxParams bp;
+    bp.d = P.d;
+    long long st = 1;
+    bp.lo_off = 0;
+    for (int a = P.d - 1; a >= 0; --a) {
+        bp.stride[a] = st;
+        bp.dims[a] = P.box_n[a];
+        bp.lo_off += (long long)P.box_lo[a] * st;
+        st *= P.n;
+    }
+    const int g = grid_for(P.box_size, 256);
+    if (dir == 0) box_copy_kernel<0><<<g, 256, 0, s>>>(grid, buf, P.box_size, bp);
+    else box_copy_kernel<1><<<g, 256, 0, s>>>(grid, buf, P.box_size, bp);
+    SK_LAUNCH_CHECK();
+    return SK_OK;
+}
+
 int launch_fill(double* p, long long count, double v, cudaStream_t s) {
     if (count <= 0) return SK_OK;
     fill_kernel<<<grid_for(count, 256), 256, 0, s>>>(p, count, v);

@@ -120,79 +120,178 @@ static int build_items(Plan& P, NodeSet& S, cudaStream_t s) {
     return SK_OK;
 }
 
-// DMMA path: nodes are sorted by key = (2^3 super-tile << 3) | cell bits. Run-length encode
-// the keys (one run per non-empty cell) and build on the host
+// DMMA path: nodes are sorted by key = (super-tile << log2 Td) | cell bits. Run-length encode
+// the keys (one run per non-empty cell) and build, on the device,
 //   batches: <= 32 nodes of one cell (interp work unit of a warp),
-//   segs:    <= kSegMax nodes of one cell (spread),
-//   sitems:  consecutive segs of one super-tile, <= kSpreadItemMax nodes (spread work unit of a
-//            warp, flushed once with coalesced atomics), sorted by size for balance.
+//   segs:    <= seg_max nodes of one cell (spread),
+//   sitems:  consecutive segs of one super-tile, <= item_max nodes (spread work unit of a
+//            warp, flushed once with coalesced atomics), sorted by size (stable) for balance.
+struct CellGeom { int d, n, tpa, T, Td; };
+
+__device__ __forceinline__ int cell_of_key(int key, const CellGeom g) {
+    const int tile = key / g.Td;
+    int sub = key % g.Td, rest = tile, tc[3], cc[3];
+    for (int a = g.d - 1; a >= 0; --a) { tc[a] = rest % g.tpa; rest /= g.tpa; }
+    for (int a = g.d - 1; a >= 0; --a) { cc[a] = g.T * tc[a] + sub % g.T; sub /= g.T; }
+    int cell = 0;
+    for (int a = 0; a < g.d; ++a) cell = cell * g.n + cc[a];
+    return cell;
+}
+
+// per run: interp batches; per tile-head run: number of segs / items of its tile (greedy
+// fill in run order, exactly the sequential rule)
+__global__ void cell_counts_kernel(const int* __restrict__ keys, const int* __restrict__ cnts, int nruns,
+                                   CellGeom g, int seg_max, int item_max, int* __restrict__ nb,
+                                   int* __restrict__ nseg, int* __restrict__ nitem) {
+    const int r = blockIdx.x * blockDim.x + threadIdx.x;
+    if (r >= nruns) return;
+    nb[r] = (cnts[r] + 31) / 32;
+    const int tile = keys[r] / g.Td;
+    int ns = 0, ni = 0;
+    if (r == 0 || keys[r - 1] / g.Td != tile) {
+        int fill = 0;
+        for (int q = r; q < nruns && keys[q] / g.Td == tile; ++q)
+            for (int b = 0; b < cnts[q]; b += seg_max) {
+                const int c = min(seg_max, cnts[q] - b);
+                if (ni == 0 || fill + c > item_max) { ++ni; fill = 0; }
+                fill += c;
+                ++ns;
+            }
+    }
+    nseg[r] = ns;
+    nitem[r] = ni;
+}
+
+__global__ void cell_write_kernel(const int* __restrict__ keys, const int* __restrict__ cnts,
+                                  const int* __restrict__ rstart, int nruns, CellGeom g, int seg_max,
+                                  int item_max, const int* __restrict__ nb_off, const int* __restrict__ seg_off,
+                                  const int* __restrict__ item_off, CellBatch* __restrict__ batches,
+                                  CellBatch* __restrict__ segs, SpreadItem* __restrict__ items,
+                                  int* __restrict__ item_cnt) {
+    const int r = blockIdx.x * blockDim.x + threadIdx.x;
+    if (r >= nruns) return;
+    const int cell = cell_of_key(keys[r], g), cnt = cnts[r], st = rstart[r];
+    int o = nb_off[r];
+    for (int b = 0; b < cnt; b += 32) batches[o++] = CellBatch{cell, st + b, min(32, cnt - b), 0};
+    const int tile = keys[r] / g.Td;
+    if (!(r == 0 || keys[r - 1] / g.Td != tile)) return;
+    int so = seg_off[r], io = item_off[r] - 1, fill = 0;
+    bool first = true;
+    for (int q = r; q < nruns && keys[q] / g.Td == tile; ++q) {
+        const int cq = cell_of_key(keys[q], g);
+        for (int b = 0; b < cnts[q]; b += seg_max) {
+            const int c = min(seg_max, cnts[q] - b);
+            if (first || fill + c > item_max) {
+                if (!first) { items[io].count = fill; item_cnt[io] = fill; }
+                ++io;
+                items[io] = SpreadItem{tile, so, so, 0};
+                fill = 0;
+                first = false;
+            }
+            segs[so++] = CellBatch{cq, rstart[q] + b, c, 0};
+            items[io].seg_end = so;
+            fill += c;
+        }
+    }
+    if (!first) { items[io].count = fill; item_cnt[io] = fill; }
+}
+
+__global__ void iota_kernel(int* __restrict__ o, int n) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) o[i] = i;
+}
+
+__global__ void gather_items_kernel(const SpreadItem* __restrict__ in, const int* __restrict__ order, int n,
+                                    SpreadItem* __restrict__ out) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) out[i] = in[order[i]];
+}
+
 static int build_cell_lists(Plan& P, NodeSet& S, cudaStream_t s) {
     const long long count = S.count;
-    int *d_unique = nullptr, *d_counts = nullptr, *d_nruns = nullptr;
-    SK_TRY(alloc((void**)&d_unique, sizeof(int) * count));
-    SK_TRY(alloc((void**)&d_counts, sizeof(int) * count));
-    SK_TRY(alloc((void**)&d_nruns, sizeof(int)));
-    size_t tb = 0;
-    cub::DeviceRunLengthEncode::Encode(nullptr, tb, S.cell_key, d_unique, d_counts, d_nruns, (int)count, s);
-    void* tmp = nullptr;
-    SK_TRY(alloc(&tmp, tb));
-    SK_CUDA(cub::DeviceRunLengthEncode::Encode(tmp, tb, S.cell_key, d_unique, d_counts, d_nruns, (int)count, s));
-    count_launch(2);
-    int nruns = 0;
-    SK_CUDA(cudaMemcpyAsync(&nruns, d_nruns, sizeof(int), cudaMemcpyDeviceToHost, s));
-    SK_CUDA(cudaStreamSynchronize(s));
-    std::vector<int> keys(nruns), cnts(nruns);
-    SK_CUDA(cudaMemcpyAsync(keys.data(), d_unique, sizeof(int) * nruns, cudaMemcpyDeviceToHost, s));
-    SK_CUDA(cudaMemcpyAsync(cnts.data(), d_counts, sizeof(int) * nruns, cudaMemcpyDeviceToHost, s));
-    SK_CUDA(cudaStreamSynchronize(s));
-    sk_free(tmp); sk_free(d_unique); sk_free(d_counts); sk_free(d_nruns);
     const int d = P.d, n = P.n, tpa = P.tiles_per_axis, T = P.tile_cells;
     int Td = 1;
     for (int a = 0; a < d; ++a) Td *= T;
-    std::vector<CellBatch> batches, segs;
-    std::vector<SpreadItem> items;
-    batches.reserve(count / 16 + nruns);
-    long long start = 0;
-    int cur_tile = -1;
+    const CellGeom g{d, n, tpa, T, Td};
     // spread work-unit size: enough items to keep ~4 per resident warp busy (148 SMs x 8
     // warps), at most kSpreadItemMax nodes (one region flush per item)
     const int item_max = (int)std::max(128LL, std::min((long long)kSpreadItemMax, count / 4736));
     const int seg_max = std::min(kSegMax, item_max);
-    for (int r = 0; r < nruns; ++r) {
-        const int key = keys[r], cnt = cnts[r];
-        const int tile = key / Td, sub = key % Td;
-        int tc[3], cc[3];
-        int rest = tile;
-        for (int a = d - 1; a >= 0; --a) { tc[a] = rest % tpa; rest /= tpa; }
-        int digits = sub;
-        for (int a = d - 1; a >= 0; --a) { cc[a] = T * tc[a] + digits % T; digits /= T; }
-        int cell = 0;
-        for (int a = 0; a < d; ++a) cell = cell * n + cc[a];
-        for (int b = 0; b < cnt; b += 32) batches.push_back(CellBatch{cell, (int)(start + b), std::min(32, cnt - b), 0});
-        for (int b = 0; b < cnt; b += seg_max) {
-            const int c = std::min(seg_max, cnt - b);
-            if (tile != cur_tile || items.back().count + c > item_max) {
-                items.push_back(SpreadItem{tile, (int)segs.size(), (int)segs.size(), 0});
-                cur_tile = tile;
-            }
-            segs.push_back(CellBatch{cell, (int)(start + b), c, 0});
-            items.back().seg_end = (int)segs.size();
-            items.back().count += c;
-        }
-        start += cnt;
-    }
-    std::stable_sort(items.begin(), items.end(),
-                     [](const SpreadItem& a, const SpreadItem& b) { return a.count > b.count; });
-    S.nbatches = (int)batches.size();
-    S.nsegs = (int)segs.size();
-    S.nsitems = (int)items.size();
-    SK_TRY(alloc(&S.batches, sizeof(CellBatch) * batches.size()));
-    SK_TRY(alloc(&S.segs, sizeof(CellBatch) * segs.size()));
-    SK_TRY(alloc(&S.sitems, sizeof(SpreadItem) * items.size()));
-    SK_CUDA(cudaMemcpyAsync(S.batches, batches.data(), sizeof(CellBatch) * batches.size(), cudaMemcpyHostToDevice, s));
-    SK_CUDA(cudaMemcpyAsync(S.segs, segs.data(), sizeof(CellBatch) * segs.size(), cudaMemcpyHostToDevice, s));
-    SK_CUDA(cudaMemcpyAsync(S.sitems, items.data(), sizeof(SpreadItem) * items.size(), cudaMemcpyHostToDevice, s));
+
+    // run-length encode the sorted keys; 7 int arrays of nruns (<= count) entries
+    int* buf = nullptr;
+    SK_TRY(alloc((void**)&buf, sizeof(int) * (7 * count + 16)));
+    int *keys = buf, *cnts = keys + count, *rstart = cnts + count, *nb = rstart + count,
+        *nseg = nb + count, *nitem = nseg + count, *scratch = nitem + count, *small = scratch + count;
+    size_t tb = 0, tb2 = 0;
+    cub::DeviceRunLengthEncode::Encode(nullptr, tb, S.cell_key, keys, cnts, small, (int)count, s);
+    cub::DeviceScan::ExclusiveSum(nullptr, tb2, cnts, rstart, (int)count, s);
+    tb = std::max(tb, tb2);
+    void* tmp = nullptr;
+    SK_TRY(alloc(&tmp, tb));
+    SK_CUDA(cub::DeviceRunLengthEncode::Encode(tmp, tb, S.cell_key, keys, cnts, small, (int)count, s));
+    count_launch(2);
+    int nruns = 0;
+    SK_CUDA(cudaMemcpyAsync(&nruns, small, sizeof(int), cudaMemcpyDeviceToHost, s));
     SK_CUDA(cudaStreamSynchronize(s));
+    const int thr = 256, blk = (nruns + thr - 1) / thr;
+    SK_CUDA(cub::DeviceScan::ExclusiveSum(tmp, tb, cnts, rstart, nruns, s));
+    cell_counts_kernel<<<blk, thr, 0, s>>>(keys, cnts, nruns, g, seg_max, item_max, nb, nseg, nitem);
+    SK_CUDA(cudaGetLastError());
+    // totals = last exclusive prefix + last count (in-place scans)
+    int last[3];
+    SK_CUDA(cudaMemcpyAsync(small + 4, nb + nruns - 1, sizeof(int), cudaMemcpyDeviceToDevice, s));
+    SK_CUDA(cudaMemcpyAsync(small + 5, nseg + nruns - 1, sizeof(int), cudaMemcpyDeviceToDevice, s));
+    SK_CUDA(cudaMemcpyAsync(small + 6, nitem + nruns - 1, sizeof(int), cudaMemcpyDeviceToDevice, s));
+    SK_CUDA(cub::DeviceScan::ExclusiveSum(tmp, tb, nb, nb, nruns, s));
+    SK_CUDA(cub::DeviceScan::ExclusiveSum(tmp, tb, nseg, nseg, nruns, s));
+    SK_CUDA(cub::DeviceScan::ExclusiveSum(tmp, tb, nitem, nitem, nruns, s));
+    count_launch(5);
+    SK_CUDA(cudaMemcpyAsync(small + 7, nb + nruns - 1, sizeof(int), cudaMemcpyDeviceToDevice, s));
+    SK_CUDA(cudaMemcpyAsync(small + 8, nseg + nruns - 1, sizeof(int), cudaMemcpyDeviceToDevice, s));
+    SK_CUDA(cudaMemcpyAsync(small + 9, nitem + nruns - 1, sizeof(int), cudaMemcpyDeviceToDevice, s));
+    int h[10];
+    SK_CUDA(cudaMemcpyAsync(h, small, sizeof(int) * 10, cudaMemcpyDeviceToHost, s));
+    SK_CUDA(cudaStreamSynchronize(s));
+    last[0] = h[4] + h[7]; last[1] = h[5] + h[8]; last[2] = h[6] + h[9];
+    S.nbatches = last[0];
+    S.nsegs = last[1];
+    S.nsitems = last[2];
+    SK_TRY(alloc(&S.batches, sizeof(CellBatch) * std::max(S.nbatches, 1)));
+    SK_TRY(alloc(&S.segs, sizeof(CellBatch) * std::max(S.nsegs, 1)));
+    SK_TRY(alloc(&S.sitems, sizeof(SpreadItem) * std::max(S.nsitems, 1)));
+    SpreadItem* items_unsorted = nullptr;
+    SK_TRY(alloc((void**)&items_unsorted, sizeof(SpreadItem) * std::max(S.nsitems, 1)));
+    // item counts and identity order in the (now free) cnts-sized scratch arrays
+    int *icnt = scratch, *icnt_sorted = nullptr, *ord = nullptr, *ord_sorted = nullptr;
+    SK_TRY(alloc((void**)&icnt_sorted, sizeof(int) * 3 * std::max(S.nsitems, 1)));
+    ord = icnt_sorted + std::max(S.nsitems, 1);
+    ord_sorted = ord + std::max(S.nsitems, 1);
+    cell_write_kernel<<<blk, thr, 0, s>>>(keys, cnts, rstart, nruns, g, seg_max, item_max, nb, nseg, nitem,
+                                          (CellBatch*)S.batches, (CellBatch*)S.segs, items_unsorted, icnt);
+    SK_CUDA(cudaGetLastError());
+    count_launch(2);
+    // stable sort of the items by node count, largest first (static round-robin balance)
+    const int ni = S.nsitems;
+    if (ni > 0) {
+        size_t tb3 = 0;
+        SK_CUDA(cub::DeviceRadixSort::SortPairsDescending(nullptr, tb3, icnt, icnt_sorted, ord, ord_sorted, ni, 0,
+                                                          32, s));
+        void* tmp3 = nullptr;
+        SK_TRY(alloc(&tmp3, tb3));
+        iota_kernel<<<(ni + 255) / 256, 256, 0, s>>>(ord, ni);
+        SK_CUDA(cub::DeviceRadixSort::SortPairsDescending(tmp3, tb3, icnt, icnt_sorted, ord, ord_sorted, ni, 0,
+                                                          32, s));
+        gather_items_kernel<<<(ni + 255) / 256, 256, 0, s>>>(items_unsorted, ord_sorted, ni,
+                                                             (SpreadItem*)S.sitems);
+        SK_CUDA(cudaGetLastError());
+        count_launch(4);
+        sk_free(tmp3);
+    }
+    sk_free(icnt_sorted);
+    sk_free(items_unsorted);
+    sk_free(tmp);
+    sk_free(buf);
     return SK_OK;
 }
 
@@ -217,7 +316,9 @@ static int plan_side(Plan& P, int sidx, const double* pts, long long count, cuda
     SK_TRY(alloc((void**)&S.u, sizeof(double) * P.d * count));
     const int big = 0x7fffffff;
     SK_CUDA(cudaMemcpyAsync(bad, &big, sizeof(int), cudaMemcpyHostToDevice, s));
+    plan_trace("side: alloc", s);
     SK_TRY(launch_scale_key(P, pts, count, u_uns, key_in, idx_in, bad, s));
+    plan_trace("side: scale_key", s);
     int hbad = 0;
     SK_CUDA(cudaMemcpyAsync(&hbad, bad, sizeof(int), cudaMemcpyDeviceToHost, s));
     SK_CUDA(cudaStreamSynchronize(s));
@@ -239,11 +340,15 @@ static int plan_side(Plan& P, int sidx, const double* pts, long long count, cuda
     SK_CUDA(cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, key_in, S.cell_key, idx_in, S.perm, (int)count,
                                             0, end_bit, s));
     count_launch(4);
+    plan_trace("side: sort", s);
     SK_TRY(launch_gather_coords(P, u_uns, S.perm, count, S.u, s));
+    plan_trace("side: gather", s);
     if (P.dmma) {
         SK_TRY(build_cell_lists(P, S, s));
+        plan_trace("side: cell lists", s);
         SK_TRY(alloc((void**)&S.taps, sizeof(double) * count * P.d * 2 * P.win.m));
         SK_TRY(launch_taps(P, sidx, s));
+        plan_trace("side: taps", s);
     } else {
         SK_TRY(launch_tile_offsets(S.cell_key, count, S.ntiles, S.tile_start, s));
         SK_CUDA(cudaStreamSynchronize(s));
@@ -342,6 +447,7 @@ int build_plan(Ctx* ctx, Plan** out, int d, const double* x, long long n, const 
 
     auto fail = [&](int code) { destroy_plan(P); return code; };
 
+    plan_trace("start", s);
     // ---- a0: geometry (bbox over x u y on all ranks), reading Q6
     double* mm = nullptr;
     if (alloc((void**)&mm, sizeof(double) * 2 * kMaxD)) return fail(SK_ENOMEM);
@@ -372,6 +478,18 @@ int build_plan(Ctx* ctx, Plan** out, int d, const double* x, long long n, const 
         const double diag = sqrt(diag2);
         P->rho = diag > 0.0 ? P->L / diag : 1.0;
         P->lambda_p = lambda / (P->rho * P->rho);
+        // touched grid box: cells floor(u) - m + 1 .. floor(u) + m of every node, u = n(rho(x -
+        // centre) + 1/2) over the global bbox, one cell of margin against rounding
+        P->box_size = 1;
+        for (int a = 0; a < d; ++a) {
+            const double ulo = ng * (P->rho * (h[a] - P->centre[a]) + 0.5);
+            const double uhi = ng * (P->rho * (h[d + a] - P->centre[a]) + 0.5);
+            const int lo = std::max(0, (int)floor(ulo) - m_w);
+            const int hi = std::min(ng - 1, (int)floor(uhi) + m_w + 1);
+            P->box_lo[a] = lo;
+            P->box_n[a] = hi - lo + 1;
+            P->box_size *= P->box_n[a];
+        }
     }
     // global counts
     {
@@ -387,6 +505,7 @@ int build_plan(Ctx* ctx, Plan** out, int d, const double* x, long long n, const 
         P->side[0].total = (long long)llround(cnt[0]);
         P->side[1].total = (long long)llround(cnt[1]);
     }
+    plan_trace("bbox + counts", s);
     // ---- a0: scale, bin, sort (both sides)
     int st = plan_side(*P, 0, x, n, s);
     if (!st) st = plan_side(*P, 1, y, m, s);
@@ -399,6 +518,7 @@ int build_plan(Ctx* ctx, Plan** out, int d, const double* x, long long n, const 
     if ((st = alloc((void**)&P->bk[0], sizeof(double) * full))) return fail(st);
     if ((st = alloc((void**)&P->bk[1], sizeof(double) * full))) return fail(st);
     if ((st = plan_coefficients(*P, s))) return fail(st);
+    plan_trace("coefficients", s);
     // ---- grid, spectrum, FFT plans
     if ((st = alloc((void**)&P->grid, sizeof(double) * P->grid_size))) return fail(st);
     if ((st = alloc((void**)&P->spec, sizeof(cufftDoubleComplex) * P->spec_size))) return fail(st);
@@ -411,6 +531,7 @@ int build_plan(Ctx* ctx, Plan** out, int d, const double* x, long long n, const 
         cufftSetStream(P->fwd, s);
         cufftSetStream(P->inv, s);
     }
+    plan_trace("fft plans", s);
     // ---- scratch
     P->max_count = std::max(n, m);
     long long mc = std::max(P->max_count, 1LL);
@@ -420,11 +541,15 @@ int build_plan(Ctx* ctx, Plan** out, int d, const double* x, long long n, const 
     if ((st = alloc((void**)&P->u_s, sizeof(double) * std::max(n, 1LL)))) return fail(st);
     if ((st = alloc((void**)&P->b_s, sizeof(double) * std::max(m, 1LL)))) return fail(st);
     if ((st = alloc((void**)&P->v_s, sizeof(double) * std::max(m, 1LL)))) return fail(st);
+    P->box_exchange = ctx->world > 1 || getenv("SK_FORCE_BOX_EXCHANGE") != nullptr;
+    if (P->box_exchange && (st = alloc((void**)&P->box_buf, sizeof(double) * std::max(P->box_size, 1LL))))
+        return fail(st);
     if ((st = alloc((void**)&P->red, sizeof(double) * 4096))) return fail(st);
     if ((st = alloc((void**)&P->red_out, sizeof(double) * 8192))) return fail(st);
     if ((st = alloc((void**)&P->flag, sizeof(int) * 4))) return fail(st);
     if (cudaMallocHost((void**)&P->host_red, sizeof(double) * 64) != cudaSuccess)
         return fail(set_error(SK_ENOMEM, "cudaMallocHost"));
+    plan_trace("scratch", s);
     *out = P;
     return SK_OK;
 }
@@ -443,7 +568,7 @@ int destroy_plan(Plan* P) {
     if (P->inv) cufftDestroy(P->inv);
     sk_free(P->w_sorted); sk_free(P->t_sorted);
     sk_free(P->a_s); sk_free(P->b_s); sk_free(P->u_s); sk_free(P->v_s);
-    sk_free(P->red); sk_free(P->red_out); sk_free(P->flag);
+    sk_free(P->red); sk_free(P->red_out); sk_free(P->flag); sk_free(P->box_buf);
     if (P->host_red) cudaFreeHost(P->host_red);
     delete (WinPoly*)P->winpoly;
     delete P;
@@ -458,9 +583,15 @@ int apply_sorted(Plan& P, int transpose, int kernel, const double* w_sorted, dou
     SK_CUDA(cudaMemsetAsync(P.grid, 0, sizeof(double) * P.grid_size, s));
     SK_TRY(launch_spread(P, src, w_sorted, P.grid, s));
     prof_end(ST_SPREAD, s);
-    if (P.ctx->world > 1) {
+    if (P.box_exchange) {
+        // a3: sum the partial grids of all ranks over the touched box only (pack, NCCL
+        // all-reduce, unpack; with one rank and SK_FORCE_BOX_EXCHANGE the grid is cleared
+        // in between, which checks that the box holds every nonzero)
         prof_begin(ST_ALLREDUCE, s);
-        SK_TRY(allreduce_sum(P.ctx, P.grid, P.grid_size));
+        SK_TRY(launch_box_copy(P, P.grid, P.box_buf, 0, s));
+        SK_TRY(allreduce_sum(P.ctx, P.box_buf, P.box_size));
+        if (P.ctx->world == 1) SK_CUDA(cudaMemsetAsync(P.grid, 0, sizeof(double) * P.grid_size, s));
+        SK_TRY(launch_box_copy(P, P.grid, P.box_buf, 1, s));
         prof_end(ST_ALLREDUCE, s);
     }
     prof_begin(ST_FFT_FWD, s);

@@ -105,6 +105,13 @@ struct Plan {
     // Sinkhorn state in sorted order
     double* a_s = nullptr; double* b_s = nullptr; double* u_s = nullptr; double* v_s = nullptr;
     long long max_count = 0;
+    // a3 exchange: the grid cells any node's window can touch form one box (same on all
+    // ranks, from the global bbox); only the box is all-reduced (c5: 77^3 of 256^3 cells)
+    int box_lo[kMaxD] = {0, 0, 0};
+    int box_n[kMaxD] = {1, 1, 1};
+    long long box_size = 0;
+    double* box_buf = nullptr;   // packed box (world > 1, or SK_FORCE_BOX_EXCHANGE)
+    bool box_exchange = false;
     int tile_cells = 0;       // tile edge in grid cells (per axis)
     int tiles_per_axis = 0;
     bool tiled = false;       // v2 tiled spread/interp usable (d = 3, 2 m_w in {12, 16})
@@ -134,6 +141,8 @@ int launch_band_coeffs(Plan& P, int kernel, int M, const cufftDoubleComplex* B, 
 int launch_update(Plan& P, int side, const double* t_sorted, const double* p_sorted,
                   double* x_sorted, int want_resid, int iter, cudaStream_t s);
 int launch_fill(double* p, long long count, double v, cudaStream_t s);
+// a3: grid box <-> packed buffer (dir 0: pack grid -> buf, 1: unpack buf -> grid)
+int launch_box_copy(const Plan& P, double* grid, double* buf, int dir, cudaStream_t s);
 int launch_scale_vec(double* p, long long count, const double* scale_dev, cudaStream_t s);
 int launch_reduce_sum_log(const double* p, const double* x, long long count, double* out_dev,
                           int op, cudaStream_t s);
@@ -147,7 +156,9 @@ int destroy_plan(Plan* P);
 int apply_sorted(Plan& P, int transpose, int kernel, const double* w_sorted, double* t_sorted);
 
 // ---- stage profiling (api.cu): CUDA-event pairs around each stage when enabled ----
-enum Stage { ST_SPREAD = 0, ST_ALLREDUCE, ST_FFT_FWD, ST_MULTIPLY, ST_FFT_INV, ST_INTERP, ST_UPDATE, ST_COUNT };
+enum Stage { ST_SPREAD = 0, ST_ALLREDUCE, ST_FFT_FWD, ST_MULTIPLY, ST_FFT_INV, ST_INTERP, ST_UPDATE, ST_PLAN, ST_COUNT };
+// host wall-clock trace of the plan phases (SK_PLAN_TRACE=1), printed to stderr
+void plan_trace(const char* phase, cudaStream_t s);
 void prof_begin(int stage, cudaStream_t s);
 void prof_end(int stage, cudaStream_t s);
 void prof_harvest();

@@ -250,6 +250,43 @@ __global__ void __launch_bounds__(128, 2) accsweep_kernel(double* out, int iters
     out[blockIdx.x * blockDim.x + threadIdx.x] = s;
 }
 
+// hybrid spread mix: rows tx 0..7 on DMMA (one m-tile), rows 8..11 on DFMA with per-lane
+// accumulators (lane (g,q) owns columns 8j+g of node slot q): no padded tensor-core rows.
+// NT n-tiles (18 = all (ty,tz) columns, 9 = half of them per warp).
+template <int NT>
+__global__ void __launch_bounds__(128, NT == 18 ? 2 : 4) hybrid_kernel(double* out, int iters) {
+    double acc[NT][2], acc2[4][NT];
+#pragma unroll
+    for (int j = 0; j < NT; ++j) {
+        acc[j][0] = acc[j][1] = 0.0;
+#pragma unroll
+        for (int r = 0; r < 4; ++r) acc2[r][j] = 0.0;
+    }
+    double y = 1.0 + threadIdx.x * 1e-6, z = 1.0 - threadIdx.x * 1e-6, a0 = 1e-3, w = 0.5;
+    for (int it = 0; it < iters; ++it) {
+        double xr[4];
+#pragma unroll
+        for (int r = 0; r < 4; ++r) xr[r] = w * (y + r);
+#pragma unroll
+        for (int j = 0; j < NT; ++j) {
+            const double b = y * (z + j);
+            asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+                : "+d"(acc[j][0]), "+d"(acc[j][1]) : "d"(a0), "d"(b));
+#pragma unroll
+            for (int r = 0; r < 4; ++r) acc2[r][j] = fma(xr[r], b, acc2[r][j]);
+        }
+        y *= 0.9999999;
+    }
+    double s = 0;
+#pragma unroll
+    for (int j = 0; j < NT; ++j) {
+        s += acc[j][0] + acc[j][1];
+#pragma unroll
+        for (int r = 0; r < 4; ++r) s += acc2[r][j];
+    }
+    out[blockIdx.x * blockDim.x + threadIdx.x] = s;
+}
+
 template <typename F>
 float timeit(F f) {
     cudaEvent_t a, b;
@@ -330,6 +367,16 @@ int main() {
         printf("36 DMMA/iter, 36 accumulators, 8 warps/SM: %.2f TFLOP/s\n", fl / ms / 1e9);
         ms = timeit([&] { accsweep_kernel<4><<<g2 * 4, 128>>>(out, iters); });
         printf("36 DMMA/iter, 4 accumulators, 32 warps/SM: %.2f TFLOP/s\n", 4 * fl / ms / 1e9);
+        // useful = 12 of 16 DMMA rows in the spread mixes above
+        ms = timeit([&] { spreadmix_kernel<true><<<g2, 128>>>(out, iters); });
+        printf("spread mix (36 DMMA + 18 DMUL), USEFUL rate: %.2f TFLOP/s\n", 0.75 * fl / ms / 1e9);
+        double flu = 2.0 * 12 * 8 * 18 * 4 * (double)iters * g2 * 4;
+        ms = timeit([&] { hybrid_kernel<18><<<g2, 128>>>(out, iters); });
+        printf("hybrid 18 DMMA + 72 DFMA + 22 DMUL, 8 warps/SM, USEFUL: %.2f TFLOP/s\n", flu / ms / 1e9);
+        ms = timeit([&] { hybrid_kernel<9><<<g2 * 2, 128>>>(out, iters); });
+        printf("hybrid half (9 DMMA + 36 DFMA + 13 DMUL), 16 warps/SM, USEFUL: %.2f TFLOP/s\n", flu / ms / 1e9);
+        ms = timeit([&] { hybrid_kernel<9><<<g2, 128>>>(out, iters); });
+        printf("hybrid half, 8 warps/SM, USEFUL: %.2f TFLOP/s\n", flu / 2 / ms / 1e9);
     }
     {
         long long gs = 1 << 21;
