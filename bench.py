@@ -113,7 +113,7 @@ def cpu_oracle_rate(cfg, budget_s: float):
     """Time the oracle (dense log-domain Alg. 1, as it stands) on a bounded seeded subsample
     of the workload; return (it/s extrapolated to the full workload, description)."""
     from oracle import dense
-    if cfg.x_dist == "jitter_grid":      # grid generators need the full K x K grid
+    if cfg.x_dist in ("jitter_grid", "pixel_grid"):   # grid generators need the full K x K grid
         x, y, a, b = make_inputs(cfg)
         rng = np.random.default_rng(0)
         ix = rng.permutation(x.shape[0])[:200_000]

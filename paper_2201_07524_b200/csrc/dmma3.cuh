@@ -52,6 +52,7 @@ struct SpreadItem {
     int count;      // nodes
 };
 constexpr int kSegMax = 1024;
+constexpr int kSegHybrid = 128;   // spread3_hybrid_kernel segments (two passes, L2-resident taps)
 constexpr int kSpreadItemMax = 4096;
 
 #ifndef SK_WORKLIST_ONLY   // plan.cu only needs the work-list types above
@@ -336,6 +337,150 @@ spread3_dmma_kernel(const SpreadItem* __restrict__ items, int nitems, const Cell
                 }
             }
             __syncwarp();
+        }
+        // flush the region: coalesced FP64 atomics along z rows
+        const int gx0 = 2 * sx - (m - 1), gy0 = 2 * sy - (m - 1), gz0 = 2 * sz - (m - 1);
+        for (int i = lane; i < C::REG; i += 32) {
+            const double v = REGm[i];
+            if (v != 0.0) {
+                const int rz = i % S, rest = i / S, ry = rest % S, rx = rest / S;
+                atomicAdd(&grid[((long long)(gx0 + rx) * n + (gy0 + ry)) * n + (gz0 + rz)], v);
+            }
+        }
+        __syncwarp();
+    }
+}
+
+// ------------------------------------------------------------------------------ spread (hybrid)
+// Same contraction as spread3_dmma_kernel without the padded tensor-core rows: rows tx = 0..7
+// are one DMMA m-tile, rows tx = 8..11 run on the FP64 vector pipe (DFMA) with per-lane
+// accumulators. Lane (g, q) owns B column 8 nt + g of node slot q, so its DFMA partials
+// acc2[r][nt] = sum over its nodes of (w phi_x[8+r]) (phi_y phi_z)[8 nt + g]; the four q-lanes
+// are reduced (reduce-scatter in 2 shuffle steps) when a segment ends. Every FP64 operation is
+// useful work (microbench: 26.3 vs 22.3 useful TFLOP/s for the padded mix).
+// Registers: all 18 n-tiles at once would need 108 FP64 accumulators (216 registers), so each
+// segment is swept twice, 9 n-tiles (ty in one half) per pass; segments are short (kSegHybrid
+// nodes) so the second pass finds the taps in L2.
+struct SpreadHCfg {
+    static constexpr int W = 12, S = W + 1, NT = 128, NWARP = NT / 32, NTH = 9;   // n-tiles per pass
+    static constexpr int TS = 3 * W;
+    static constexpr int REG = S * S * S;
+    static constexpr size_t SMEM_BYTES = sizeof(double) * (NWARP * REG);
+};
+
+__global__ void __launch_bounds__(128, 2)
+spread3_hybrid_kernel(const SpreadItem* __restrict__ items, int nitems, const CellBatch* __restrict__ segs,
+                      const double* __restrict__ taps, const double* __restrict__ w,
+                      double* __restrict__ grid, int n) {
+    using C = SpreadHCfg;
+    constexpr int W = C::W, S = C::S, m = W / 2, NTH = C::NTH, TS = C::TS;
+    extern __shared__ __align__(16) double smem[];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int g = lane >> 2, q = lane & 3;
+    double* REGm = smem + warp * C::REG;
+    const int ns = n / 2;
+    const int gw = blockIdx.x * C::NWARP + warp, nw = gridDim.x * C::NWARP;
+    const int z1 = (8 + g) % W;
+
+    for (int ii = gw; ii < nitems; ii += nw) {
+        const SpreadItem it = items[ii];
+        const int sz = it.stile % ns, sy = (it.stile / ns) % ns, sx = it.stile / ns / ns;
+        for (int i = lane; i < C::REG; i += 32) REGm[i] = 0.0;
+        __syncwarp();
+        for (int sg = it.seg_begin; sg < it.seg_end; ++sg) {
+            const CellBatch seg = segs[sg];
+            const int cz = seg.cell % n, cy = (seg.cell / n) % n, cx = seg.cell / n / n;
+            const int ox = cx - 2 * sx, oy = cy - 2 * sy, oz = cz - 2 * sz;   // in {0,1}
+            const double* T0 = taps + (long long)seg.start * TS;
+            const double* w0 = w + seg.start;
+            const int nks = (seg.count + 3) >> 2;
+            prefetch_range(T0, (long long)seg.count * TS * 8, lane);
+            if (lane < 8) prefetch_l2(w0 + 16 * lane);
+#pragma unroll 1
+            for (int half = 0; half < 2; ++half) {
+                // pass over columns 72 half .. 72 half + 71: ty in 6 half .. 6 half + 5
+                double acc[NTH][2], acc2[4][NTH];
+#pragma unroll
+                for (int j = 0; j < NTH; ++j) {
+                    acc[j][0] = acc[j][1] = 0.0;
+#pragma unroll
+                    for (int r = 0; r < 4; ++r) acc2[r][j] = 0.0;
+                }
+                // operands of k-step s for node 4 s + q: w, phi_x[g], phi_x[8..11], the six
+                // phi_y of this half, phi_z at {g, z1, 4+g}
+                auto load_ops = [&](int s, double& wv, double& x0, double2 (&x8)[2], double2 (&yy)[3],
+                                    double (&zz)[3]) {
+                    const int jr = 4 * s + q;
+                    const bool ok = jr < seg.count;
+                    const double* tr = T0 + (ok ? jr : 0) * TS;
+                    wv = ok ? __ldg(w0 + jr) : 0.0;
+                    x0 = __ldg(tr + g);
+                    x8[0] = __ldg(reinterpret_cast<const double2*>(tr + 8));
+                    x8[1] = __ldg(reinterpret_cast<const double2*>(tr + 10));
+                    const double2* y2 = reinterpret_cast<const double2*>(tr + W + 6 * half);
+#pragma unroll
+                    for (int i = 0; i < 3; ++i) yy[i] = __ldg(y2 + i);
+                    zz[0] = __ldg(tr + 2 * W + g);
+                    zz[1] = __ldg(tr + 2 * W + z1);
+                    zz[2] = __ldg(tr + 2 * W + 4 + g);
+                };
+                double wn, x0n, zn[3];
+                double2 x8n[2], yn[3];
+                load_ops(0, wn, x0n, x8n, yn, zn);
+#pragma unroll 1
+                for (int s = 0; s < nks; ++s) {
+                    const double a0 = wn * x0n;                             // A[tx = g][k = q]
+                    const double xr[4] = {wn * x8n[0].x, wn * x8n[0].y, wn * x8n[1].x, wn * x8n[1].y};
+                    double yv[6], zv[3];
+#pragma unroll
+                    for (int i = 0; i < 3; ++i) { yv[2 * i] = yn[i].x; yv[2 * i + 1] = yn[i].y; }
+                    zv[0] = zn[0]; zv[1] = zn[1]; zv[2] = zn[2];
+                    if (s + 1 < nks) load_ops(s + 1, wn, x0n, x8n, yn, zn);   // software pipeline
+#pragma unroll
+                    for (int j = 0; j < NTH; ++j) {
+                        // column 8 (9 half + j) + g: ty = 6 half + 2 (j/3) + {0, g>=4, 1}[j%3]
+                        const int k3 = j / 3, r3 = j % 3;
+                        const double yvv = (r3 == 0) ? yv[2 * k3]
+                                         : ((r3 == 1) ? (g >= 4 ? yv[2 * k3 + 1] : yv[2 * k3]) : yv[2 * k3 + 1]);
+                        const double b = yvv * zv[r3];
+                        dmma884(acc[j][0], acc[j][1], a0, b);
+#pragma unroll
+                        for (int r = 0; r < 4; ++r) acc2[r][j] = fma(xr[r], b, acc2[r][j]);
+                    }
+                }
+                // DMMA rows tx = g: columns 8 nt + 2 q + e
+                {
+                    double* rx = REGm + (ox + g) * S * S + oy * S + oz;
+#pragma unroll
+                    for (int j = 0; j < NTH; ++j)
+#pragma unroll
+                        for (int e = 0; e < 2; ++e) {
+                            const int col = 8 * (NTH * half + j) + 2 * q + e;
+                            rx[(col / W) * S + (col % W)] += acc[j][e];
+                        }
+                }
+                // DFMA rows tx = 8 + r: reduce-scatter over the q-lanes, lane q keeps row 8 + q
+                {
+                    const bool hi2 = (q & 2) != 0, hi1 = (q & 1) != 0;
+                    double* rx = REGm + (ox + 8 + q) * S * S + oy * S + oz;
+#pragma unroll
+                    for (int j = 0; j < NTH; ++j) {
+                        double keep[2];
+#pragma unroll
+                        for (int rr = 0; rr < 2; ++rr) {
+                            const double send = hi2 ? acc2[rr][j] : acc2[2 + rr][j];
+                            const double mine = hi2 ? acc2[2 + rr][j] : acc2[rr][j];
+                            keep[rr] = mine + __shfl_xor_sync(0xffffffffu, send, 2);
+                        }
+                        const double send = hi1 ? keep[0] : keep[1];
+                        const double mine = hi1 ? keep[1] : keep[0];
+                        const double fin = mine + __shfl_xor_sync(0xffffffffu, send, 1);
+                        const int col = 8 * (NTH * half + j) + g;
+                        rx[(col / W) * S + (col % W)] += fin;
+                    }
+                }
+                __syncwarp();
+            }
         }
         // flush the region: coalesced FP64 atomics along z rows
         const int gx0 = 2 * sx - (m - 1), gy0 = 2 * sy - (m - 1), gz0 = 2 * sz - (m - 1);

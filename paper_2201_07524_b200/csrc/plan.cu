@@ -216,7 +216,7 @@ static int build_cell_lists(Plan& P, NodeSet& S, cudaStream_t s) {
     // spread work-unit size: enough items to keep ~4 per resident warp busy (148 SMs x 8
     // warps), at most kSpreadItemMax nodes (one region flush per item)
     const int item_max = (int)std::max(128LL, std::min((long long)kSpreadItemMax, count / 4736));
-    const int seg_max = std::min(kSegMax, item_max);
+    const int seg_max = std::min(P.spread_hybrid ? kSegHybrid : kSegMax, item_max);
 
     // run-length encode the sorted keys; 7 int arrays of nruns (<= count) entries
     int* buf = nullptr;
@@ -441,6 +441,9 @@ int build_plan(Ctx* ctx, Plan** out, int d, const double* x, long long n, const 
         P->dmma = ((P->tiled && m_w == 6) || (d == 2 && m_w == 8 && err >= 0.0 && err <= 1e-14)) &&
                   getenv("SK_NO_DMMA") == nullptr && getenv("SK_FORCE_V1") == nullptr;
         if (P->dmma && d == 2) P->tiled = false;
+        // hybrid DMMA+DFMA spread (no padded rows): opt-in until it beats the padded kernel
+        // (c5: 20.6 vs 15.5 ms under ncu, issue/latency-bound with 2 passes per segment)
+        P->spread_hybrid = P->dmma && d == 3 && getenv("SK_SPREAD3_HYBRID") != nullptr;
     }
     P->tile_cells = P->dmma ? (d == 3 ? 2 : kSup2) : choose_tile(d, ng, P->tiled);
     P->tiles_per_axis = ng / P->tile_cells;

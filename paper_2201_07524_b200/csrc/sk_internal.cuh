@@ -116,6 +116,7 @@ struct Plan {
     int tiles_per_axis = 0;
     bool tiled = false;       // v2 tiled spread/interp usable (d = 3, 2 m_w in {12, 16})
     bool dmma = false;        // FP64 tensor-core spread/interp (d = 3, 2 m_w = 12)
+    bool spread_hybrid = false;  // d = 3 spread: DMMA rows 0..7 + DFMA rows 8..11 (no padding)
     void* winpoly = nullptr;  // host WinPoly (window tap polynomials)
 };
 

@@ -60,7 +60,18 @@ CONFIGS = {
                  sub_n=100_000, sub_m=80_000),
 }
 
-CONFIG_INDEX = {"c1": 1, "c2": 2, "c3": 3, "c4": 4, "c5": 5}
+# the paper's image experiments (Tables 3, 6, 7) at its own
+# lambda = 20, r = 2: two K x K grayscale images on the same pixel grid, pixel centres
+# ((i + 1/2)/K, (j + 1/2)/K), weights = normalised gray levels. DOTmark is not in the container;
+# each image is a seeded smooth bump field (the c4 recipe) standing in for it. NFFT parameters
+# are the build's choice (the paper gives none): N = 64 puts the Fourier truncation of the
+# Gaussian at exp(-pi^2 32^2 / lambda') ~ e^-48, m_w = 8 (FP64 window error), sigma = 2.
+for _K in (32, 64, 128, 256, 512):
+    CONFIGS[f"img{_K}"] = Config(f"img{_K}", 2, _K * _K, _K * _K, 20.0, 64, 2.0, 8, 1 / 16, 8, 100,
+                                 "pixel_grid", "pixel_grid", "bumps", grid_x=_K, grid_y=_K)
+
+CONFIG_INDEX = {"c1": 1, "c2": 2, "c3": 3, "c4": 4, "c5": 5,
+                "img32": 6, "img64": 7, "img128": 8, "img256": 9, "img512": 10}
 
 
 def get(name: str) -> Config:

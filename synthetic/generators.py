@@ -17,6 +17,7 @@ Distribution recipes (BASELINE.json configs; readings in DESIGN.md):
                U[0,1]^d, isotropic sigma, clipped to [0,1]^d
   shell        uniform in the volume of the shell 0.3 <= |y - 1/2| <= 0.4
   jitter_grid  ((i + 1/2) + U(-0.4, 0.4)) / K per axis on a K x K grid
+  pixel_grid   pixel centres (i + 1/2) / K of a K x K image (NEXT-1 image workloads)
 Weights: uniform 1/n; dirichlet = Exp(1) normalised (Dirichlet(1));
 bumps = smooth field of 32 Gaussian bumps at the pixel centre + 1e-6, normalised.
 """
@@ -68,6 +69,13 @@ def _jitter_grid(g, K):
     return pts
 
 
+def _pixel_grid(K):
+    """Pixel centres ((i + 1/2)/K, (j + 1/2)/K) of a K x K image, row-major (i slowest)."""
+    i = (np.arange(K, dtype=np.float64) + 0.5) / K
+    gx, gy = np.meshgrid(i, i, indexing="ij")
+    return np.stack([gx.ravel(), gy.ravel()], axis=1)
+
+
 def _bump_weights(g, pts_or_centres):
     """Smooth random field (32 Gaussian bumps) at the given points, + 1e-6, normalised."""
     nb = 32
@@ -103,6 +111,9 @@ def _points(cfg: Config, side: str, seed: int):
     if dist == "jitter_grid":
         assert d == 2 and K * K == count
         return _jitter_grid(g, K)
+    if dist == "pixel_grid":
+        assert d == 2 and K * K == count
+        return _pixel_grid(K)
     raise ValueError(dist)
 
 

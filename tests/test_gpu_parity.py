@@ -279,3 +279,61 @@ def test_host_buffer_solve_matches_device(capi, ctx):
     # identical inputs; only the order of the FP64 atomics in the spread flush differs
     # (well-conditioned workload, kappa ~ 10^1.6, so rounding is not amplified)
     assert abs(h[0] - d_[0]) <= 1e-12 * abs(h[0]) and abs(h[1] - d_[1]) <= 1e-12 * abs(h[1])
+
+
+@pytest.mark.parametrize("name,n,m", [("c1", 1000, 1000), ("c2", 20000, 15000), ("c5", 200000, 160000)])
+def test_box_exchange_is_exact(capi, ctx, name, n, m):
+    """a3 exchange over the touched box only: with SK_FORCE_BOX_EXCHANGE a
+    one-rank plan packs the box, clears the whole grid and unpacks it before the FFT, so the
+    matvec is bit-identical iff the box holds every nonzero of the spread grid."""
+    cfg = get(name)
+    x, y, a, b = make_inputs(cfg.with_(n=n, m=m) if cfg.n > n else cfg)
+    P0 = capi.Plan(ctx, dev(x), dev(y), cfg.lam, cfg.N, cfg.sigma, cfg.m_w, cfg.eps_B, cfg.p)
+    os.environ["SK_FORCE_BOX_EXCHANGE"] = "1"
+    try:
+        P1 = capi.Plan(ctx, dev(x), dev(y), cfg.lam, cfg.N, cfg.sigma, cfg.m_w, cfg.eps_B, cfg.p)
+    finally:
+        del os.environ["SK_FORCE_BOX_EXCHANGE"]
+    info = P1.info()
+    n_grid = int(info["n_grid"])
+    assert info["box_size"] == int(np.prod(info["box_n"][:cfg.d]))
+    assert info["box_size"] < n_grid ** cfg.d
+    # the spread grid is zero outside the box
+    g = capi.nfft_spread(P1, 1, dev(b)).cpu().numpy()
+    sl = tuple(slice(lo, lo + k) for lo, k in zip(info["box_lo"][:cfg.d], info["box_n"][:cfg.d]))
+    inside = np.zeros(g.shape, bool)
+    inside[sl] = True
+    assert np.all(g[~inside] == 0.0) and np.any(g[inside] != 0.0)
+    for tr, w in ((0, b), (1, a)):
+        for kernel in (0, 1):
+            t0 = capi.fastsum_apply(P0, dev(w), tr, kernel).cpu().numpy()
+            t1 = capi.fastsum_apply(P1, dev(w), tr, kernel).cpu().numpy()
+            # same data; only the order of the spread's FP64 atomics may differ
+            assert np.abs(t0 - t1).max() <= 1e-13 * np.abs(t0).max()
+
+
+# ------------------------------------------------------------------ NEXT-1: image workloads (lambda = 20)
+@pytest.mark.parametrize("name", ["img32", "img64"])
+def test_image_divergence_parity(capi, ctx, name):
+    """two K x K bump-field images on the pixel grid at the paper's
+    lambda = 20 (Tables 3, 6, 7). Well conditioned, so the GPU's s~ and s match
+    the dense oracle far inside the BJ gate (the paper reports agreement to 13-14 digits,
+    P:L1088-1091)."""
+    cfg = get(name)
+    x, y, a, b = make_inputs(cfg)
+    ref, _, _ = dense.sinkhorn_divergence(x, y, a, b, cfg.lam, cfg.iters)
+    sd, sc, info, *_ = _gpu_divergence(capi, ctx, cfg, x, y, a, b)
+    assert abs(sc - ref["s_cost"]) <= 1e-10 * abs(ref["s_cost"]), (sc, ref, info.asdict())
+    assert abs(sd - ref["s_dual"]) <= 1e-10 * abs(ref["s_dual"]), (sd, ref, info.asdict())
+
+
+@pytest.mark.parametrize("name", ["img128", "img512"])
+def test_image_matvec_parity(capi, ctx, name):
+    cfg = get(name)
+    x, y, a, b = make_inputs(cfg)
+    ci = CONFIG_INDEX[name]
+    rx = check_rows(ci, 4096, x.shape[0])
+    ry = check_rows(ci, 4096, y.shape[0], seed=1)
+    weights = {"marginal": (b, a), "uniform01": (uniform_test_weights(ci, y.shape[0]), uniform_test_weights(ci, x.shape[0], 1))}
+    worst = _matvec_case(capi, ctx, cfg, x, y, a, b, rx, ry, weights)
+    assert max(max(v) for v in worst.values()) <= 1e-9, worst

@@ -51,7 +51,35 @@ def _worker(rank, world, port, q):
         # --- unique-id broadcast pattern (rank 0 creates, everyone receives the same bytes)
         obj = [bytes(range(128)) if rank == 0 else None]
         dist.broadcast_object_list(obj, src=0)
-        q.put((rank, err_mv, err_s, tm.item(), obj[0] == bytes(range(128))))
+        # --- box-restricted grid exchange: global bbox by MIN/MAX all-reduce,
+        # every rank spreads its shard, only the touched box is summed across ranks
+        from oracle import nfft_ref
+        rng2 = np.random.default_rng(11)
+        x2, y2 = 0.3 + 0.4 * rng2.random((50, 2)), 0.2 + 0.5 * rng2.random((46, 2))
+        w2 = rng2.random(46)
+        lo3, hi3 = shard_range(46, rank, world)
+        mine = np.concatenate([x2[shard_range(50, rank, world)[0]:shard_range(50, rank, world)[1]], y2[lo3:hi3]])
+        mn, mx = torch.from_numpy(mine.min(0)), torch.from_numpy(mine.max(0))
+        dist.all_reduce(mn, op=dist.ReduceOp.MIN)
+        dist.all_reduce(mx, op=dist.ReduceOp.MAX)
+        centre = 0.5 * (mn.numpy() + mx.numpy())
+        rho = (0.5 - 1 / 16) / float(np.sqrt(((mx.numpy() - mn.numpy()) ** 2).sum()))
+        n_grid, m_w = 32, 4
+        ulo = n_grid * (rho * (mn.numpy() - centre) + 0.5)
+        uhi = n_grid * (rho * (mx.numpy() - centre) + 0.5)
+        blo = np.maximum(0, np.floor(ulo).astype(int) - m_w)
+        bhi = np.minimum(n_grid - 1, np.floor(uhi).astype(int) + m_w + 1)
+        sl = tuple(slice(l, h + 1) for l, h in zip(blo, bhi))
+        part = nfft_ref.grid_spread(nfft_ref.scale(y2[lo3:hi3], centre, rho), w2[lo3:hi3], n_grid, m_w, 2.0)
+        outside = part.copy()
+        outside[sl] = 0.0
+        box = torch.from_numpy(np.ascontiguousarray(part[sl]))
+        dist.all_reduce(box)
+        full = nfft_ref.grid_spread(nfft_ref.scale(y2, centre, rho), w2, n_grid, m_w, 2.0)
+        rebuilt = np.zeros_like(full)
+        rebuilt[sl] = box.numpy()
+        err_box = float(np.abs(rebuilt - full).max() / np.abs(full).max()) + float(np.abs(outside).max())
+        q.put((rank, err_mv, err_s, tm.item(), obj[0] == bytes(range(128)), err_box, box.numel() < full.size))
     finally:
         dist.destroy_process_group()
 
@@ -79,7 +107,8 @@ def test_two_rank_gloo_decomposition():
     for p in procs:
         p.join(timeout=60)
         assert p.exitcode == 0
-    for rank, err_mv, err_s, tmax, id_ok in res:
+    for rank, err_mv, err_s, tmax, id_ok, err_box, smaller in res:
+        assert err_box < 1e-14 and smaller, err_box
         assert err_mv < 1e-15, err_mv
         assert err_s < 1e-14, err_s
         assert tmax == float(world)
