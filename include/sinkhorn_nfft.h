@@ -104,6 +104,21 @@ int fastsum_apply(sk_plan_t plan, int transpose, int kernel, const double* w, do
 int sinkhorn_run(sk_plan_t plan, const double* a, const double* b, int iters, double tol,
                  int rescale_policy, double* u, double* v, sk_run_info* info);
 
+/* (sinkhorn_run with tol == 0, no profiling and iters > 2 captures one iteration as a CUDA
+ * graph on a plan-private stream and replays it iters-1 times on the context stream.) */
+
+/* sinkhorn_run plus per-iteration convergence diagnostics (Sec. 3.3
+ * P:L312-424). trace: HOST array of 6 * iters doubles, iteration k (0-based) at trace[6k..]:
+ *   [0] ||pi 1 - p||_1 of the iterate before the u-update (row part of Eq. (Error) P:L333;
+ *       its column part is 0 there), [1] D_KL(p | pi 1) at that iterate (Lemma
+ *       f decreases by exactly this), [2] sum_i p_i log alpha_i after the update,
+ *   [3..5] the same for the v-update: ||pi^T 1 - p~||_1, D_KL(p~ | pi^T 1), sum_j p~_j log alpha~_j.
+ * After any half-step the objective (Eq. (objfunc), unnormalised k) is
+ * f = 1 - sum p log alpha - sum p~ log alpha~. Entries of iterations not run (tol stop) are NaN.
+ * Sums over all ranks. Costs two extra log() per node and half-step. */
+int sinkhorn_run_trace(sk_plan_t plan, const double* a, const double* b, int iters, double tol,
+                       int rescale_policy, double* u, double* v, sk_run_info* info, double* trace);
+
 /* Divergences at (u, v) (reading Q1):
  *   s_dual = 1/lambda + (1/lambda) (sum a log u + sum b log v) - (1/lambda) sum_j (K^T u)_j v_j
  *            (Eq. (14) P:L211 / Alg. 2 result line P:L732; 2 fast summations incl. K^T u)
@@ -149,13 +164,16 @@ long long sk_launch_count(void);
  * starts recording an event pair around every stage of every fast summation; sk_profile_read
  * writes out[2k] = number of timed launches and out[2k+1] = their total device milliseconds
  * for stage k = 0 spread, 1 grid all-reduce, 2 forward FFT, 3 multiply, 4 inverse FFT,
- * 5 interp, 6 update (nstages <= 7 entries are written); reset != 0 clears the totals. */
+ * 5 interp, 6 update, 7 plan (sinkhorn_solve's fastsum_plan; nstages <= 8 entries are
+ * written); reset != 0 clears the totals. While profiling, sinkhorn_run launches every kernel
+ * eagerly (no CUDA-graph replay of iterations). */
 void sk_profile(int on);
 int sk_profile_read(double* out, int nstages, int reset);
 
 /* Device memory of destroyed plans is cached by the library and reused (best fit, ordered on
  * the allocating stream with events); this returns every cached block to the driver. Call it
- * after fastsum_plan_destroy when the memory is needed elsewhere. */
+ * after fastsum_plan_destroy when the memory is needed elsewhere. The cuFFT handles of
+ * destroyed plans are pooled the same way and destroyed here too. */
 void sk_release_cache(void);
 
 const char* sk_last_error(void);

@@ -46,13 +46,14 @@ def up_to_date() -> bool:
 
 
 def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and up_to_date():
+    lib = os.environ.get("SK_LIB_OUT", LIB)   # experiments: build variants side by side
+    if not force and lib == LIB and up_to_date():
         return LIB
     os.makedirs(LIBDIR, exist_ok=True)
     os.makedirs(BUILD, exist_ok=True)
     nvcc = _nvcc()
     common = ["-O3", "-std=c++17", *ARCH, "-lineinfo", "-Xcompiler", "-fPIC", "-Xptxas", "-v",
-              "-I", os.path.join(ROOT, "include")]
+              "-I", os.path.join(ROOT, "include"), *os.environ.get("SK_NVCC_FLAGS", "").split()]
 
     def compile_unit(u):
         obj = os.path.join(BUILD, u.replace(".cu", ".o"))
@@ -66,14 +67,14 @@ def build(force: bool = False, verbose: bool = False) -> str:
 
     with cf.ThreadPoolExecutor(max_workers=len(UNITS)) as ex:
         objs = list(ex.map(compile_unit, UNITS))
-    link = [nvcc, *ARCH, "-shared", "-o", LIB, *objs, "-L", os.path.join(CUDA_HOME, "lib64"),
+    link = [nvcc, *ARCH, "-shared", "-o", lib, *objs, "-L", os.path.join(CUDA_HOME, "lib64"),
             "-lcufft", "-ldl", "-Xlinker", "-rpath," + os.path.join(CUDA_HOME, "lib64")]
     r = subprocess.run(link, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError(f"link failed:\n{r.stderr[-6000:]}")
     if verbose:
-        print("built", LIB)
-    return LIB
+        print("built", lib)
+    return lib
 
 
 if __name__ == "__main__":

@@ -13,7 +13,7 @@ import os
 import torch
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_PKG, "lib", "libsk_nfft.so")
+LIB_PATH = os.environ.get("SK_LIB_PATH") or os.path.join(_PKG, "lib", "libsk_nfft.so")
 
 if not os.path.exists(LIB_PATH):
     raise ImportError(f"libsk_nfft.so not built ({LIB_PATH}); run `python -m paper_2201_07524_b200.build` "
@@ -56,6 +56,7 @@ _sig = {
     "fastsum_plan_destroy": ([_vp], _i),
     "fastsum_apply": ([_vp, _i, _i, _vp, _vp], _i),
     "sinkhorn_run": ([_vp, _vp, _vp, _i, _d, _i, _vp, _vp, ctypes.POINTER(RunInfo)], _i),
+    "sinkhorn_run_trace": ([_vp, _vp, _vp, _i, _d, _i, _vp, _vp, ctypes.POINTER(RunInfo), _dp], _i),
     "sinkhorn_divergence": ([_vp, _vp, _vp, _vp, _vp, _dp, _dp], _i),
     "sinkhorn_solve": ([_vp, _i, _vp, _ll, _vp, _ll, _vp, _vp, _d, _i, _d, _i, _d, _i, _i, _i, _dp, _dp,
                         ctypes.POINTER(RunInfo)], _i),
@@ -237,6 +238,23 @@ def sinkhorn_run(plan: Plan, a, b, iters: int, tol: float = 0.0, rescale_policy:
                              _ptr(u), _ptr(v), ctypes.byref(info))
     _check(code, info)
     return u, v, info
+
+
+TRACE_FIELDS = ("row_resid", "row_kl", "sum_a_log_u", "col_resid", "col_kl", "sum_b_log_v")
+
+
+def sinkhorn_run_trace(plan: Plan, a, b, iters: int, tol: float = 0.0, rescale_policy: int = 0, u=None, v=None):
+    """Alg. 2 with per-iteration diagnostics; returns (u, v, RunInfo, trace [iters, 6] numpy,
+    columns TRACE_FIELDS; NaN rows for iterations not run)."""
+    import numpy as np
+    u = torch.ones(plan.n, dtype=torch.float64, device=a.device) if u is None else u
+    v = torch.ones(plan.m, dtype=torch.float64, device=a.device) if v is None else v
+    info = RunInfo()
+    tr = np.empty((max(int(iters), 0), 6))
+    code = _lib.sinkhorn_run_trace(plan.handle, _ptr(a), _ptr(b), int(iters), float(tol), int(rescale_policy),
+                                   _ptr(u), _ptr(v), ctypes.byref(info), tr.ctypes.data_as(_dp))
+    _check(code, info)
+    return u, v, info, tr
 
 
 def sinkhorn_divergence(plan: Plan, a, b, u, v):

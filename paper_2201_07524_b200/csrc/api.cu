@@ -229,7 +229,10 @@ extern "C" {
 
 const char* sk_last_error(void) { return g_err.c_str(); }
 
-void sk_release_cache(void) { dev_cache_release(); }
+void sk_release_cache(void) {
+    fft_pool_release();
+    dev_cache_release();
+}
 
 void sk_profile(int on) {
     if (!on) prof_harvest();
@@ -380,12 +383,15 @@ int fastsum_coefficients(sk_plan_t plan, int kernel, double* b) {
 }
 
 // Sum of the 3-slot update partials -> slot(SL_UPD)[0..2] (resid sum, min t, 0).
-static int finalize_update(Plan& P) {
-    return launch_finalize_partials(P.red, 592, 3, slot(P, SL_UPD), P.ctx->stream);
+static int finalize_update(Plan& P, double* out) {
+    return launch_finalize_partials(P.red, kUpdBlocks, kUpdVals, out, P.ctx->stream);
 }
 
-int sinkhorn_run(sk_plan_t plan, const double* a, const double* b, int iters, double tol,
-                 int rescale_policy, double* u, double* v, sk_run_info* info) {
+// Alg. 2. trace (host, may be NULL): per iteration kTraceVals doubles, see
+// sinkhorn_run_trace in include/sinkhorn_nfft.h.
+constexpr int kTraceVals = 6;
+static int run_impl(sk_plan_t plan, const double* a, const double* b, int iters, double tol,
+                    int rescale_policy, double* u, double* v, sk_run_info* info, double* trace) {
     if (!plan) return set_error(SK_EINVAL, "NULL plan");
     Plan& P = *plan->p;
     Ctx* C = P.ctx;
@@ -401,14 +407,27 @@ int sinkhorn_run(sk_plan_t plan, const double* a, const double* b, int iters, do
     SK_TRY(launch_permute_in(v, Y.perm, Y.count, P.v_s, s));
     int hflag[4] = {0x7fffffff, 0x7fffffff, 0x7fffffff, 0x7fffffff};
     SK_CUDA(cudaMemcpyAsync(P.flag, hflag, sizeof(hflag), cudaMemcpyHostToDevice, s));
+    double* trace_dev = nullptr;
+    if (trace && iters > 0) SK_TRY(dev_alloc((void**)&trace_dev, sizeof(double) * kTraceVals * iters, s));
+    // per half-step (residual, KL, sum p log x) from the finalized update slot
+    auto record = [&](int it, int half) -> int {
+        double* r = slot(P, SL_C);
+        SK_TRY(finalize_update(P, r));
+        double* dst = trace_dev + (long long)it * kTraceVals + 3 * half;
+        SK_CUDA(cudaMemcpyAsync(dst, r, sizeof(double), cudaMemcpyDeviceToDevice, s));
+        SK_CUDA(cudaMemcpyAsync(dst + 1, r + 2, 2 * sizeof(double), cudaMemcpyDeviceToDevice, s));
+        return SK_OK;
+    };
     cudaEvent_t e0, e1;
     cudaEventCreate(&e0);
     cudaEventCreate(&e1);
     cudaEventRecord(e0, s);
     double resid = NAN, kappa = NAN;
     int done = 0;
-    for (int it = 0; it < iters; ++it) {
-        const bool last = (it == iters - 1);
+    // one iteration of Alg. 2; it < 0: inside a CUDA graph, the iteration number for error
+    // reports comes from the device counter P.flag[4]
+    auto body = [&](int it, bool last) -> int {
+        const int* iter_dev = it < 0 ? P.flag + 4 : nullptr;
         if (rescale_policy != 0) {
             // Eq. (scale): v <- c v, c = 1/geomean(v) or 1/max(v) (reading Q4)
             double* r = slot(P, SL_E);
@@ -422,14 +441,65 @@ int sinkhorn_run(sk_plan_t plan, const double* a, const double* b, int iters, do
         // odd Delta: t = K v, u = a / t   (Eq. (even_F_sink))
         SK_TRY(apply_sorted(P, 0, 0, P.v_s, P.t_sorted));
         prof_begin(ST_UPDATE, s);
-        SK_TRY(launch_update(P, 0, P.t_sorted, P.a_s, P.u_s, (tol > 0 || last) ? 1 : 0, it, s));
+        SK_TRY(launch_update(P, 0, P.t_sorted, P.a_s, P.u_s, trace_dev ? 2 : ((tol > 0 || last) ? 1 : 0), it,
+                             iter_dev, s));
         prof_end(ST_UPDATE, s);
-        if (tol > 0 || last) SK_TRY(finalize_update(P));
+        if (tol > 0 || last) SK_TRY(finalize_update(P, slot(P, SL_UPD)));
+        if (trace_dev) SK_TRY(record(it, 0));
         // even Delta: t~ = K^T u, v = b / t~   (Eq. (odd_F_sink))
         SK_TRY(apply_sorted(P, 1, 0, P.u_s, P.t_sorted));
         prof_begin(ST_UPDATE, s);
-        SK_TRY(launch_update(P, 1, P.t_sorted, P.b_s, P.v_s, 0, it, s));
+        SK_TRY(launch_update(P, 1, P.t_sorted, P.b_s, P.v_s, trace_dev ? 2 : 0, it, iter_dev, s));
         prof_end(ST_UPDATE, s);
+        if (trace_dev) SK_TRY(record(it, 1));
+        return SK_OK;
+    };
+    int it0 = 0;
+    // Fixed-count runs replay iterations 0 .. iters-2 as one CUDA graph (cuFFT, NCCL and the
+    // kernels of an iteration captured once): launch-bound small workloads lose the per-kernel
+    // CPU launch cost. Off under the stage profiler, tracing, tol > 0 or SK_NO_GRAPH.
+    static const bool no_graph = getenv("SK_NO_GRAPH") != nullptr;
+    if (!trace_dev && tol == 0 && !g_prof.on && iters > 2 && !no_graph) {
+        int zero = 0;
+        SK_CUDA(cudaMemcpyAsync(P.flag + 4, &zero, sizeof(int), cudaMemcpyHostToDevice, s));
+        cudaGraph_t graph = nullptr;
+        cudaGraphExec_t exec = nullptr;
+        const long long l0 = g_launches.load();
+        // capture on the plan's private stream (the caller's may be the legacy default stream,
+        // which cannot be captured); the graph is then launched on the caller's stream
+        if (!P.cap_stream) SK_CUDA(cudaStreamCreateWithFlags(&P.cap_stream, cudaStreamNonBlocking));
+        const cudaStream_t user = s;
+        auto use_stream = [&](cudaStream_t t) {
+            s = t;
+            C->stream = t;
+            cufftSetStream(P.fwd, t);
+            cufftSetStream(P.inv, t);
+        };
+        use_stream(P.cap_stream);
+        cudaError_t ce = cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal);
+        if (ce != cudaSuccess) { use_stream(user); return set_error(SK_ECUDA, std::string("graph capture: ") + cudaGetErrorString(ce)); }
+        int st = body(-1, false);
+        if (!st) st = launch_increment(P.flag + 4, s);
+        ce = cudaStreamEndCapture(s, &graph);
+        use_stream(user);
+        if (st) { if (graph) cudaGraphDestroy(graph); return st; }
+        if (ce != cudaSuccess) return set_error(SK_ECUDA, std::string("graph capture: ") + cudaGetErrorString(ce));
+        const long long per_iter = g_launches.load() - l0;
+        ce = cudaGraphInstantiate(&exec, graph, 0);
+        cudaGraphDestroy(graph);
+        if (ce != cudaSuccess) return set_error(SK_ECUDA, std::string("graph instantiate: ") + cudaGetErrorString(ce));
+        for (int it = 0; it < iters - 1; ++it) {
+            ce = cudaGraphLaunch(exec, s);
+            if (ce != cudaSuccess) { cudaGraphExecDestroy(exec); return set_error(SK_ECUDA, std::string("graph launch: ") + cudaGetErrorString(ce)); }
+        }
+        count_launch(per_iter * (iters - 2));   // the capture counted one iteration's kernels
+        cudaGraphExecDestroy(exec);
+        it0 = iters - 1;
+        done = iters - 1;
+    }
+    for (int it = it0; it < iters; ++it) {
+        const bool last = (it == iters - 1);
+        SK_TRY(body(it, last));
         done = it + 1;
         if (tol > 0 || last) {
             double* r = slot(P, SL_UPD);
@@ -446,6 +516,14 @@ int sinkhorn_run(sk_plan_t plan, const double* a, const double* b, int iters, do
         }
     }
     cudaEventRecord(e1, s);
+    if (trace_dev) {
+        // every trace entry is a sum over nodes: one all-reduce over ranks
+        SK_TRY(allreduce_sum(C, trace_dev, (long long)kTraceVals * iters));
+        for (int i = 0; i < kTraceVals * iters; ++i) trace[i] = NAN;
+        SK_CUDA(cudaMemcpyAsync(trace, trace_dev, sizeof(double) * kTraceVals * done, cudaMemcpyDeviceToHost, s));
+        SK_CUDA(cudaStreamSynchronize(s));
+        dev_free(trace_dev, s);
+    }
     SK_TRY(launch_permute_out(P.u_s, X.perm, X.count, u, s));
     SK_TRY(launch_permute_out(P.v_s, Y.perm, Y.count, v, s));
     SK_CUDA(cudaMemcpyAsync(hflag, P.flag, sizeof(hflag), cudaMemcpyDeviceToHost, s));
@@ -476,6 +554,17 @@ int sinkhorn_run(sk_plan_t plan, const double* a, const double* b, int iters, do
     }
     if (tol > 0 && !(resid <= tol)) return set_error(SK_ENOTCONVERGED, "residual above tol");
     return SK_OK;
+}
+
+int sinkhorn_run(sk_plan_t plan, const double* a, const double* b, int iters, double tol,
+                 int rescale_policy, double* u, double* v, sk_run_info* info) {
+    return run_impl(plan, a, b, iters, tol, rescale_policy, u, v, info, nullptr);
+}
+
+int sinkhorn_run_trace(sk_plan_t plan, const double* a, const double* b, int iters, double tol,
+                       int rescale_policy, double* u, double* v, sk_run_info* info, double* trace) {
+    if (!trace) return set_error(SK_EINVAL, "NULL trace");
+    return run_impl(plan, a, b, iters, tol, rescale_policy, u, v, info, trace);
 }
 
 int sinkhorn_divergence(sk_plan_t plan, const double* a, const double* b, const double* u,

@@ -126,15 +126,15 @@ interp3_dmma_kernel(const CellBatch* __restrict__ batches, int nbatches, const d
     const int per = (nbatches + nw - 1) / nw;
     const int b_lo = gw * per, b_hi = min(nbatches, b_lo + per);
 
+    CellBatch Bnext = b_lo < b_hi ? batches[b_lo] : CellBatch{0, 0, 0, 0};
     for (int bi = b_lo; bi < b_hi; ++bi) {
-        const CellBatch B = batches[bi];
+        const CellBatch B = Bnext;   // descriptor loaded one batch ahead
+        if (bi + 1 < b_hi) Bnext = batches[bi + 1];
         const int cz = B.cell % n, cy = (B.cell / n) % n, cx = B.cell / n / n;
         const double* T0 = taps + (long long)B.start * TS;
         const int last = B.count - 1;
-        if (bi + 1 < b_hi) {   // next batch of this warp: stream its taps into L2
-            const CellBatch Bn = batches[bi + 1];
-            prefetch_range(taps + (long long)Bn.start * TS, (long long)Bn.count * TS * 8, lane);
-        }
+        if (bi + 1 < b_hi)   // next batch of this warp: stream its taps into L2
+            prefetch_range(taps + (long long)Bnext.start * TS, (long long)Bnext.count * TS * 8, lane);
         // B fragments: phi_z of node 8 nt + g at tz = 4 s + q
         double bf[KS][4];
 #pragma unroll
@@ -284,7 +284,7 @@ spread3_dmma_kernel(const SpreadItem* __restrict__ items, int nitems, const Cell
                 const int jr = 4 * s + q;                            // node of this lane's A/B
                 const bool ok = jr < seg.count;
                 const double* tr = T0 + (ok ? jr : 0) * TS;
-                wv = ok ? __ldg(w0 + jr) : 0.0;
+                wv = __ldg(w0 + (ok ? jr : 0));   // masked at use: no predicated load to wait on
                 x0 = __ldg(tr + g);
                 x1 = (8 + g < W) ? __ldg(tr + 8 + g) : 0.0;
                 const double2* y2 = reinterpret_cast<const double2*>(tr + W);
@@ -304,7 +304,8 @@ spread3_dmma_kernel(const SpreadItem* __restrict__ items, int nitems, const Cell
                     prefetch_range(T0 + (long long)n0 * TS, (long long)(n1 - n0) * TS * 8, lane);
                     if (lane < 2) prefetch_l2(w0 + n0 + 16 * lane);
                 }
-                const double a0 = wn * x0n, a1 = wn * x1n;           // A[tx = g | 8 + g][k = q]
+                const double wu = (4 * s + q < seg.count) ? wn : 0.0;
+                const double a0 = wu * x0n, a1 = wu * x1n;           // A[tx = g | 8 + g][k = q]
                 double yv[W], zv[3];
 #pragma unroll
                 for (int i = 0; i < 6; ++i) { yv[2 * i] = yn[i].x; yv[2 * i + 1] = yn[i].y; }
@@ -413,7 +414,7 @@ spread3_hybrid_kernel(const SpreadItem* __restrict__ items, int nitems, const Ce
                     const int jr = 4 * s + q;
                     const bool ok = jr < seg.count;
                     const double* tr = T0 + (ok ? jr : 0) * TS;
-                    wv = ok ? __ldg(w0 + jr) : 0.0;
+                    wv = __ldg(w0 + (ok ? jr : 0));   // masked at use: no predicated load to wait on
                     x0 = __ldg(tr + g);
                     x8[0] = __ldg(reinterpret_cast<const double2*>(tr + 8));
                     x8[1] = __ldg(reinterpret_cast<const double2*>(tr + 10));
@@ -429,8 +430,9 @@ spread3_hybrid_kernel(const SpreadItem* __restrict__ items, int nitems, const Ce
                 load_ops(0, wn, x0n, x8n, yn, zn);
 #pragma unroll 1
                 for (int s = 0; s < nks; ++s) {
-                    const double a0 = wn * x0n;                             // A[tx = g][k = q]
-                    const double xr[4] = {wn * x8n[0].x, wn * x8n[0].y, wn * x8n[1].x, wn * x8n[1].y};
+                    const double wu = (4 * s + q < seg.count) ? wn : 0.0;
+                    const double a0 = wu * x0n;                             // A[tx = g][k = q]
+                    const double xr[4] = {wu * x8n[0].x, wu * x8n[0].y, wu * x8n[1].x, wu * x8n[1].y};
                     double yv[6], zv[3];
 #pragma unroll
                     for (int i = 0; i < 3; ++i) { yv[2 * i] = yn[i].x; yv[2 * i + 1] = yn[i].y; }

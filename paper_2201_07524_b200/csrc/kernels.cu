@@ -334,7 +334,7 @@ __global__ void finalize_kernel(const double* __restrict__ partial, int nparts, 
     }
 }
 
-constexpr int kRedGrid = 592;  // 4 x 148 SMs
+constexpr int kRedGrid = kUpdBlocks;  // 4 x 148 SMs
 
 int launch_reduce_sum_log(const double* p, const double* x, long long count, double* out_dev,
                           int op, cudaStream_t s) {
@@ -370,38 +370,58 @@ int launch_finalize_partials(const double* red, int nparts, int nvals, double* o
 }
 
 // ------------------------------------------------------------------ a7: fused update
-// x_new = p / t; partial slots: [0] sum |x_old t - p| (residual of the marginal that this
-// update makes exact, Eq. (Error)), [1] min t, [2] unused.
+// x_new = p / t; partial slots (kUpdVals per block): [0] sum |x_old t - p| (residual of the
+// marginal that this update makes exact, Eq. (Error)), [1] min t, and with
+// want_resid == 2 (diagnostics): [2] D_KL(p | x_old t) = sum p log(x_new /
+// x_old) (the Lemma at), [3] sum p log x_new (f = 1 - [3]_u - [3]_v after a step).
 __global__ void update_kernel(const double* __restrict__ t, const double* __restrict__ p,
                               double* __restrict__ x, long long count, int want_resid, int iter,
-                              int* __restrict__ bad, double* __restrict__ partial) {
+                              const int* __restrict__ iter_dev, int* __restrict__ bad,
+                              double* __restrict__ partial) {
     __shared__ double sh[kRedBlock / 32];
-    double res = 0.0, tmin = INFINITY;
+    double res = 0.0, tmin = INFINITY, kl = 0.0, slog = 0.0;
+    if (iter_dev) iter = *iter_dev;   // graph replay: iteration number from the device counter
     for (long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x; k < count;
          k += (long long)gridDim.x * blockDim.x) {
-        double tk = t[k], pk = p[k];
-        if (want_resid) res += fabs(x[k] * tk - pk);
+        const double tk = t[k], pk = p[k];
+        const double xo = x[k], xn = pk / tk;
+        if (want_resid) res += fabs(xo * tk - pk);
+        if (want_resid == 2 && pk > 0.0) {
+            kl += pk * log(xn / xo);
+            slog += pk * log(xn);
+        }
         tmin = fmin(tmin, tk);
         if (!(tk > 1e-300) || !isfinite(tk)) {  // SK_ENONPOS (tau_pos = 1e-300)
             atomicMin(bad, (int)k);
             atomicMin(bad + 1, iter);
         }
-        x[k] = pk / tk;
+        x[k] = xn;
     }
-    double r0 = block_sum<kRedBlock>(res, sh);
-    double r1 = block_min<kRedBlock>(tmin, sh);
+    const double r0 = block_sum<kRedBlock>(res, sh);
+    const double r1 = block_min<kRedBlock>(tmin, sh);
+    const double r2 = want_resid == 2 ? block_sum<kRedBlock>(kl, sh) : 0.0;
+    const double r3 = want_resid == 2 ? block_sum<kRedBlock>(slog, sh) : 0.0;
     if (threadIdx.x == 0) {
-        partial[blockIdx.x * 3 + 0] = r0;
-        partial[blockIdx.x * 3 + 1] = r1;
-        partial[blockIdx.x * 3 + 2] = 0.0;
+        partial[blockIdx.x * kUpdVals + 0] = r0;
+        partial[blockIdx.x * kUpdVals + 1] = r1;
+        partial[blockIdx.x * kUpdVals + 2] = r2;
+        partial[blockIdx.x * kUpdVals + 3] = r3;
     }
 }
 
 int launch_update(Plan& P, int side, const double* t_sorted, const double* p_sorted,
-                  double* x_sorted, int want_resid, int iter, cudaStream_t s) {
+                  double* x_sorted, int want_resid, int iter, const int* iter_dev, cudaStream_t s) {
     long long count = P.side[side].count;  // count == 0 still writes neutral partials
     update_kernel<<<kRedGrid, kRedBlock, 0, s>>>(t_sorted, p_sorted, x_sorted, count, want_resid,
-                                                 iter, P.flag + 2 * side, P.red);
+                                                 iter, iter_dev, P.flag + 2 * side, P.red);
+    SK_LAUNCH_CHECK();
+    return SK_OK;
+}
+
+__global__ void increment_kernel(int* p) { p[0] += 1; }
+
+int launch_increment(int* counter_dev, cudaStream_t s) {
+    increment_kernel<<<1, 1, 0, s>>>(counter_dev);
     SK_LAUNCH_CHECK();
     return SK_OK;
 }

@@ -3,6 +3,9 @@
 #include <cub/cub.cuh>
 #include <math.h>
 #include <algorithm>
+#include <map>
+#include <mutex>
+#include <tuple>
 #include <vector>
 
 #include "sk_internal.cuh"
@@ -80,6 +83,54 @@ static void kb_coefficients(double lam_p, double rho, int kernel, double L, int 
     c.assign(s.size() + 1, 0.0);
     c[0] = F[0];
     for (size_t i = 0; i < s.size(); ++i) c[i + 1] = s[i] / (double)(i + 1);
+}
+
+// ---------------------------------------------------------------- cuFFT plan pool
+// cufftPlanMany / cufftDestroy allocate and free work areas (device-synchronising) and cost
+// milliseconds; a plan takes its FFT handles from this pool and returns them when destroyed,
+// so back-to-back plans of one size (every bench step, every solve) reuse them. A handle is
+// owned by one plan at a time, so distinct live plans never share one.
+struct FftKey {
+    int device, d, n, type;
+    bool operator<(const FftKey& o) const {
+        return std::tie(device, d, n, type) < std::tie(o.device, o.d, o.n, o.type);
+    }
+};
+static std::mutex g_fft_mu;
+static std::multimap<FftKey, cufftHandle> g_fft_pool;
+
+static int fft_acquire(int d, int n, cufftType type, cudaStream_t s, cufftHandle* out) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    const FftKey k{dev, d, n, (int)type};
+    {
+        std::lock_guard<std::mutex> g(g_fft_mu);
+        auto it = g_fft_pool.find(k);
+        if (it != g_fft_pool.end()) {
+            *out = it->second;
+            g_fft_pool.erase(it);
+            SK_CUFFT(cufftSetStream(*out, s));
+            return SK_OK;
+        }
+    }
+    int dims[3] = {n, n, n};
+    SK_CUFFT(cufftPlanMany(out, d, dims, nullptr, 1, 0, nullptr, 1, 0, type, 1));
+    SK_CUFFT(cufftSetStream(*out, s));
+    return SK_OK;
+}
+
+static void fft_release(int d, int n, cufftType type, cufftHandle h) {
+    if (!h) return;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    std::lock_guard<std::mutex> g(g_fft_mu);
+    g_fft_pool.emplace(FftKey{dev, d, n, (int)type}, h);
+}
+
+void fft_pool_release() {
+    std::lock_guard<std::mutex> g(g_fft_mu);
+    for (auto& kv : g_fft_pool) cufftDestroy(kv.second);
+    g_fft_pool.clear();
 }
 
 // ---------------------------------------------------------------- plan
@@ -372,10 +423,8 @@ static int plan_coefficients(Plan& P, cudaStream_t s) {
     cufftDoubleComplex* B = nullptr;
     SK_TRY(alloc((void**)&samp, sizeof(double) * Md));
     SK_TRY(alloc((void**)&B, sizeof(cufftDoubleComplex) * Bsz));
-    cufftHandle h;
-    int dims[3] = {M, M, M};
-    SK_CUFFT(cufftPlanMany(&h, P.d, dims, nullptr, 1, 0, nullptr, 1, 0, CUFFT_D2Z, 1));
-    SK_CUFFT(cufftSetStream(h, s));
+    cufftHandle h = 0;
+    SK_TRY(fft_acquire(P.d, M, CUFFT_D2Z, s, &h));
     for (int kernel = 0; kernel < 2; ++kernel) {
         std::vector<double> c;
         kb_coefficients(P.lambda_p, P.rho, kernel, P.L, P.p_smooth, c);
@@ -385,7 +434,7 @@ static int plan_coefficients(Plan& P, cudaStream_t s) {
         SK_TRY(launch_band_coeffs(P, kernel, M, B, s));
     }
     SK_CUDA(cudaStreamSynchronize(s));
-    cufftDestroy(h);
+    fft_release(P.d, M, CUFFT_D2Z, h);
     sk_free(samp);
     sk_free(B);
     return SK_OK;
@@ -526,13 +575,8 @@ int build_plan(Ctx* ctx, Plan** out, int d, const double* x, long long n, const 
     if ((st = alloc((void**)&P->grid, sizeof(double) * P->grid_size))) return fail(st);
     if ((st = alloc((void**)&P->spec, sizeof(cufftDoubleComplex) * P->spec_size))) return fail(st);
     {
-        int dims[3] = {ng, ng, ng};
-        cufftResult r1 = cufftPlanMany(&P->fwd, d, dims, nullptr, 1, 0, nullptr, 1, 0, CUFFT_D2Z, 1);
-        cufftResult r2 = cufftPlanMany(&P->inv, d, dims, nullptr, 1, 0, nullptr, 1, 0, CUFFT_Z2D, 1);
-        if (r1 != CUFFT_SUCCESS || r2 != CUFFT_SUCCESS)
-            return fail(set_error(SK_ECUFFT, "cufftPlanMany failed"));
-        cufftSetStream(P->fwd, s);
-        cufftSetStream(P->inv, s);
+        if ((st = fft_acquire(d, ng, CUFFT_D2Z, s, &P->fwd))) return fail(st);
+        if ((st = fft_acquire(d, ng, CUFFT_Z2D, s, &P->inv))) return fail(st);
     }
     plan_trace("fft plans", s);
     // ---- scratch
@@ -549,7 +593,7 @@ int build_plan(Ctx* ctx, Plan** out, int d, const double* x, long long n, const 
         return fail(st);
     if ((st = alloc((void**)&P->red, sizeof(double) * 4096))) return fail(st);
     if ((st = alloc((void**)&P->red_out, sizeof(double) * 8192))) return fail(st);
-    if ((st = alloc((void**)&P->flag, sizeof(int) * 4))) return fail(st);
+    if ((st = alloc((void**)&P->flag, sizeof(int) * 8))) return fail(st);
     if (cudaMallocHost((void**)&P->host_red, sizeof(double) * 64) != cudaSuccess)
         return fail(set_error(SK_ENOMEM, "cudaMallocHost"));
     plan_trace("scratch", s);
@@ -567,8 +611,9 @@ int destroy_plan(Plan* P) {
     }
     sk_free(P->grid); sk_free(P->spec);
     for (int k = 0; k < 2; ++k) { sk_free(P->D[k]); sk_free(P->bk[k]); }
-    if (P->fwd) cufftDestroy(P->fwd);
-    if (P->inv) cufftDestroy(P->inv);
+    fft_release(P->d, P->n, CUFFT_D2Z, P->fwd);
+    fft_release(P->d, P->n, CUFFT_Z2D, P->inv);
+    if (P->cap_stream) cudaStreamDestroy(P->cap_stream);
     sk_free(P->w_sorted); sk_free(P->t_sorted);
     sk_free(P->a_s); sk_free(P->b_s); sk_free(P->u_s); sk_free(P->v_s);
     sk_free(P->red); sk_free(P->red_out); sk_free(P->flag); sk_free(P->box_buf);

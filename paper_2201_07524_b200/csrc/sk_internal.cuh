@@ -95,13 +95,14 @@ struct Plan {
     double* D[2] = {nullptr, nullptr};  // multiplier tables (kernel 0, 1) over the half band
     double* bk[2] = {nullptr, nullptr}; // b_k on the full band (N+1)^d (diagnostics)
     cufftHandle fwd = 0, inv = 0;
+    cudaStream_t cap_stream = nullptr;  // private stream for CUDA-graph capture of iterations
     // scratch
     double* w_sorted = nullptr;   // [max count]
     double* t_sorted = nullptr;   // [max count]
     double* red = nullptr;        // block partials
     double* red_out = nullptr;    // reduced scalars (device)
     double* host_red = nullptr;   // pinned host mirror
-    int* flag = nullptr;          // device error flag / first bad index
+    int* flag = nullptr;          // [0..3] first bad (index, iteration) per side, [4] graph iteration counter
     // Sinkhorn state in sorted order
     double* a_s = nullptr; double* b_s = nullptr; double* u_s = nullptr; double* v_s = nullptr;
     long long max_count = 0;
@@ -140,8 +141,11 @@ int launch_sample_kernel(Plan& P, int kernel, int M, const double* kb_coef, int 
 int launch_band_coeffs(Plan& P, int kernel, int M, const cufftDoubleComplex* B, cudaStream_t s);
 // Sinkhorn fused update: x_s <- p_s / t (t = interpolated), partial sums into red
 int launch_update(Plan& P, int side, const double* t_sorted, const double* p_sorted,
-                  double* x_sorted, int want_resid, int iter, cudaStream_t s);
+                  double* x_sorted, int want_resid, int iter, const int* iter_dev, cudaStream_t s);
+int launch_increment(int* counter_dev, cudaStream_t s);   // counter_dev[0] += 1 (graph iteration counter)
 int launch_fill(double* p, long long count, double v, cudaStream_t s);
+constexpr int kUpdVals = 4;     // update_kernel partials per block (residual, min t, KL, sum p log x)
+constexpr int kUpdBlocks = 592; // update / reduction grid (4 x 148 SMs)
 // a3: grid box <-> packed buffer (dir 0: pack grid -> buf, 1: unpack buf -> grid)
 int launch_box_copy(const Plan& P, double* grid, double* buf, int dir, cudaStream_t s);
 int launch_scale_vec(double* p, long long count, const double* scale_dev, cudaStream_t s);
@@ -154,6 +158,7 @@ int launch_finalize_partials(const double* red, int nparts, int nvals, double* o
 int build_plan(Ctx* ctx, Plan** out, int d, const double* x, long long n, const double* y,
                long long m, double lambda, int N, double sigma, int m_w, double eps_B, int p);
 int destroy_plan(Plan* P);
+void fft_pool_release();   // destroy the pooled cuFFT handles (sk_release_cache)
 int apply_sorted(Plan& P, int transpose, int kernel, const double* w_sorted, double* t_sorted);
 
 // ---- stage profiling (api.cu): CUDA-event pairs around each stage when enabled ----

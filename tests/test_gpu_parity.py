@@ -337,3 +337,61 @@ def test_image_matvec_parity(capi, ctx, name):
     weights = {"marginal": (b, a), "uniform01": (uniform_test_weights(ci, y.shape[0]), uniform_test_weights(ci, x.shape[0], 1))}
     worst = _matvec_case(capi, ctx, cfg, x, y, a, b, rx, ry, weights)
     assert max(max(v) for v in worst.values()) <= 1e-9, worst
+
+
+# ------------------------------------------------------------------ NEXT-3: diagnostics, stopping, lambda sweep
+def _c1_small():
+    cfg = get("c1")
+    x, y, a, b = make_inputs(cfg)
+    return cfg, x[:400], y[:300], a[:400] / a[:400].sum(), b[:300] / b[:300].sum()
+
+
+def test_trace_matches_oracle(capi, ctx):
+    """Per-iteration residuals ||E||_1 (Eq. (Error)), KL terms (Lemma P:L353) and
+    sum p log alpha of the GPU run against oracle.diagnostics on the same inputs."""
+    from oracle import diagnostics as D
+    cfg, x, y, a, b = _c1_small()
+    lam, iters = 30.0, 25
+    ref, al, at = D.sinkhorn_trace(x, y, a, b, lam, iters)
+    P = capi.Plan(ctx, dev(x), dev(y), lam, cfg.N, cfg.sigma, cfg.m_w, cfg.eps_B, cfg.p)
+    u, v, info, tr = capi.sinkhorn_run_trace(P, dev(a), dev(b), iters)
+    assert info.iters_done == iters and tr.shape == ref.shape
+    err = np.abs(tr - ref)
+    assert (err <= 1e-9 * np.maximum(1.0, np.abs(ref)) + 1e-12).all(), (err.max(axis=0), ref[-1], tr[-1])
+    # the run itself is unchanged by tracing (up to the order of the spread's FP64 atomics)
+    u2, v2, _ = capi.sinkhorn_run(P, dev(a), dev(b), iters)
+    assert float(((u - u2).abs() / u2).max()) < 1e-11 and float(((v - v2).abs() / v2).max()) < 1e-11
+
+
+def test_residual_stopping_matches_oracle(capi, ctx):
+    """tol > 0 (reading Q5): stop after the first iteration whose residual ||pi 1 - p||_1 (measured
+    at its u-update) is <= tol; the oracle's trace fixes which iteration that is."""
+    from oracle import diagnostics as D
+    cfg, x, y, a, b = _c1_small()
+    lam, tol = 30.0, 1e-7
+    ref, *_ = D.sinkhorn_trace(x, y, a, b, lam, 60)
+    want = next(it + 1 for it in range(60) if ref[it, 0] <= tol)
+    P = capi.Plan(ctx, dev(x), dev(y), lam, cfg.N, cfg.sigma, cfg.m_w, cfg.eps_B, cfg.p)
+    u, v, info = capi.sinkhorn_run(P, dev(a), dev(b), 60, tol=tol)
+    assert info.iters_done == want and info.residual <= tol
+    with pytest.raises(capi.SkError) as e:
+        capi.sinkhorn_run(P, dev(a), dev(b), 3, tol=1e-14)
+    assert e.value.code == capi.SK_ENOTCONVERGED
+
+
+@pytest.mark.parametrize("lam", [5.0, 10.0, 15.0, 20.0, 25.0])
+def test_lambda_sweep_sandwich(capi, ctx, lam):
+    """Fig. 3: n = n~ = 1000 at lambda in {5, ..., 25}, r = 2 (d = 1, c1 inputs).
+    GPU s and s~ equal the oracle's, and s <= W_2^2 <= s~ with W_2^2 from the exact 1-D
+    quantile formula (Prop. 3.3 sandwich). N = 128: at lambda = 5 the kernel is still
+    e^-5 at the regularisation radius L, and N = 64 leaves a 2e-8 fast-summation error
+    (oracle.nfft_ref.fastsum_ndft, the method's own error); N = 128 gives 4e-11."""
+    from oracle import exact_ot
+    cfg = get("c1")
+    x, y, a, b = make_inputs(cfg)
+    ref, _, _ = dense.sinkhorn_divergence(x, y, a, b, lam, 300)
+    sd, sc, info, *_ = _gpu_divergence(capi, ctx, cfg.with_(lam=lam, N=128), x, y, a, b, iters=300)
+    assert abs(sc - ref["s_cost"]) <= 1e-9 * abs(ref["s_cost"]), (lam, sc, ref)
+    assert abs(sd - ref["s_dual"]) <= 1e-9 * abs(ref["s_dual"]), (lam, sd, ref)
+    W = exact_ot.w2_1d(x[:, 0], a, y[:, 0], b)
+    assert sd <= W <= sc
