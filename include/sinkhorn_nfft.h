@@ -65,7 +65,11 @@ typedef struct {
 /* Create a context on `device` (the current CUDA device is switched to it). rank/world_size
  * describe the SPMD job; nccl_unique_id: 128-byte ncclUniqueId (host) from
  * sk_nccl_unique_id() on rank 0, broadcast by the caller; NULL iff world_size == 1.
- * cuda_stream: cudaStream_t to enqueue on (NULL = legacy default stream). */
+ * cuda_stream: cudaStream_t to enqueue on (NULL = legacy default stream).
+ * Test hook: with world_size == 1 and the environment variable SK_EMULATE_WORLD=k (k >= 2) the
+ * context behaves as k ranks holding identical shards (every sum over ranks is k times the
+ * local one, min/max are unchanged, no NCCL), which exercises every multi-rank code path
+ * (global counts, box exchange, scalar all-reduces) on one GPU. */
 int sinkhorn_init(sk_ctx_t* ctx, int device, int rank, int world_size,
                   const void* nccl_unique_id, void* cuda_stream);
 int sinkhorn_finalize(sk_ctx_t ctx);

@@ -296,6 +296,18 @@ int launch_scale_vec(double* p, long long count, const double* scale_dev, cudaSt
     return SK_OK;
 }
 
+__global__ void scale_const_kernel(double* p, long long count, double c) {
+    for (long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x; k < count;
+         k += (long long)gridDim.x * blockDim.x)
+        p[k] *= c;
+}
+int launch_scale_const(double* p, long long count, double c, cudaStream_t s) {
+    if (count <= 0) return SK_OK;
+    scale_const_kernel<<<grid_for(count, 256), 256, 0, s>>>(p, count, c);
+    SK_LAUNCH_CHECK();
+    return SK_OK;
+}
+
 // ------------------------------------------------------------------ a8: reductions
 // op 0: sum p_i log x_i;  op 1: sum x_i;  op 2: sum p_i x_i;  op 3: sum log x_i;  op 4: max x_i
 __global__ void reduce_kernel(const double* __restrict__ p, const double* __restrict__ x,

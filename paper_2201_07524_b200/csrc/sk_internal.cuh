@@ -74,6 +74,7 @@ struct Ctx {
     int world = 1;
     cudaStream_t stream = nullptr;
     void* nccl_comm = nullptr;    // ncclComm_t when world > 1
+    bool emulated = false;        // SK_EMULATE_WORLD test hook: `world` identical ranks, no NCCL
 };
 
 struct Plan {
@@ -149,6 +150,7 @@ constexpr int kUpdBlocks = 592; // update / reduction grid (4 x 148 SMs)
 // a3: grid box <-> packed buffer (dir 0: pack grid -> buf, 1: unpack buf -> grid)
 int launch_box_copy(const Plan& P, double* grid, double* buf, int dir, cudaStream_t s);
 int launch_scale_vec(double* p, long long count, const double* scale_dev, cudaStream_t s);
+int launch_scale_const(double* p, long long count, double c, cudaStream_t s);
 int launch_reduce_sum_log(const double* p, const double* x, long long count, double* out_dev,
                           int op, cudaStream_t s);
 int launch_rescale_factor(double* r, int policy, double total, cudaStream_t s);

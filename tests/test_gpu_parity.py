@@ -395,3 +395,40 @@ def test_lambda_sweep_sandwich(capi, ctx, lam):
     assert abs(sd - ref["s_dual"]) <= 1e-9 * abs(ref["s_dual"]), (lam, sd, ref)
     W = exact_ot.w2_1d(x[:, 0], a, y[:, 0], b)
     assert sd <= W <= sc
+
+
+# ------------------------------------------------------------------ multi-rank code paths on one GPU
+def test_emulated_two_rank_world(capi):
+    """SK_EMULATE_WORLD=2: two ranks with identical shards (x, y, weights a/2, b/2 on each), i.e.
+    every atom duplicated with half its mass. Every multi-rank path runs (global counts via the
+    sum all-reduce, box exchange of the grid, scalar all-reduces). Exact consequences:
+    K_global v = 2 K v; the Sinkhorn iterates are U = u/4, V = v at every iteration, so
+    s~ is unchanged and s drops by log(4)/lambda (Eq. (14) P:L211 with sum p = 1)."""
+    cfg = get("c3").with_(n=20000, m=15000)
+    x, y, a, b = make_inputs(cfg)
+    a, b = a / a.sum(), b / b.sum()
+    iters = 20
+    c1 = capi.Context(0)
+    P1 = capi.Plan(c1, dev(x), dev(y), cfg.lam, cfg.N, cfg.sigma, cfg.m_w, cfg.eps_B, cfg.p)
+    w = dev(uniform_test_weights(3, y.shape[0]))
+    t1 = capi.fastsum_apply(P1, w, 0, 0)
+    u1, v1, _ = capi.sinkhorn_run(P1, dev(a), dev(b), iters)
+    sd1, sc1 = capi.sinkhorn_divergence(P1, dev(a), dev(b), u1, v1)
+    os.environ["SK_EMULATE_WORLD"] = "2"
+    try:
+        c2 = capi.Context(0)
+    finally:
+        del os.environ["SK_EMULATE_WORLD"]
+    P2 = capi.Plan(c2, dev(x), dev(y), cfg.lam, cfg.N, cfg.sigma, cfg.m_w, cfg.eps_B, cfg.p)
+    info = P2.info()
+    assert info["total_x"] == 2 * x.shape[0] and info["total_y"] == 2 * y.shape[0]
+    t2 = capi.fastsum_apply(P2, w, 0, 0)
+    assert float(((t2 - 2 * t1).abs()).max() / t1.abs().max()) < 1e-13
+    u2, v2, _ = capi.sinkhorn_run(P2, dev(a / 2), dev(b / 2), iters)
+    assert float(((4 * u2 - u1).abs() / u1).max()) < 1e-11 and float(((v2 - v1).abs() / v1).max()) < 1e-11
+    sd2, sc2 = capi.sinkhorn_divergence(P2, dev(a / 2), dev(b / 2), u2, v2)
+    assert abs(sc2 - sc1) <= 1e-11 * abs(sc1)
+    assert abs(sd2 - (sd1 - math.log(4) / cfg.lam)) <= 1e-11 * abs(sd1)
+    for P, c in ((P1, c1), (P2, c2)):
+        P.close()
+        c.close()
