@@ -89,6 +89,30 @@ int sk_nccl_unique_id(void* out);
 int fastsum_plan(sk_ctx_t ctx, sk_plan_t* plan, int d,
                  const double* x, long long n_local, const double* y, long long m_local,
                  double lambda, int N, double sigma, int m_w, double eps_B, int p_smooth);
+
+/* Extended plan: the cost |x - y|^r for r in {1, 2}.
+ * r = 2 is fastsum_plan. r = 1 is the Laplace kernel exp(-lambda |x - y|) (P:L456-470 with
+ * r = 1): lambda' = lambda / rho; the kernel is also regularised at 0 by
+ *   K_I(r) = sum_{i < p_smooth} c_i (r / a)^{2i} on r <= a = near_cells / (sigma N) (torus
+ *   units), K_I^{(k)}(a) = K^{(k)}(a) for k < p_smooth (even, so smooth at 0),
+ * the Fourier series is built from K_I | K | K_B, and every fast summation adds the near field
+ *   t_i += sum over |x'_i - y'_j| < a of w_j (K - K_I)(|x'_i - y'_j|)
+ * (direct sum over the source tiles around each target). The divergence kernel c K uses
+ * c = |x - y| in original units. r = 1 runs the plain spread / interp kernels.
+ * Errors: SK_EINVAL for r not in {1, 2}, near_cells < 1, p_smooth > 8 (r = 1; the monomial K_I system is ill-conditioned beyond) or
+ * a >= 1/2 - eps_B; otherwise as fastsum_plan. */
+typedef struct {
+    double lambda;
+    int    r;             /* 1 or 2 */
+    int    N;
+    double sigma;
+    int    m_w;
+    double eps_B;
+    int    p_smooth;
+    int    near_cells;    /* r = 1: near-field radius in oversampled-grid cells */
+} sk_plan_opts;
+int fastsum_plan_ex(sk_ctx_t ctx, sk_plan_t* plan, int d, const double* x, long long n_local,
+                    const double* y, long long m_local, const sk_plan_opts* opts);
 int fastsum_plan_destroy(sk_plan_t plan);
 
 /* One fast-summation matvec (Eq. (matexp)/(matexpt)):

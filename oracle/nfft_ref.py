@@ -122,15 +122,16 @@ def radial_kernel(r, lamp, rho, kernel):
     return k if kernel == 0 else (r * r / rho ** 2) * k
 
 
-def taylor_KB(lamp, rho, kernel, L, p, h=1.0):
+def taylor_KB(lamp, rho, kernel, L, p, h=1.0, derivs=None):
     """Coefficients c of K_B(r) = sum_i c_i t^i, t = (r - L)/(h/2 - L), degree 2p - 2,
-    solving the 2p - 1 interpolation conditions (intpol_cond_3/4)."""
+    solving the 2p - 1 interpolation conditions (intpol_cond_3/4).
+    derivs(r, p): [K^{(k)}(r), k < p] of the radial profile (default: the r = 2 kernels)."""
     D = h / 2 - L
     deg = 2 * p - 2
     nc = deg + 1
     A = np.zeros((nc, nc))
     rhs = np.zeros(nc)
-    dK = _radial_derivs(L, lamp, rho, kernel, p)
+    dK = derivs(L, p) if derivs is not None else _radial_derivs(L, lamp, rho, kernel, p)
     row = 0
     # d^k/dr^k at r = L (t = 0): k! c_k / D^k = K^{(k)}(L)
     for k in range(p):

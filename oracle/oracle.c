@@ -10,7 +10,7 @@
  * Everything here is a dense, direct evaluation of a definition from the
  * paper, written in the paper's order (P:Lx = /root/reference/PAPER.md line x):
  *
- *   oracle_direct_sum     Eq. (matexp)  P:L462-465  t_i = sum_j w_j exp(-lam |x_i - y_j|^2)
+ *   oracle_direct_sum     Eq. (matexp)  P:L462-465  t_i = sum_j w_j exp(-lam |x_i - y_j|^r)
  *                         Eq. (matexpt) P:L467-470  (transpose = swap the point sets)
  *                         kernel 1: c_ij exp(-lam c_ij), the integrand of the upper
  *                         divergence s~ = sum_ij pi_ij d_ij^r (Def 3.1)
@@ -28,8 +28,9 @@
  *                         residuals |pi 1 - a|_1, |pi^T 1 - b|_1  (Eq. (Error))
  *                         H(pi) = -sum pi log pi                  (Def 3.1)
  *
- * Cost c_ij = sum_a (x_ia - y_ja)^2 in the caller's coordinates (r = 2; d_ij^r with
- * d the Euclidean distance). All sums are Neumaier-compensated. Rows are
+ * Cost c_ij = d_ij^r with d_ij = |x_i - y_j| the Euclidean distance in the caller's
+ * coordinates, r = 2 (squared Euclidean, the BJ hot path) or r = 1 (Euclidean,
+ * SURVEY §8(f) NEXT-2); every entry point takes r. All sums are Neumaier-compensated. Rows are
  * independent and are distributed over OpenMP threads; each row is summed
  * serially in index order, so results do not depend on the thread count.
  */
@@ -51,10 +52,10 @@ static inline void kadd(kahan_t* k, double v) {
 }
 static inline double kval(const kahan_t* k) { return k->s + k->c; }
 
-static inline double cost(int d, const double* xi, const double* yj) {
+static inline double cost(int d, int r, const double* xi, const double* yj) {
     double c = 0.0;
     for (int a = 0; a < d; ++a) { double t = xi[a] - yj[a]; c += t * t; }
-    return c;
+    return r == 2 ? c : sqrt(c);
 }
 
 int oracle_num_threads(void) {
@@ -73,31 +74,31 @@ void oracle_set_threads(int nt) {
 #endif
 }
 
-/* t[r] = sum_j w[j] K(x[rows[r]], y[j]); rows == NULL means all n rows (r = i).
+/* t[q] = sum_j w[j] K(x[rows[q]], y[j]); rows == NULL means all n rows (q = i).
  * kernel 0: K = exp(-lam c); kernel 1: K = c exp(-lam c). */
 void oracle_direct_sum(int d, const double* x, long long n, const double* y, long long m,
-                       const double* w, double lam, int kernel,
+                       const double* w, double lam, int r, int kernel,
                        const long long* rows, long long nrows, double* t) {
     long long R = rows ? nrows : n;
     #pragma omp parallel for schedule(dynamic, 16)
-    for (long long r = 0; r < R; ++r) {
-        long long i = rows ? rows[r] : r;
+    for (long long q = 0; q < R; ++q) {
+        long long i = rows ? rows[q] : q;
         const double* xi = x + i * d;
         kahan_t acc = {0.0, 0.0};
         for (long long j = 0; j < m; ++j) {
-            double c = cost(d, xi, y + j * d);
+            double c = cost(d, r, xi, y + j * d);
             double k = exp(-lam * c);
             if (kernel == 1) k *= c;
             kadd(&acc, w[j] * k);
         }
-        t[r] = kval(&acc);
+        t[q] = kval(&acc);
     }
 }
 
 /* Alg. 1 in the plain (scaling) domain, fixed iteration count. Returns the number of
  * a non-positive / non-finite denominator (0 if none). alpha, alpha_t: out. */
 int oracle_sinkhorn_plain(int d, const double* x, long long n, const double* y, long long m,
-                          const double* a, const double* b, double lam, int iters,
+                          const double* a, const double* b, double lam, int r, int iters,
                           double* alpha, double* alpha_t) {
     int bad = 0;
     for (long long i = 0; i < n; ++i) alpha[i] = 1.0;
@@ -108,7 +109,7 @@ int oracle_sinkhorn_plain(int d, const double* x, long long n, const double* y, 
         for (long long i = 0; i < n; ++i) {
             kahan_t acc = {0.0, 0.0};
             for (long long j = 0; j < m; ++j)
-                kadd(&acc, exp(-lam * cost(d, x + i * d, y + j * d)) * alpha_t[j]);
+                kadd(&acc, exp(-lam * cost(d, r, x + i * d, y + j * d)) * alpha_t[j]);
             double s = kval(&acc);
             if (!(s > 0.0) || !isfinite(s)) bad += 1;
             alpha[i] = a[i] / s;
@@ -118,7 +119,7 @@ int oracle_sinkhorn_plain(int d, const double* x, long long n, const double* y, 
         for (long long j = 0; j < m; ++j) {
             kahan_t acc = {0.0, 0.0};
             for (long long i = 0; i < n; ++i)
-                kadd(&acc, exp(-lam * cost(d, x + i * d, y + j * d)) * alpha[i]);
+                kadd(&acc, exp(-lam * cost(d, r, x + i * d, y + j * d)) * alpha[i]);
             double s = kval(&acc);
             if (!(s > 0.0) || !isfinite(s)) bad += 1;
             alpha_t[j] = b[j] / s;
@@ -128,16 +129,16 @@ int oracle_sinkhorn_plain(int d, const double* x, long long n, const double* y, 
 }
 
 /* log-sum-exp of lam*(pot[j] - c(p, q_j)) over j, two passes (max, then compensated sum). */
-static double lse_row(int d, const double* p, const double* q, long long cnt,
+static double lse_row(int d, int r, const double* p, const double* q, long long cnt,
                       const double* pot, double lam) {
     double mx = -INFINITY;
     for (long long j = 0; j < cnt; ++j) {
-        double v = lam * (pot[j] - cost(d, p, q + j * d));
+        double v = lam * (pot[j] - cost(d, r, p, q + j * d));
         if (v > mx) mx = v;
     }
     kahan_t acc = {0.0, 0.0};
     for (long long j = 0; j < cnt; ++j) {
-        double v = lam * (pot[j] - cost(d, p, q + j * d));
+        double v = lam * (pot[j] - cost(d, r, p, q + j * d));
         kadd(&acc, exp(v - mx));
     }
     return mx + log(kval(&acc));
@@ -146,24 +147,24 @@ static double lse_row(int d, const double* p, const double* q, long long cnt,
 /* Log-domain Alg. 1: g^0 = 0 (alpha~ = 1), u (f) first, fixed iters. f, g: out.
  * f_in/g_in may be NULL (cold start) or a warm start for g (f_in ignored). */
 void oracle_sinkhorn_log(int d, const double* x, long long n, const double* y, long long m,
-                         const double* a, const double* b, double lam, int iters,
+                         const double* a, const double* b, double lam, int r, int iters,
                          const double* g_in, double* f, double* g) {
     for (long long j = 0; j < m; ++j) g[j] = g_in ? g_in[j] : 0.0;
     for (long long i = 0; i < n; ++i) f[i] = 0.0;
     for (int it = 0; it < iters; ++it) {
         #pragma omp parallel for schedule(static)
         for (long long i = 0; i < n; ++i)
-            f[i] = (log(a[i]) - lse_row(d, x + i * d, y, m, g, lam)) / lam;
+            f[i] = (log(a[i]) - lse_row(d, r, x + i * d, y, m, g, lam)) / lam;
         #pragma omp parallel for schedule(static)
         for (long long j = 0; j < m; ++j)
-            g[j] = (log(b[j]) - lse_row(d, y + j * d, x, n, f, lam)) / lam;
+            g[j] = (log(b[j]) - lse_row(d, r, y + j * d, x, n, f, lam)) / lam;
     }
 }
 
 /* out[0] = s~ (upper, transport cost), out[1] = s (dual / lower, Eq. (14)),
  * out[2] = sum pi, out[3] = |pi 1 - a|_1, out[4] = |pi^T 1 - b|_1, out[5] = H(pi). */
 void oracle_divergence(int d, const double* x, long long n, const double* y, long long m,
-                       const double* a, const double* b, double lam,
+                       const double* a, const double* b, double lam, int r,
                        const double* f, const double* g, double* out) {
     kahan_t cost_acc = {0, 0}, mass = {0, 0}, ent = {0, 0}, rres = {0, 0}, cres = {0, 0};
     kahan_t af = {0, 0}, bg = {0, 0};
@@ -175,7 +176,7 @@ void oracle_divergence(int d, const double* x, long long n, const double* y, lon
     for (long long i = 0; i < n; ++i) {
         kahan_t sc = {0, 0}, sm = {0, 0}, se = {0, 0};
         for (long long j = 0; j < m; ++j) {
-            double c = cost(d, x + i * d, y + j * d);
+            double c = cost(d, r, x + i * d, y + j * d);
             double lp = lam * (f[i] + g[j] - c);
             double pij = exp(lp);
             kadd(&sc, pij * c);
@@ -197,7 +198,7 @@ void oracle_divergence(int d, const double* x, long long n, const double* y, lon
     for (long long j = 0; j < m; ++j) {
         kahan_t s = {0, 0};
         for (long long i = 0; i < n; ++i)
-            kadd(&s, exp(lam * (f[i] + g[j] - cost(d, x + i * d, y + j * d))));
+            kadd(&s, exp(lam * (f[i] + g[j] - cost(d, r, x + i * d, y + j * d))));
         colsum[j] = kval(&s);
     }
     for (long long j = 0; j < m; ++j) {

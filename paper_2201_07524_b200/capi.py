@@ -32,6 +32,12 @@ _NAMES = {0: "SK_OK", 1: "SK_EINVAL", 2: "SK_EGEOMETRY", 3: "SK_ENONPOS", 4: "SK
           5: "SK_ECUDA", 6: "SK_ECUFFT", 7: "SK_ENCCL", 8: "SK_ENOMEM"}
 
 
+class PlanOpts(ctypes.Structure):
+    _fields_ = [("lam", ctypes.c_double), ("r", ctypes.c_int), ("N", ctypes.c_int), ("sigma", ctypes.c_double),
+                ("m_w", ctypes.c_int), ("eps_B", ctypes.c_double), ("p_smooth", ctypes.c_int),
+                ("near_cells", ctypes.c_int)]
+
+
 class RunInfo(ctypes.Structure):
     _fields_ = [("iters_done", ctypes.c_int), ("residual", ctypes.c_double), ("bad_iter", ctypes.c_int),
                 ("bad_index", ctypes.c_longlong), ("kappa_log10_est", ctypes.c_double),
@@ -53,6 +59,7 @@ _sig = {
     "sinkhorn_finalize": ([_vp], _i),
     "sk_nccl_unique_id": ([_vp], _i),
     "fastsum_plan": ([_vp, ctypes.POINTER(_vp), _i, _vp, _ll, _vp, _ll, _d, _i, _d, _i, _d, _i], _i),
+    "fastsum_plan_ex": ([_vp, ctypes.POINTER(_vp), _i, _vp, _ll, _vp, _ll, ctypes.POINTER(PlanOpts)], _i),
     "fastsum_plan_destroy": ([_vp], _i),
     "fastsum_apply": ([_vp, _i, _i, _vp, _vp], _i),
     "sinkhorn_run": ([_vp, _vp, _vp, _i, _d, _i, _vp, _vp, ctypes.POINTER(RunInfo)], _i),
@@ -169,14 +176,21 @@ class Plan:
     """fastsum_plan / fastsum_plan_destroy (x: [n, d], y: [m, d] CUDA float64)."""
 
     def __init__(self, ctx: Context, x: torch.Tensor, y: torch.Tensor, lam: float, N: int, sigma: float = 2.0,
-                 m_w: int = 8, eps_B: float = 1 / 16, p_smooth: int = 8):
+                 m_w: int = 8, eps_B: float = 1 / 16, p_smooth: int = 8, r: int = 2, near_cells: int = 16):
+        """r = 2: fastsum_plan; r = 1: fastsum_plan_ex (Laplace kernel + near field)."""
         d = x.shape[1] if x.dim() == 2 else 1
         self.ctx, self.d = ctx, d
         self.n, self.m = x.shape[0], y.shape[0]
-        self.lam = lam
+        self.lam, self.r = lam, r
         h = _vp()
-        _check(_lib.fastsum_plan(ctx.handle, ctypes.byref(h), d, _ptr(x), self.n, _ptr(y), self.m, float(lam),
-                                 int(N), float(sigma), int(m_w), float(eps_B), int(p_smooth)))
+        if r == 2:
+            _check(_lib.fastsum_plan(ctx.handle, ctypes.byref(h), d, _ptr(x), self.n, _ptr(y), self.m, float(lam),
+                                     int(N), float(sigma), int(m_w), float(eps_B), int(p_smooth)))
+        else:
+            o = PlanOpts(float(lam), int(r), int(N), float(sigma), int(m_w), float(eps_B), int(p_smooth),
+                         int(near_cells))
+            _check(_lib.fastsum_plan_ex(ctx.handle, ctypes.byref(h), d, _ptr(x), self.n, _ptr(y), self.m,
+                                        ctypes.byref(o)))
         self.handle = h
         info = self.info()
         self.grid_n = int(info["n_grid"])

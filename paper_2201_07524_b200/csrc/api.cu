@@ -313,7 +313,20 @@ int fastsum_plan(sk_ctx_t ctx, sk_plan_t* plan, int d, const double* x, long lon
     if (!ctx || !plan) return set_error(SK_EINVAL, "NULL ctx/plan");
     SK_CUDA(cudaSetDevice(ctx->c.device));
     Plan* P = nullptr;
-    SK_TRY(build_plan(&ctx->c, &P, d, x, n_local, y, m_local, lambda, N, sigma, m_w, eps_B, p_smooth));
+    SK_TRY(build_plan(&ctx->c, &P, d, x, n_local, y, m_local, lambda, N, sigma, m_w, eps_B, p_smooth, 2, 0));
+    sk_plan* h = new sk_plan();
+    h->p = P;
+    *plan = h;
+    return SK_OK;
+}
+
+int fastsum_plan_ex(sk_ctx_t ctx, sk_plan_t* plan, int d, const double* x, long long n_local,
+                    const double* y, long long m_local, const sk_plan_opts* o) {
+    if (!ctx || !plan || !o) return set_error(SK_EINVAL, "NULL ctx/plan/opts");
+    SK_CUDA(cudaSetDevice(ctx->c.device));
+    Plan* P = nullptr;
+    SK_TRY(build_plan(&ctx->c, &P, d, x, n_local, y, m_local, o->lambda, o->N, o->sigma, o->m_w, o->eps_B,
+                      o->p_smooth, o->r, o->near_cells));
     sk_plan* h = new sk_plan();
     h->p = P;
     *plan = h;

@@ -443,12 +443,26 @@ struct KernelParams {
     double lam_p, rho2_inv, L, half, tscale;  // tscale = 1 / (1/2 - L)
     int d, M, kernel, kb_deg;
     double kb[32];                          // K_B coefficients in t = (r - L) / (1/2 - L)
+    // r = 1 (NEXT-2): K(r) = exp(-lam' r) (c K with c = r / rho), K_I on r <= near_a
+    int rpow, ki_n;
+    double rho_inv, near_a;
+    double ki[16];                          // K_I coefficients in (r / near_a)^2
 };
 
 __device__ __forceinline__ double radial(double r, const KernelParams& kp) {
+    if (kp.rpow == 1) {
+        const double k = exp(-kp.lam_p * r);
+        return kp.kernel == 0 ? k : r * kp.rho_inv * k;
+    }
     double r2 = r * r;
     double k = exp(-kp.lam_p * r2);
     return kp.kernel == 0 ? k : r2 * kp.rho2_inv * k;
+}
+__device__ __forceinline__ double ki_poly(double r, const double* c, int nc, double a) {
+    const double t2 = (r / a) * (r / a);
+    double acc = c[nc - 1];
+    for (int i = nc - 2; i >= 0; --i) acc = acc * t2 + c[i];
+    return acc;
 }
 __device__ __forceinline__ double kb_poly(double r, const KernelParams& kp) {
     double t = (r - kp.L) * kp.tscale;
@@ -470,7 +484,8 @@ __global__ void sample_kernel_kernel(KernelParams kp, double* __restrict__ out, 
         }
         double r = sqrt(r2);
         double v;
-        if (r <= kp.L) v = radial(r, kp);
+        if (kp.rpow == 1 && r <= kp.near_a) v = ki_poly(r, kp.ki, kp.ki_n, kp.near_a);
+        else if (r <= kp.L) v = radial(r, kp);
         else if (r <= kp.half) v = kb_poly(r, kp);
         else v = kb_poly(kp.half, kp);
         out[e] = v;
@@ -490,6 +505,11 @@ int launch_sample_kernel(Plan& P, int kernel, int M, const double* kb_coef, int 
     kp.kernel = kernel;
     kp.kb_deg = kb_deg;
     for (int i = 0; i <= kb_deg && i < 32; ++i) kp.kb[i] = kb_coef[i];
+    kp.rpow = P.rpow;
+    kp.rho_inv = 1.0 / P.rho;
+    kp.near_a = P.near_a;
+    kp.ki_n = P.ki_n;
+    for (int i = 0; i < 16; ++i) kp.ki[i] = P.ki[kernel][i];
     long long total = 1;
     for (int a = 0; a < P.d; ++a) total *= M;
     sample_kernel_kernel<<<grid_for(total, 256), 256, 0, s>>>(kp, out, total);
@@ -562,6 +582,81 @@ int launch_band_coeffs(Plan& P, int kernel, int M, const cufftDoubleComplex* B, 
     long long total = 1;
     for (int a = 0; a < P.d; ++a) total *= (P.N + 1);
     band_kernel<<<grid_for(total, 256), 256, 0, s>>>(bp, B, P.bk[kernel], P.D[kernel]);
+    SK_LAUNCH_CHECK();
+    return SK_OK;
+}
+
+// ------------------------------------------------------------------ r = 1 near field (NEXT-2)
+// t_i += sum over sources j with |x'_i - y'_j| < a of w_j (K - K_I)(|x'_i - y'_j|): the part
+// of the Laplace kernel that the inner regularisation K_I removed from the Fourier series
+// ("we add a so called nearfield"). One thread per target (sorted order); candidate
+// sources come from the source tiles (v1 path CSR) covering the target's cell +- near_cells.
+struct NearParams {
+    int d, n, T, tpa, R, ki_n, kernel;
+    double a, lam_p, rho_inv, inv_n;
+    double ki[16];
+};
+
+__global__ void nearfield_kernel(NearParams np, const double* __restrict__ ut, long long nt,
+                                 const double* __restrict__ us, long long ns,
+                                 const int* __restrict__ tile_start, const double* __restrict__ w,
+                                 double* __restrict__ t) {
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < nt;
+         i += (long long)gridDim.x * blockDim.x) {
+        double ui[kMaxD];
+        int lo[kMaxD] = {0, 0, 0}, hi[kMaxD] = {0, 0, 0};
+        for (int a = 0; a < np.d; ++a) {
+            ui[a] = ut[a * nt + i];
+            const int c = (int)floor(ui[a]);
+            lo[a] = max(0, (c - np.R) / np.T);
+            hi[a] = min(np.tpa - 1, (c + np.R + 1) / np.T);
+        }
+        const double a2 = np.a * np.a;
+        double acc = 0.0;
+        for (int t0 = lo[0]; t0 <= hi[0]; ++t0)
+            for (int t1 = (np.d > 1 ? lo[1] : 0); t1 <= (np.d > 1 ? hi[1] : 0); ++t1)
+                for (int t2 = (np.d > 2 ? lo[2] : 0); t2 <= (np.d > 2 ? hi[2] : 0); ++t2) {
+                    int tile = t0;
+                    if (np.d > 1) tile = tile * np.tpa + t1;
+                    if (np.d > 2) tile = tile * np.tpa + t2;
+                    for (int j = tile_start[tile]; j < tile_start[tile + 1]; ++j) {
+                        double r2 = 0.0;
+                        for (int a = 0; a < np.d; ++a) {
+                            const double dx = (ui[a] - us[a * ns + j]) * np.inv_n;
+                            r2 += dx * dx;
+                        }
+                        if (r2 < a2) {
+                            const double r = sqrt(r2);
+                            const double k = exp(-np.lam_p * r);
+                            const double kk = np.kernel == 0 ? k : r * np.rho_inv * k;
+                            acc += w[j] * (kk - ki_poly(r, np.ki, np.ki_n, np.a));
+                        }
+                    }
+                }
+        t[i] += acc;
+    }
+}
+
+int launch_nearfield(Plan& P, int src, int dst, int kernel, const double* w_sorted, double* t_sorted,
+                     cudaStream_t s) {
+    const NodeSet& S = P.side[src];
+    const NodeSet& D = P.side[dst];
+    if (D.count <= 0 || S.count <= 0) return SK_OK;
+    NearParams np;
+    np.d = P.d;
+    np.n = P.n;
+    np.T = P.tile_cells;
+    np.tpa = P.tiles_per_axis;
+    np.R = P.near_cells;
+    np.ki_n = P.ki_n;
+    np.kernel = kernel;
+    np.a = P.near_a;
+    np.lam_p = P.lambda_p;
+    np.rho_inv = 1.0 / P.rho;
+    np.inv_n = 1.0 / P.n;
+    for (int i = 0; i < 16; ++i) np.ki[i] = P.ki[kernel][i];
+    nearfield_kernel<<<grid_for(D.count, 128), 128, 0, s>>>(np, D.u, D.count, S.u, S.count, S.tile_start,
+                                                            w_sorted, t_sorted);
     SK_LAUNCH_CHECK();
     return SK_OK;
 }

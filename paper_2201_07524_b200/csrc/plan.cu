@@ -46,6 +46,64 @@ static void radial_derivs(double a, double rho, int kernel, double r, int p, dou
     }
 }
 
+// r = 1 (NEXT-2): f(r) = P0(r) exp(-a r), P0 = 1 (kernel 0) or r / rho (kernel 1);
+// f^{(k)} = P_k exp(-a r) with P_{k+1} = P_k' - a P_k (P_k of degree <= 1).
+static void radial_derivs_r1(double a, double rho, int kernel, double r, int p, double* out) {
+    double c0 = kernel == 0 ? 1.0 : 0.0, c1 = kernel == 0 ? 0.0 : 1.0 / rho;   // P = c0 + c1 r
+    const double e = exp(-a * r);
+    for (int k = 0; k < p; ++k) {
+        out[k] = (c0 + c1 * r) * e;
+        const double n0 = c1 - a * c0, n1 = -a * c1;
+        c0 = n0;
+        c1 = n1;
+    }
+}
+
+static void radial_derivs_any(int rpow, double a, double rho, int kernel, double r, int p, double* out) {
+    if (rpow == 1) radial_derivs_r1(a, rho, kernel, r, p, out);
+    else radial_derivs(a, rho, kernel, r, p, out);
+}
+
+// Inner regularisation for r = 1 (NEXT-2): K_I(r) = sum_{i<p} c_i (r/a)^{2i} with
+// K_I^{(k)}(a) = K^{(k)}(a), k < p (even, so smooth at 0). Dense p x p solve with partial
+// pivoting on the host.
+static int ki_coefficients(double lam_p, double rho, int kernel, double a, int p, std::vector<double>& c) {
+    std::vector<double> dK(p), A(p * p, 0.0), rhs(p);
+    radial_derivs_r1(lam_p, rho, kernel, a, p, dK.data());
+    for (int k = 0; k < p; ++k) {
+        for (int i = 0; i < p; ++i) {
+            const int e = 2 * i;
+            if (e < k) continue;
+            double f = 1.0;
+            for (int q = e - k + 1; q <= e; ++q) f *= q;   // e! / (e - k)!
+            A[k * p + i] = f / pow(a, k);
+        }
+        rhs[k] = dK[k];
+    }
+    for (int col = 0; col < p; ++col) {
+        int piv = col;
+        for (int r = col + 1; r < p; ++r)
+            if (fabs(A[r * p + col]) > fabs(A[piv * p + col])) piv = r;
+        if (A[piv * p + col] == 0.0) return set_error(SK_EINVAL, "inner regularisation system is singular");
+        if (piv != col) {
+            for (int i = 0; i < p; ++i) std::swap(A[col * p + i], A[piv * p + i]);
+            std::swap(rhs[col], rhs[piv]);
+        }
+        for (int r = col + 1; r < p; ++r) {
+            const double f = A[r * p + col] / A[col * p + col];
+            for (int i = col; i < p; ++i) A[r * p + i] -= f * A[col * p + i];
+            rhs[r] -= f * rhs[col];
+        }
+    }
+    c.assign(p, 0.0);
+    for (int r = p - 1; r >= 0; --r) {
+        double v = rhs[r];
+        for (int i = r + 1; i < p; ++i) v -= A[r * p + i] * c[i];
+        c[r] = v / A[r * p + r];
+    }
+    return SK_OK;
+}
+
 static double binom(int n, int k) {
     double r = 1.0;
     for (int i = 1; i <= k; ++i) r = r * (n - k + i) / i;
@@ -58,11 +116,11 @@ static double binom(int n, int k) {
 // r = p - 1 at t = 0 (data F^{(k+1)}(0)) and t = 1 (zeros):
 //   s(t) = (1-t)^r sum_{k<r} sum_{j<r-k} C(r-1+j, j) s^{(k)}(0)/k! t^{k+j},
 // and K_B(t) = F(0) + int_0^t s.
-static void kb_coefficients(double lam_p, double rho, int kernel, double L, int p,
+static void kb_coefficients(int rpow, double lam_p, double rho, int kernel, double L, int p,
                             std::vector<double>& c) {
     const double D = 0.5 - L;
     std::vector<double> dK(p);
-    radial_derivs(lam_p, rho, kernel, L, p, dK.data());
+    radial_derivs_any(rpow, lam_p, rho, kernel, L, p, dK.data());
     std::vector<double> F(p);
     double Dk = 1.0;
     for (int k = 0; k < p; ++k) { F[k] = dK[k] * Dk; Dk *= D; }
@@ -427,7 +485,13 @@ static int plan_coefficients(Plan& P, cudaStream_t s) {
     SK_TRY(fft_acquire(P.d, M, CUFFT_D2Z, s, &h));
     for (int kernel = 0; kernel < 2; ++kernel) {
         std::vector<double> c;
-        kb_coefficients(P.lambda_p, P.rho, kernel, P.L, P.p_smooth, c);
+        kb_coefficients(P.rpow, P.lambda_p, P.rho, kernel, P.L, P.p_smooth, c);
+        if (P.rpow == 1) {
+            std::vector<double> ci;
+            SK_TRY(ki_coefficients(P.lambda_p, P.rho, kernel, P.near_a, P.p_smooth, ci));
+            for (int i = 0; i < (int)ci.size(); ++i) P.ki[kernel][i] = ci[i];
+            P.ki_n = (int)ci.size();
+        }
         SK_TRY(launch_sample_kernel(P, kernel, M, c.data(), (int)c.size() - 1, samp, s));
         SK_CUFFT(cufftExecD2Z(h, samp, B));
         count_launch();
@@ -441,8 +505,12 @@ static int plan_coefficients(Plan& P, cudaStream_t s) {
 }
 
 int build_plan(Ctx* ctx, Plan** out, int d, const double* x, long long n, const double* y,
-               long long m, double lambda, int N, double sigma, int m_w, double eps_B, int p) {
+               long long m, double lambda, int N, double sigma, int m_w, double eps_B, int p,
+               int rpow, int near_cells) {
     if (d < 1 || d > 3) return set_error(SK_EINVAL, "d must be 1, 2 or 3");
+    if (rpow != 1 && rpow != 2) return set_error(SK_EINVAL, "r must be 1 or 2");
+    if (rpow == 1 && (near_cells < 1 || p > 8))
+        return set_error(SK_EINVAL, "r = 1 needs near_cells >= 1 and p_smooth <= 8 (K_I monomial system)");
     if (N < 2 || (N & 1)) return set_error(SK_EINVAL, "N must be even and >= 2");
     if (!(lambda > 0.0) || !isfinite(lambda)) return set_error(SK_EINVAL, "lambda must be > 0");
     if (m_w < 2 || m_w > 8) return set_error(SK_EINVAL, "m_w must be in [2, 8]");
@@ -473,6 +541,13 @@ int build_plan(Ctx* ctx, Plan** out, int d, const double* x, long long n, const 
     P->eps_B = eps_B;
     P->p_smooth = p;
     P->L = 0.5 - eps_B;
+    P->rpow = rpow;
+    P->near_cells = rpow == 1 ? near_cells : 0;
+    P->near_a = rpow == 1 ? (double)near_cells / ng : 0.0;
+    if (rpow == 1 && !(P->near_a < P->L)) {
+        delete P;
+        return set_error(SK_EINVAL, "near-field radius near_cells / (sigma N) must be < 1/2 - eps_B");
+    }
     P->grid_size = 1;
     for (int a = 0; a < d; ++a) P->grid_size *= ng;
     P->spec_size = 1;
@@ -485,10 +560,11 @@ int build_plan(Ctx* ctx, Plan** out, int d, const double* x, long long n, const 
         WinPoly* wp = new WinPoly();
         const double err = build_winpoly(m_w, sigma, wp);
         P->winpoly = wp;
-        P->tiled = (d == 3) && (m_w == 6 || m_w == 8) && err >= 0.0 && err <= 1e-14 &&
+        // r = 1 runs the plain v1 spread / interp: its near field walks the source tiles
+        P->tiled = (d == 3) && (m_w == 6 || m_w == 8) && err >= 0.0 && err <= 1e-14 && rpow == 2 &&
                    getenv("SK_FORCE_V1") == nullptr;
         P->dmma = ((P->tiled && m_w == 6) || (d == 2 && m_w == 8 && err >= 0.0 && err <= 1e-14)) &&
-                  getenv("SK_NO_DMMA") == nullptr && getenv("SK_FORCE_V1") == nullptr;
+                  rpow == 2 && getenv("SK_NO_DMMA") == nullptr && getenv("SK_FORCE_V1") == nullptr;
         if (P->dmma && d == 2) P->tiled = false;
         // hybrid DMMA+DFMA spread (no padded rows): opt-in until it beats the padded kernel
         // (c5: 20.6 vs 15.5 ms under ncu, issue/latency-bound with 2 passes per segment)
@@ -529,7 +605,8 @@ int build_plan(Ctx* ctx, Plan** out, int d, const double* x, long long n, const 
         }
         const double diag = sqrt(diag2);
         P->rho = diag > 0.0 ? P->L / diag : 1.0;
-        P->lambda_p = lambda / (P->rho * P->rho);
+        // exp(-lam |x - y|^r) = exp(-lam' |x' - y'|^r) with x' = rho (x - centre)
+        P->lambda_p = rpow == 2 ? lambda / (P->rho * P->rho) : lambda / P->rho;
         // touched grid box: cells floor(u) - m + 1 .. floor(u) + m of every node, u = n(rho(x -
         // centre) + 1/2) over the global bbox, one cell of margin against rounding
         P->box_size = 1;
@@ -655,6 +732,7 @@ int apply_sorted(Plan& P, int transpose, int kernel, const double* w_sorted, dou
     prof_end(ST_FFT_INV, s);
     prof_begin(ST_INTERP, s);
     SK_TRY(launch_interp(P, dst, P.grid, t_sorted, s));
+    if (P.rpow == 1) SK_TRY(launch_nearfield(P, src, dst, kernel, w_sorted, t_sorted, s));
     prof_end(ST_INTERP, s);
     return SK_OK;
 }

@@ -85,6 +85,13 @@ struct Plan {
     double sigma = 2.0;
     Window win{};
     double lambda = 0, lambda_p = 0, rho = 1, L = 0, eps_B = 0;
+    int rpow = 2;             // cost |x - y|^r, r in {1, 2}
+    // r = 1 (NEXT-2): inner regularisation K_I on |x'| <= near_a (torus units) and the
+    // near-field correction sum over |x'_i - y'_j| < near_a of w_j (K - K_I)
+    int near_cells = 0;
+    double near_a = 0.0;
+    double ki[2][16] = {};    // K_I coefficients in (r / near_a)^2, kernels 0 and 1
+    int ki_n = 0;
     int p_smooth = 8;
     double centre[kMaxD] = {0, 0, 0};
     long long grid_size = 0;  // n^d
@@ -158,7 +165,10 @@ int launch_finalize_partials(const double* red, int nparts, int nvals, double* o
 
 // ---- plan.cu ----
 int build_plan(Ctx* ctx, Plan** out, int d, const double* x, long long n, const double* y,
-               long long m, double lambda, int N, double sigma, int m_w, double eps_B, int p);
+               long long m, double lambda, int N, double sigma, int m_w, double eps_B, int p,
+               int rpow, int near_cells);
+int launch_nearfield(Plan& P, int src, int dst, int kernel, const double* w_sorted, double* t_sorted,
+                     cudaStream_t s);
 int destroy_plan(Plan* P);
 void fft_pool_release();   // destroy the pooled cuFFT handles (sk_release_cache)
 int apply_sorted(Plan& P, int transpose, int kernel, const double* w_sorted, double* t_sorted);

@@ -432,3 +432,46 @@ def test_emulated_two_rank_world(capi):
     for P, c in ((P1, c1), (P2, c2)):
         P.close()
         c.close()
+
+
+# ------------------------------------------------------------------ NEXT-2: r = 1 (Laplace kernel + near field)
+@pytest.mark.parametrize("d,n,N", [(1, 300, 128), (2, 150, 128)])
+def test_r1_fastsum_matches_oracle(capi, ctx, d, n, N):
+    """fastsum_plan_ex with r = 1: the GPU fast summation equals the oracle's statement of the
+    same method (laplace_ref.fastsum_ndft: exact NDFTs of K_R's b_k plus the brute-force near
+    field) to the window error, and the direct sum to the method error (both kernels, both
+    directions)."""
+    from oracle import laplace_ref as LR
+    rng = np.random.default_rng(10 + d)
+    x, y = rng.random((n, d)), rng.random((n + 7, d))
+    wy, wx = rng.random(n + 7), rng.random(n)
+    lam = 20.0
+    P = capi.Plan(ctx, dev(x), dev(y), lam, N, 2.0, 8, 1 / 16, 8, r=1, near_cells=16)
+    for kernel in (0, 1):
+        t = capi.fastsum_apply(P, dev(wy), 0, kernel).cpu().numpy()
+        tt = capi.fastsum_apply(P, dev(wx), 1, kernel).cpu().numpy()
+        m_ref = LR.fastsum_ndft(x, y, wy, lam, N, 1 / 16, 8, 16, kernel=kernel)
+        mt_ref = LR.fastsum_ndft(y, x, wx, lam, N, 1 / 16, 8, 16, kernel=kernel)
+        assert rel_linf(t, m_ref) <= 1e-12 and rel_linf(tt, mt_ref) <= 1e-12, (kernel, rel_linf(t, m_ref))
+        ref = dense.direct_sum(x, y, wy, lam, kernel, r=1)
+        reft = dense.direct_sum(y, x, wx, lam, kernel, r=1)
+        tol = 5e-8 if d == 1 else 5e-7
+        assert rel_linf(t, ref) <= tol and rel_linf(tt, reft) <= tol, (kernel, rel_linf(t, ref), rel_linf(tt, reft))
+
+
+def test_r1_divergence_and_w1_sandwich(capi, ctx):
+    """Alg. 2 with r = 1 on the c1 inputs (d = 1, n = m = 1000, lam = 20): s~ and s match the
+    dense oracle within SPEC's r = 1 gate (1e-6) and s <= W_1 <= s~ with the exact 1-D W_1."""
+    from oracle import exact_ot
+    cfg = get("c1")
+    x, y, a, b = make_inputs(cfg)
+    lam, iters, N = 20.0, 200, 256
+    ref, _, _ = dense.sinkhorn_divergence(x, y, a, b, lam, iters, r=1)
+    P = capi.Plan(ctx, dev(x), dev(y), lam, N, 2.0, 8, 1 / 16, 8, r=1, near_cells=16)
+    da, db = dev(a), dev(b)
+    u, v, info = capi.sinkhorn_run(P, da, db, iters)
+    sd, sc = capi.sinkhorn_divergence(P, da, db, u, v)
+    assert abs(sc - ref["s_cost"]) <= 1e-6 * abs(ref["s_cost"]), (sc, ref)
+    assert abs(sd - ref["s_dual"]) <= 1e-6 * abs(ref["s_dual"]), (sd, ref)
+    W = exact_ot.w1_1d(x[:, 0], a, y[:, 0], b)
+    assert sd <= W <= sc
