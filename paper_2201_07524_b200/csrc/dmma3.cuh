@@ -107,9 +107,21 @@ taps_precompute_kernel(const double* __restrict__ u, long long count, const __gr
 struct InterpDCfg {
     static constexpr int W = 12, KS = W / 4, NT = 128, NWARP = NT / 32, TS = 3 * W;
     static constexpr int XS = W + 2;                          // phi_x row stride (doubles)
-    static constexpr size_t SMEM_BYTES = sizeof(double) * NWARP * 32 * XS;
+    static constexpr int GBLK = W * W * W;                    // the cell's 12^3 grid block
+    static constexpr size_t SMEM_BYTES = sizeof(double) * NWARP * (32 * XS + GBLK);   // STAGE
+    static constexpr size_t SMEM_BYTES_NOSTAGE = sizeof(double) * NWARP * 32 * XS;     // more L1
 };
 
+__device__ __forceinline__ void cp_async8(void* smem_dst, const void* gmem_src) {
+    const unsigned sa = (unsigned)__cvta_generic_to_shared(smem_dst);
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(sa), "l"(gmem_src));
+}
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+
+// STAGE: copy each cell's 12^3 grid block to shared memory once and read the A fragments from
+// there (pays when cells hold several batches: c5 interp 16.1 -> 14.2 ms); otherwise read them
+// through L1 straight from the grid.
+template <bool STAGE>
 __global__ void __launch_bounds__(128, SK_INTERP3_MINB)
 interp3_dmma_kernel(const CellBatch* __restrict__ batches, int nbatches, const double* __restrict__ taps,
                     const double* __restrict__ grid, int n, double* __restrict__ t_out) {
@@ -120,7 +132,9 @@ interp3_dmma_kernel(const CellBatch* __restrict__ batches, int nbatches, const d
     const long long n2 = (long long)n * n;
     const int gw = blockIdx.x * C::NWARP + warp, nw = gridDim.x * C::NWARP;
     extern __shared__ __align__(16) double smem[];
-    double* XT = smem + warp * 32 * C::XS;        // [node][XS] phi_x rows of the current batch
+    double* XT = smem + warp * (STAGE ? 32 * C::XS + C::GBLK : 32 * C::XS);   // [node][XS] phi_x rows
+    double* GB = XT + 32 * C::XS;                          // [tx][ty][tz] grid block of the cell
+    int cur_cell = -1;
     // contiguous slice of the cell-sorted batch list per warp: consecutive batches of one
     // cell reuse its 12^3 grid block from L1, and the taps stream sequentially
     const int per = (nbatches + nw - 1) / nw;
@@ -133,6 +147,18 @@ interp3_dmma_kernel(const CellBatch* __restrict__ batches, int nbatches, const d
         const int cz = B.cell % n, cy = (B.cell / n) % n, cx = B.cell / n / n;
         const double* T0 = taps + (long long)B.start * TS;
         const int last = B.count - 1;
+        // a new cell: copy its 12^3 grid block to shared memory (async, overlapped with the
+        // batch's tap loads below); the following batches of the cell read it from there
+        const bool new_cell = STAGE && B.cell != cur_cell;
+        if (new_cell) {
+            __syncwarp();
+            const double* Gb = grid + (long long)(cx - m + 1) * n2 + (long long)(cy - m + 1) * n + (cz - m + 1);
+            for (int i = lane; i < C::GBLK; i += 32) {
+                const int r = i / W, c = i % W;
+                cp_async8(GB + i, Gb + (long long)(r / W) * n2 + (long long)(r % W) * n + c);
+            }
+            cur_cell = B.cell;
+        }
         if (bi + 1 < b_hi)   // next batch of this warp: stream its taps into L2
             prefetch_range(taps + (long long)Bnext.start * TS, (long long)Bnext.count * TS * 8, lane);
         // B fragments: phi_z of node 8 nt + g at tz = 4 s + q
@@ -170,8 +196,13 @@ interp3_dmma_kernel(const CellBatch* __restrict__ batches, int nbatches, const d
         double acc[4][2];
 #pragma unroll
         for (int nt = 0; nt < 4; ++nt) acc[nt][0] = acc[nt][1] = 0.0;
-        const double* Hb = grid + (long long)(cx - m + 1) * n2 + (long long)(cy - m + 1) * n + (cz - m + 1) + q;
-        const long long ry[3] = {(long long)g * n, (long long)ty1 * n, (long long)(4 + g) * n};
+        if (new_cell) cp_async_wait_all();
+        __syncwarp();
+        const double* Hb = STAGE ? GB + q
+                                 : grid + (long long)(cx - m + 1) * n2 + (long long)(cy - m + 1) * n + (cz - m + 1) + q;
+        const long long sxs = STAGE ? W * W : n2;
+        const long long ry[3] = {STAGE ? g * W : (long long)g * n, STAGE ? ty1 * W : (long long)ty1 * n,
+                                 STAGE ? (4 + g) * W : (long long)(4 + g) * n};
 #pragma unroll 1
         for (int k = 0; k < W / 2; ++k) {
             // three m-tiles (one period of ty) per step, their DMMAs interleaved s-major so
@@ -183,9 +214,9 @@ interp3_dmma_kernel(const CellBatch* __restrict__ batches, int nbatches, const d
             double a[3][KS];
 #pragma unroll
             for (int r3 = 0; r3 < 3; ++r3) {
-                const double* Hrow = Hb + (long long)txr[r3] * n2 + ry[r3];
+                const double* Hrow = Hb + txr[r3] * sxs + ry[r3];
 #pragma unroll
-                for (int s = 0; s < KS; ++s) a[r3][s] = __ldg(Hrow + 4 * s);
+                for (int s = 0; s < KS; ++s) a[r3][s] = STAGE ? Hrow[4 * s] : __ldg(Hrow + 4 * s);
             }
             double d[3][4][2];
 #pragma unroll

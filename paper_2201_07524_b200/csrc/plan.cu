@@ -364,6 +364,7 @@ static int build_cell_lists(Plan& P, NodeSet& S, cudaStream_t s) {
     SK_CUDA(cudaStreamSynchronize(s));
     last[0] = h[4] + h[7]; last[1] = h[5] + h[8]; last[2] = h[6] + h[9];
     S.nbatches = last[0];
+    S.ncells = nruns;
     S.nsegs = last[1];
     S.nsitems = last[2];
     SK_TRY(alloc(&S.batches, sizeof(CellBatch) * std::max(S.nbatches, 1)));

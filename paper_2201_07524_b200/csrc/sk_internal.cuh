@@ -61,6 +61,7 @@ struct NodeSet {
     // DMMA path (d = 3, W = 12): per-cell work lists
     void* batches = nullptr;     // CellBatch[nbatches]: <= 32 nodes of one cell (interp)
     int nbatches = 0;
+    int ncells = 0;              // non-empty cells
     void* segs = nullptr;        // CellBatch[nsegs]: <= kSegMax nodes of one cell (spread)
     int nsegs = 0;
     void* sitems = nullptr;      // SpreadItem[nsitems]: segments of one 2^3 super-tile (spread)

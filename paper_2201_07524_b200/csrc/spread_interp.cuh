@@ -236,12 +236,17 @@ inline int interp_dispatch(Plan& P, const NodeSet& S, const double* grid, double
         using C = InterpDCfg;
         static bool attr = false;
         if (!attr) {
-            cudaFuncSetAttribute(interp3_dmma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM_BYTES);
+            cudaFuncSetAttribute(interp3_dmma_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM_BYTES);
+            cudaFuncSetAttribute(interp3_dmma_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM_BYTES);
             attr = true;
         }
         if (S.nbatches > 0) {
-            const int g = persistent_grid(interp3_dmma_kernel, C::NT, C::SMEM_BYTES, (S.nbatches + C::NWARP - 1) / C::NWARP);
-            interp3_dmma_kernel<<<g, C::NT, C::SMEM_BYTES, s>>>((const CellBatch*)S.batches, S.nbatches, S.taps, grid, P.n, t);
+            // stage grid blocks when cells average >= 1.5 batches (32 nodes each)
+            const bool stage = 2LL * S.nbatches >= 3LL * S.ncells;
+            const auto kern = stage ? interp3_dmma_kernel<true> : interp3_dmma_kernel<false>;
+            const size_t sm = stage ? C::SMEM_BYTES : C::SMEM_BYTES_NOSTAGE;
+            const int g = persistent_grid(kern, C::NT, sm, (S.nbatches + C::NWARP - 1) / C::NWARP);
+            kern<<<g, C::NT, sm, s>>>((const CellBatch*)S.batches, S.nbatches, S.taps, grid, P.n, t);
             count_launch();
         }
         cudaError_t e = cudaGetLastError();
