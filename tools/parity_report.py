@@ -67,8 +67,9 @@ def main():
         del x, y, a, b
         # divergence on the oracle-sized subsample
         k = min(args.k, cfg.n, cfg.m)
-        xs, ys, as_, bs = make_inputs(cfg.with_(n=min(cfg.n, 4 * k), m=min(cfg.m, 4 * k))) if name != "c4" else (None,) * 4
-        if name == "c4":
+        grid_like = cfg.x_dist in ("jitter_grid", "pixel_grid")
+        xs, ys, as_, bs = make_inputs(cfg.with_(n=min(cfg.n, 4 * k), m=min(cfg.m, 4 * k))) if not grid_like else (None,) * 4
+        if grid_like:
             # c4 is a jittered grid: take every (K/k')-th row and column block of the full grid
             x, y, a, b = make_inputs(cfg)
             idx = np.random.default_rng(0).choice(x.shape[0], size=k, replace=False)
