@@ -150,17 +150,20 @@ static void kb_coefficients(int rpow, double lam_p, double rho, int kernel, doub
 // owned by one plan at a time, so distinct live plans never share one.
 struct FftKey {
     int device, d, n, type;
+    long long batch;
     bool operator<(const FftKey& o) const {
-        return std::tie(device, d, n, type) < std::tie(o.device, o.d, o.n, o.type);
+        return std::tie(device, d, n, type, batch) < std::tie(o.device, o.d, o.n, o.type, o.batch);
     }
 };
 static std::mutex g_fft_mu;
 static std::multimap<FftKey, cufftHandle> g_fft_pool;
 
-static int fft_acquire(int d, int n, cufftType type, cudaStream_t s, cufftHandle* out) {
+// d-dimensional n^d transform; batch > 1: `batch` contiguous transforms (rank d, default
+// strides) -- the 1-D batched transforms of the pruned FFT use d = 1.
+int fft_acquire(int d, int n, cufftType type, cudaStream_t s, cufftHandle* out, long long batch) {
     int dev = 0;
     cudaGetDevice(&dev);
-    const FftKey k{dev, d, n, (int)type};
+    const FftKey k{dev, d, n, (int)type, batch};
     {
         std::lock_guard<std::mutex> g(g_fft_mu);
         auto it = g_fft_pool.find(k);
@@ -172,17 +175,17 @@ static int fft_acquire(int d, int n, cufftType type, cudaStream_t s, cufftHandle
         }
     }
     int dims[3] = {n, n, n};
-    SK_CUFFT(cufftPlanMany(out, d, dims, nullptr, 1, 0, nullptr, 1, 0, type, 1));
+    SK_CUFFT(cufftPlanMany(out, d, dims, nullptr, 1, 0, nullptr, 1, 0, type, (int)batch));
     SK_CUFFT(cufftSetStream(*out, s));
     return SK_OK;
 }
 
-static void fft_release(int d, int n, cufftType type, cufftHandle h) {
+void fft_release(int d, int n, cufftType type, cufftHandle h, long long batch) {
     if (!h) return;
     int dev = 0;
     cudaGetDevice(&dev);
     std::lock_guard<std::mutex> g(g_fft_mu);
-    g_fft_pool.emplace(FftKey{dev, d, n, (int)type}, h);
+    g_fft_pool.emplace(FftKey{dev, d, n, (int)type, batch}, h);
 }
 
 void fft_pool_release() {
@@ -656,6 +659,7 @@ int build_plan(Ctx* ctx, Plan** out, int d, const double* x, long long n, const 
         if ((st = fft_acquire(d, ng, CUFFT_D2Z, s, &P->fwd))) return fail(st);
         if ((st = fft_acquire(d, ng, CUFFT_Z2D, s, &P->inv))) return fail(st);
     }
+    if ((st = pruned_fft_setup(*P, s))) return fail(st);
     plan_trace("fft plans", s);
     // ---- scratch
     P->max_count = std::max(n, m);
@@ -691,6 +695,7 @@ int destroy_plan(Plan* P) {
     for (int k = 0; k < 2; ++k) { sk_free(P->D[k]); sk_free(P->bk[k]); }
     fft_release(P->d, P->n, CUFFT_D2Z, P->fwd);
     fft_release(P->d, P->n, CUFFT_Z2D, P->inv);
+    pruned_fft_teardown(*P, P->ctx->stream);
     if (P->cap_stream) cudaStreamDestroy(P->cap_stream);
     sk_free(P->w_sorted); sk_free(P->t_sorted);
     sk_free(P->a_s); sk_free(P->b_s); sk_free(P->u_s); sk_free(P->v_s);
@@ -720,17 +725,21 @@ int apply_sorted(Plan& P, int transpose, int kernel, const double* w_sorted, dou
         SK_TRY(launch_box_copy(P, P.grid, P.box_buf, 1, s));
         prof_end(ST_ALLREDUCE, s);
     }
-    prof_begin(ST_FFT_FWD, s);
-    SK_CUFFT(cufftExecD2Z(P.fwd, P.grid, P.spec));
-    count_launch();
-    prof_end(ST_FFT_FWD, s);
-    prof_begin(ST_MULTIPLY, s);
-    SK_TRY(launch_multiply(P, kernel, s));
-    prof_end(ST_MULTIPLY, s);
-    prof_begin(ST_FFT_INV, s);
-    SK_CUFFT(cufftExecZ2D(P.inv, P.spec, P.grid));
-    count_launch();
-    prof_end(ST_FFT_INV, s);
+    if (P.pruned) {
+        SK_TRY(pruned_fft_apply(P, kernel, s));
+    } else {
+        prof_begin(ST_FFT_FWD, s);
+        SK_CUFFT(cufftExecD2Z(P.fwd, P.grid, P.spec));
+        count_launch();
+        prof_end(ST_FFT_FWD, s);
+        prof_begin(ST_MULTIPLY, s);
+        SK_TRY(launch_multiply(P, kernel, s));
+        prof_end(ST_MULTIPLY, s);
+        prof_begin(ST_FFT_INV, s);
+        SK_CUFFT(cufftExecZ2D(P.inv, P.spec, P.grid));
+        count_launch();
+        prof_end(ST_FFT_INV, s);
+    }
     prof_begin(ST_INTERP, s);
     SK_TRY(launch_interp(P, dst, P.grid, t_sorted, s));
     if (P.rpow == 1) SK_TRY(launch_nearfield(P, src, dst, kernel, w_sorted, t_sorted, s));

@@ -105,6 +105,12 @@ struct Plan {
     double* bk[2] = {nullptr, nullptr}; // b_k on the full band (N+1)^d (diagnostics)
     cufftHandle fwd = 0, inv = 0;
     cudaStream_t cap_stream = nullptr;  // private stream for CUDA-graph capture of iterations
+    // NEXT-4 pruned FFT (d = 3, pruned_fft.cu): batched 1-D transforms over box rows / band rows
+    bool pruned = false;
+    long long pr_rows_z = 0, pr_rows_y = 0, pr_rows_x = 0;
+    double* pr_A = nullptr;
+    void *pr_Z = nullptr, *pr_Y = nullptr, *pr_X = nullptr;   // cufftDoubleComplex buffers
+    cufftHandle pr_fz = 0, pr_iz = 0, pr_y = 0, pr_x = 0;
     // scratch
     double* w_sorted = nullptr;   // [max count]
     double* t_sorted = nullptr;   // [max count]
@@ -172,6 +178,12 @@ int launch_nearfield(Plan& P, int src, int dst, int kernel, const double* w_sort
                      cudaStream_t s);
 int destroy_plan(Plan* P);
 void fft_pool_release();   // destroy the pooled cuFFT handles (sk_release_cache)
+// ---- pruned_fft.cu (NEXT-4) ----
+int pruned_fft_setup(Plan& P, cudaStream_t s);      // sets P.pruned when the box pays
+void pruned_fft_teardown(Plan& P, cudaStream_t s);
+int pruned_fft_apply(Plan& P, int kernel, cudaStream_t s);   // a4 + a5 + a6 on P.grid in place
+int fft_acquire(int d, int n, cufftType type, cudaStream_t s, cufftHandle* out, long long batch = 1);
+void fft_release(int d, int n, cufftType type, cufftHandle h, long long batch = 1);
 int apply_sorted(Plan& P, int transpose, int kernel, const double* w_sorted, double* t_sorted);
 
 // ---- stage profiling (api.cu): CUDA-event pairs around each stage when enabled ----

@@ -117,6 +117,19 @@ def test_matvec_parity_full_size(capi, ctx, name, n_rows):
     assert not bad, worst
 
 
+def test_matvec_parity_c5_full_size(capi, ctx):
+    """c5 at full size (1e8 + 8e7 nodes, the bench's plan): both directions and both kernels on
+    256 seeded rows per direction against the direct sum over all sources (the 4096-row run is
+    tools/parity_report.py --rows 4096, profiles/)."""
+    cfg = get("c5")
+    x, y, a, b = make_inputs(cfg)
+    ci = CONFIG_INDEX["c5"]
+    rx = check_rows(ci, 256, x.shape[0])
+    ry = check_rows(ci, 256, y.shape[0], seed=1)
+    worst = _matvec_case(capi, ctx, cfg, x, y, a, b, rx, ry, {"marginal": (b, a)})
+    assert max(max(v) for v in worst.values()) <= 1e-9, worst
+
+
 def test_matvec_parity_c1_converged_weights(capi, ctx):
     """Weights (iii): the oracle's converged scalings v = exp(lam g), u = exp(lam f).
     At BJ's N = 64 the K v direction meets 1e-9 but K^T u does not: u spans e^{lam range(f)}
@@ -475,3 +488,24 @@ def test_r1_divergence_and_w1_sandwich(capi, ctx):
     assert abs(sd - ref["s_dual"]) <= 1e-6 * abs(ref["s_dual"]), (sd, ref)
     W = exact_ot.w1_1d(x[:, 0], a, y[:, 0], b)
     assert sd <= W <= sc
+
+
+@pytest.mark.parametrize("name,n,m", [("c3", 200000, 200000), ("c5", 400000, 320000)])
+def test_pruned_fft_equals_full_fft(capi, ctx, name, n, m):
+    """NEXT-4: the box/band-pruned a4-a6 stages (batched 1-D transforms over the rows that can be
+    nonzero or are read) equal the full n^3 cuFFT path: a multi-dimensional DFT is the product of
+    its 1-D DFTs, and the skipped rows are zero in (outside the box) or discarded (outside the
+    band / box)."""
+    cfg = get(name)
+    x, y, a, b = make_inputs(cfg.with_(n=n, m=m))
+    P1 = capi.Plan(ctx, dev(x), dev(y), cfg.lam, cfg.N, cfg.sigma, cfg.m_w, cfg.eps_B, cfg.p)
+    os.environ["SK_NO_PRUNED_FFT"] = "1"
+    try:
+        P0 = capi.Plan(ctx, dev(x), dev(y), cfg.lam, cfg.N, cfg.sigma, cfg.m_w, cfg.eps_B, cfg.p)
+    finally:
+        del os.environ["SK_NO_PRUNED_FFT"]
+    for tr, w in ((0, b), (1, a)):
+        for kernel in (0, 1):
+            t1 = capi.fastsum_apply(P1, dev(w), tr, kernel).cpu().numpy()
+            t0 = capi.fastsum_apply(P0, dev(w), tr, kernel).cpu().numpy()
+            assert rel_linf(t1, t0) <= 1e-13, (tr, kernel, rel_linf(t1, t0))
