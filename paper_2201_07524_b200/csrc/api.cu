@@ -495,8 +495,7 @@ static int run_impl(sk_plan_t plan, const double* a, const double* b, int iters,
         auto use_stream = [&](cudaStream_t t) {
             s = t;
             C->stream = t;
-            cufftSetStream(P.fwd, t);
-            cufftSetStream(P.inv, t);
+            plan_set_stream(P, t);   // every cuFFT handle of the plan (full and pruned)
         };
         use_stream(P.cap_stream);
         cudaError_t ce = cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal);

@@ -683,6 +683,11 @@ int build_plan(Ctx* ctx, Plan** out, int d, const double* x, long long n, const 
     return SK_OK;
 }
 
+void plan_set_stream(Plan& P, cudaStream_t s) {
+    for (cufftHandle h : {P.fwd, P.inv, P.pr_fz, P.pr_iz, P.pr_y, P.pr_x})
+        if (h) cufftSetStream(h, s);
+}
+
 int destroy_plan(Plan* P) {
     if (!P) return SK_OK;
     tls_stream = P->ctx->stream;

@@ -177,6 +177,7 @@ int build_plan(Ctx* ctx, Plan** out, int d, const double* x, long long n, const 
 int launch_nearfield(Plan& P, int src, int dst, int kernel, const double* w_sorted, double* t_sorted,
                      cudaStream_t s);
 int destroy_plan(Plan* P);
+void plan_set_stream(Plan& P, cudaStream_t s);   // cufftSetStream on all of the plan's handles
 void fft_pool_release();   // destroy the pooled cuFFT handles (sk_release_cache)
 // ---- pruned_fft.cu (NEXT-4) ----
 int pruned_fft_setup(Plan& P, cudaStream_t s);      // sets P.pruned when the box pays
