@@ -16,8 +16,11 @@ Contents (each function cites the passage it follows; P:Lx = PAPER.md line x):
   nfft_ref.py  geometry reading, Kaiser-Bessel window, NDFT, kernel Fourier
                coefficients b_k, regularised kernel K~ with two-point Taylor K_B,
                gridding/interpolation definitions, NDFT fast summation
-  exact_ot.py  exact LP optimal transport (brute force / linprog), 1-D W2 closed form
+  exact_ot.py  exact LP optimal transport (brute force / linprog), 1-D W2 and W1 closed forms
   measures.py  entropy, KL divergence
+  diagnostics.py  per-iteration residual / KL / objective trace of Alg. 1 (NEXT-3)
+  laplace_ref.py  r = 1 fast summation: inner regularisation K_I, regularised kernel, NDFT far
+               field + brute-force near field (NEXT-2)
 
 Parity status: every function is pinned by a ``-m "not gpu"`` test in
 ``tests/test_oracle_pins.py``; none is
