@@ -509,3 +509,35 @@ def test_pruned_fft_equals_full_fft(capi, ctx, name, n, m):
             t1 = capi.fastsum_apply(P1, dev(w), tr, kernel).cpu().numpy()
             t0 = capi.fastsum_apply(P0, dev(w), tr, kernel).cpu().numpy()
             assert rel_linf(t1, t0) <= 1e-13, (tr, kernel, rel_linf(t1, t0))
+
+
+# ------------------------------------------------------------------ degenerate and empty inputs
+@pytest.mark.parametrize("d", [1, 2, 3])
+def test_degenerate_coincident_points(capi, ctx, d):
+    """All atoms of both measures at one point (bbox diagonal 0, the rho = 1 branch): K = 1, so
+    pi = a b^T after one iteration, s~ = 0 and s = -(H(a) + H(b)) / lam (Eq. (14) with
+    log u_i + log v_j = log a_i + log b_j and unit mass)."""
+    rng = np.random.default_rng(d)
+    n, m, lam = 37, 29, 7.0
+    x, y = np.full((n, d), 0.3), np.full((m, d), 0.3)
+    a, b = rng.random(n), rng.random(m)
+    a, b = a / a.sum(), b / b.sum()
+    m_w = 6 if d == 3 else 8
+    P = capi.Plan(ctx, dev(x), dev(y), lam, 32, 2.0, m_w)
+    u, v, info = capi.sinkhorn_run(P, dev(a), dev(b), 5)
+    sd, sc = capi.sinkhorn_divergence(P, dev(a), dev(b), u, v)
+    H = -(a * np.log(a)).sum() - (b * np.log(b)).sum()
+    assert abs(sc) <= 1e-15
+    assert abs(sd + H / lam) <= 1e-12 * H / lam
+
+
+def test_empty_measure_is_rejected(capi, ctx):
+    """A measure with no atoms at all (every rank empty) has no geometry: SK_EGEOMETRY; a side
+    empty while the other is not is a valid plan whose matvec into it is empty."""
+    x = np.random.default_rng(0).random((10, 2))
+    with pytest.raises(capi.SkError) as e:
+        capi.Plan(ctx, dev(np.zeros((0, 2))), dev(np.zeros((0, 2))), 10.0, 32)
+    assert e.value.code == capi.SK_EGEOMETRY
+    P = capi.Plan(ctx, dev(x), dev(np.zeros((0, 2))), 10.0, 32)
+    t = capi.fastsum_apply(P, dev(np.zeros(0)), 0, 0).cpu().numpy()
+    assert t.shape == (10,) and np.all(t == 0.0)
