@@ -109,12 +109,12 @@ int launch_bbox(const double* pts, long long count, int d, double* out_minmax, c
     int g = grid_for(count, kRedBlock);
     if (g > 1024) g = 1024;
     double* part = nullptr;
-    SK_CUDA(cudaMallocAsync(&part, sizeof(double) * 2 * d * g, s));
+    SK_TRY(dev_alloc((void**)&part, sizeof(double) * 2 * d * g, s));
     bbox_kernel<<<g, kRedBlock, 0, s>>>(pts, count, d, part);
     SK_LAUNCH_CHECK();
     bbox_final<<<1, kRedBlock, 0, s>>>(part, g, d, out_minmax);
     SK_LAUNCH_CHECK();
-    SK_CUDA(cudaFreeAsync(part, s));
+    dev_free(part, s);
     return SK_OK;
 }
 

@@ -194,6 +194,32 @@ void fft_pool_release() {
     g_fft_pool.clear();
 }
 
+// ---------------------------------------------------------------- pinned scalar buffers
+// Every plan needs 64 pinned doubles for its host-read scalars; cudaMallocHost costs ~ms, so
+// freed buffers are pooled (plans are created per solve).
+static std::mutex g_pin_mu;
+static std::vector<double*> g_pin_pool;
+
+static int pinned_acquire(double** out) {
+    {
+        std::lock_guard<std::mutex> g(g_pin_mu);
+        if (!g_pin_pool.empty()) {
+            *out = g_pin_pool.back();
+            g_pin_pool.pop_back();
+            return SK_OK;
+        }
+    }
+    if (cudaMallocHost((void**)out, sizeof(double) * 64) != cudaSuccess)
+        return set_error(SK_ENOMEM, "cudaMallocHost");
+    return SK_OK;
+}
+
+static void pinned_release(double* p) {
+    if (!p) return;
+    std::lock_guard<std::mutex> g(g_pin_mu);
+    g_pin_pool.push_back(p);
+}
+
 // ---------------------------------------------------------------- plan
 // All plan memory goes through the caching allocator, ordered on the plan's stream.
 static thread_local cudaStream_t tls_stream = nullptr;
@@ -676,8 +702,7 @@ int build_plan(Ctx* ctx, Plan** out, int d, const double* x, long long n, const 
     if ((st = alloc((void**)&P->red, sizeof(double) * 4096))) return fail(st);
     if ((st = alloc((void**)&P->red_out, sizeof(double) * 8192))) return fail(st);
     if ((st = alloc((void**)&P->flag, sizeof(int) * 8))) return fail(st);
-    if (cudaMallocHost((void**)&P->host_red, sizeof(double) * 64) != cudaSuccess)
-        return fail(set_error(SK_ENOMEM, "cudaMallocHost"));
+    if ((st = pinned_acquire(&P->host_red))) return fail(st);
     plan_trace("scratch", s);
     *out = P;
     return SK_OK;
@@ -705,7 +730,7 @@ int destroy_plan(Plan* P) {
     sk_free(P->w_sorted); sk_free(P->t_sorted);
     sk_free(P->a_s); sk_free(P->b_s); sk_free(P->u_s); sk_free(P->v_s);
     sk_free(P->red); sk_free(P->red_out); sk_free(P->flag); sk_free(P->box_buf);
-    if (P->host_red) cudaFreeHost(P->host_red);
+    pinned_release(P->host_red);
     delete (WinPoly*)P->winpoly;
     delete P;
     return SK_OK;
