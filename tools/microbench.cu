@@ -287,6 +287,70 @@ __global__ void __launch_bounds__(128, NT == 18 ? 2 : 4) hybrid_kernel(double* o
     out[blockIdx.x * blockDim.x + threadIdx.x] = s;
 }
 
+// the spread mix with m16n8k4: one DMMA covers both m-tiles (rows g, 8+g) with one B operand
+template <bool WITH_DMUL>
+__global__ void __launch_bounds__(128, 2) spreadmix16_kernel(double* out, int iters) {
+    double acc[18][4];
+#pragma unroll
+    for (int j = 0; j < 18; ++j) acc[j][0] = acc[j][1] = acc[j][2] = acc[j][3] = 0.0;
+    double y = 1.0 + threadIdx.x * 1e-6, z = 1.0 - threadIdx.x * 1e-6, a0 = 1e-3, a1 = 2e-3;
+    for (int it = 0; it < iters; ++it) {
+#pragma unroll
+        for (int j = 0; j < 18; ++j) {
+            const double b = WITH_DMUL ? y * (z + j) : y;
+            asm("mma.sync.aligned.m16n8k4.row.col.f64.f64.f64.f64 {%0,%1,%2,%3}, {%4,%5}, {%6}, {%0,%1,%2,%3};"
+                : "+d"(acc[j][0]), "+d"(acc[j][1]), "+d"(acc[j][2]), "+d"(acc[j][3]) : "d"(a0), "d"(a1), "d"(b));
+        }
+        y *= 0.9999999;
+    }
+    double s = 0;
+#pragma unroll
+    for (int j = 0; j < 18; ++j) s += acc[j][0] + acc[j][1] + acc[j][2] + acc[j][3];
+    out[blockIdx.x * blockDim.x + threadIdx.x] = s;
+}
+
+// spread mix with the 18 products grouped in one asm block ahead of the 36 DMMAs: does grouping
+// the FP64 vector ops (fewer DMMA <-> DMUL transitions on the shared pipe) lower their cost?
+__global__ void __launch_bounds__(128, 2) spreadmix_grouped_kernel(double* out, int iters) {
+    double acc[2][18][2];
+#pragma unroll
+    for (int i = 0; i < 2; ++i)
+#pragma unroll
+        for (int j = 0; j < 18; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+    double y = 1.0 + threadIdx.x * 1e-6, a0 = 1e-3, a1 = 2e-3;
+    double zz[18];
+#pragma unroll
+    for (int j = 0; j < 18; ++j) zz[j] = 1.0 - threadIdx.x * 1e-6 + j;
+#pragma unroll 1
+    for (int it = 0; it < iters; ++it) {
+        // 18 products as a dependent chain (b_j = b_{j-1} c + z_j, one DFMA each) so that the
+        // token below depends on all of them
+        double b[18];
+        b[0] = fma(y, zz[17], zz[0]);
+#pragma unroll
+        for (int j = 1; j < 18; ++j) b[j] = fma(b[j - 1], y, zz[j]);
+        // token: every DMMA waits for the last product, so ptxas cannot interleave the DMULs
+        // with the DMMAs (one DMMA <-> FP64-vector transition per k-step instead of 36)
+        double tok;
+        asm volatile("sub.f64 %0, %1, %1;" : "=d"(tok) : "d"(b[17]));
+        const double a0t = a0 + tok, a1t = a1 + tok;
+#pragma unroll
+        for (int j = 0; j < 18; ++j) {
+            asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+                         : "+d"(acc[0][j][0]), "+d"(acc[0][j][1]) : "d"(a0t), "d"(b[j]));
+            asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+                         : "+d"(acc[1][j][0]), "+d"(acc[1][j][1]) : "d"(a1t), "d"(b[j]));
+        }
+        y *= 0.9999999;
+    }
+    double s = 0;
+#pragma unroll
+    for (int i = 0; i < 2; ++i)
+#pragma unroll
+        for (int j = 0; j < 18; ++j) s += acc[i][j][0] + acc[i][j][1];
+    out[blockIdx.x * blockDim.x + threadIdx.x] = s;
+}
+
 template <typename F>
 float timeit(F f) {
     cudaEvent_t a, b;
@@ -370,6 +434,12 @@ int main() {
         // useful = 12 of 16 DMMA rows in the spread mixes above
         ms = timeit([&] { spreadmix_kernel<true><<<g2, 128>>>(out, iters); });
         printf("spread mix (36 DMMA + 18 DMUL), USEFUL rate: %.2f TFLOP/s\n", 0.75 * fl / ms / 1e9);
+        ms = timeit([&] { spreadmix16_kernel<true><<<g2, 128>>>(out, iters); });
+        printf("spread mix m16n8k4 (18 DMMA16 + 18 DMUL, 8 warps/SM): %.2f TFLOP/s issued, USEFUL %.2f\n", fl / ms / 1e9, 0.75 * fl / ms / 1e9);
+        ms = timeit([&] { spreadmix16_kernel<false><<<g2, 128>>>(out, iters); });
+        printf("spread mix m16n8k4 without DMUL: %.2f TFLOP/s issued\n", fl / ms / 1e9);
+        ms = timeit([&] { spreadmix_grouped_kernel<<<g2, 128>>>(out, iters); });
+        printf("spread mix, 18 DMUL grouped in one asm block: %.2f TFLOP/s issued, USEFUL %.2f\n", fl / ms / 1e9, 0.75 * fl / ms / 1e9);
         double flu = 2.0 * 12 * 8 * 18 * 4 * (double)iters * g2 * 4;
         ms = timeit([&] { hybrid_kernel<18><<<g2, 128>>>(out, iters); });
         printf("hybrid 18 DMMA + 72 DFMA + 22 DMUL, 8 warps/SM, USEFUL: %.2f TFLOP/s\n", flu / ms / 1e9);
