@@ -359,6 +359,11 @@ def main():
         "roofline": {"bound": "alu", "kernel": dom, "achieved": achieved, "peak": fp64_peak,
                      "unit": "TFLOP/s", "frac": achieved / fp64_peak, "traffic": traffic,
                      "traffic_source": traffic_src,
+                     "traffic_note": ("DRAM bytes are dominated by the plan-time window-tap table (d x 2m_w doubles "
+                                      "per node, read once per launch; DESIGN.md §6): evaluating the taps in the "
+                                      "kernel instead would add ~130 FP64 vector ops per lane and k-step to a "
+                                      "kernel bound by the shared FP64/DMMA pipe, while the table runs at ~20 % "
+                                      "of HBM bandwidth") if traffic else None,
                      "algorithmic": f"2*(2m_w)^d flops per node per launch, {pts_per_launch:.3g} nodes/launch",
                      "peak_source": f"{N_SM} SMs x {FP64_FMA_PER_CLK_PER_SM} FP64 FMA/clk x 2 x sm_max_mhz "
                                     f"{pk.get('sm_max_mhz')} (DESIGN.md)",
