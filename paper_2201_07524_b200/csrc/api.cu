@@ -644,11 +644,20 @@ int sinkhorn_solve(sk_ctx_t ctx, int d, const double* x, long long n_local, cons
     double* pb = pa + nn;
     double* pu = pb + mm;
     double* pv = pu + nn;
+    // host inputs: the nodes go first on the context stream (the plan needs them); the
+    // weights, needed only from sinkhorn_run on, travel on a side stream behind the plan
+    static thread_local cudaStream_t copy_stream = nullptr;
+    cudaEvent_t weights_ready = nullptr;
     if (inputs_on_host) {
         if (nn) SK_CUDA(cudaMemcpyAsync(px, x, sizeof(double) * nn * d, cudaMemcpyHostToDevice, s));
         if (mm) SK_CUDA(cudaMemcpyAsync(py, y, sizeof(double) * mm * d, cudaMemcpyHostToDevice, s));
-        if (nn) SK_CUDA(cudaMemcpyAsync(pa, a, sizeof(double) * nn, cudaMemcpyHostToDevice, s));
-        if (mm) SK_CUDA(cudaMemcpyAsync(pb, b, sizeof(double) * mm, cudaMemcpyHostToDevice, s));
+        if (!copy_stream) SK_CUDA(cudaStreamCreateWithFlags(&copy_stream, cudaStreamNonBlocking));
+        SK_CUDA(cudaEventCreateWithFlags(&weights_ready, cudaEventDisableTiming));
+        SK_CUDA(cudaEventRecord(weights_ready, s));            // buf is ordered on s
+        SK_CUDA(cudaStreamWaitEvent(copy_stream, weights_ready, 0));
+        if (nn) SK_CUDA(cudaMemcpyAsync(pa, a, sizeof(double) * nn, cudaMemcpyHostToDevice, copy_stream));
+        if (mm) SK_CUDA(cudaMemcpyAsync(pb, b, sizeof(double) * mm, cudaMemcpyHostToDevice, copy_stream));
+        SK_CUDA(cudaEventRecord(weights_ready, copy_stream));
         dx = px; dy = py; da = pa; db = pb;
     }
     SK_TRY(launch_fill(pu, nn, 1.0, s));
@@ -657,6 +666,10 @@ int sinkhorn_solve(sk_ctx_t ctx, int d, const double* x, long long n_local, cons
     prof_begin(ST_PLAN, s);
     int st = fastsum_plan(ctx, &plan, d, dx, nn, dy, mm, lambda, N, sigma, m_w, eps_B, p_smooth);
     prof_end(ST_PLAN, s);
+    if (weights_ready) {
+        cudaStreamWaitEvent(s, weights_ready, 0);
+        cudaEventDestroy(weights_ready);
+    }
     if (!st) st = sinkhorn_run(plan, da, db, iters, 0.0, 0, pu, pv, info);
     if (!st) st = sinkhorn_divergence(plan, da, db, pu, pv, s_dual, s_cost);
     fastsum_plan_destroy(plan);

@@ -104,6 +104,10 @@ taps_precompute_kernel(const double* __restrict__ u, long long count, const __gr
 #ifndef SK_INTERP3_MINB
 #define SK_INTERP3_MINB 3
 #endif
+#ifndef SK_INTERP3_KUNROLL
+#define SK_INTERP3_KUNROLL 1
+#endif
+constexpr int kInterpKUnroll = SK_INTERP3_KUNROLL;
 struct InterpDCfg {
     static constexpr int W = 12, KS = W / 4, NT = 128, NWARP = NT / 32, TS = 3 * W;
     static constexpr int XS = W + 2;                          // phi_x row stride (doubles)
@@ -203,7 +207,7 @@ interp3_dmma_kernel(const CellBatch* __restrict__ batches, int nbatches, const d
         const long long sxs = STAGE ? W * W : n2;
         const long long ry[3] = {STAGE ? g * W : (long long)g * n, STAGE ? ty1 * W : (long long)ty1 * n,
                                  STAGE ? (4 + g) * W : (long long)(4 + g) * n};
-#pragma unroll 1
+#pragma unroll kInterpKUnroll
         for (int k = 0; k < W / 2; ++k) {
             // three m-tiles (one period of ty) per step, their DMMAs interleaved s-major so
             // 12 independent accumulations separate dependent DMMAs
