@@ -53,3 +53,12 @@ def test_binding_loads_and_matches_header():
     # no compute without a GPU: only error paths that do not touch the device
     assert capi._lib.sinkhorn_run(None, None, None, 1, 0.0, 0, None, None, None) == capi.SK_EINVAL
     assert b"NULL plan" in capi._lib.sk_last_error()
+
+
+def test_missing_library_fails_loudly():
+    """The product path has no CPU fallback: without the CUDA library the binding refuses to import."""
+    import sys
+    env = dict(os.environ, SK_LIB_PATH="/nonexistent/libsk_nfft.so")
+    r = subprocess.run([sys.executable, "-c", "import paper_2201_07524_b200.capi"], cwd=ROOT, env=env,
+                       capture_output=True, text=True)
+    assert r.returncode != 0 and "ImportError" in r.stderr
