@@ -382,6 +382,9 @@ def main():
         "clocks": clk,
         "divergence": {"s_dual": results[0], "s_cost": results[1]} if results else None,
         "kappa_log10_est": results[2].kappa_log10_est if results else None,
+        # SURVEY §8(d)'s narrower definition: iterations / device time of sinkhorn_run alone
+        # (no plan, no divergence), from the run's own CUDA events, last timed step, rank 0
+        "sinkhorn_run_iterations_per_s": (cfg.iters / results[2].seconds) if results and results[2].seconds > 0 else None,
     }
     if e2e:
         line["e2e"] = e2e
