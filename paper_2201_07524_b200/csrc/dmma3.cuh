@@ -277,6 +277,7 @@ struct SpreadDCfg {
     static constexpr size_t SMEM_BYTES = sizeof(double) * (NWARP * REG);
 };
 
+template <bool XP>
 __global__ void __launch_bounds__(128, 2)
 spread3_dmma_kernel(const SpreadItem* __restrict__ items, int nitems, const CellBatch* __restrict__ segs,
                     const double* __restrict__ taps, const double* __restrict__ w,
@@ -315,13 +316,22 @@ spread3_dmma_kernel(const SpreadItem* __restrict__ items, int nitems, const Cell
             // node's 12 phi_y values -> 12 loads per k-step instead of 36.
             const int z1 = (8 + g) % W;
             // operands of k-step s: w*phi_x (A, 2 rows), phi_y[0..12), phi_z at {g, z1, 4+g}
+            // A rows are region rows r = tx + ox_node: a segment may hold the nodes of an x-pair
+            // of cells (seg.pad = nodes of the first cell, ox = 0; the rest sit at ox = 1)
             auto load_ops = [&](int s, double& wv, double& x0, double& x1, double2 (&yy)[6], double (&zz)[3]) {
                 const int jr = 4 * s + q;                            // node of this lane's A/B
                 const bool ok = jr < seg.count;
                 const double* tr = T0 + (ok ? jr : 0) * TS;
                 wv = __ldg(w0 + (ok ? jr : 0));   // masked at use: no predicated load to wait on
-                x0 = __ldg(tr + g);
-                x1 = (8 + g < W) ? __ldg(tr + 8 + g) : 0.0;
+                if constexpr (XP) {
+                    const int oxn = jr >= seg.pad ? 1 : 0;   // segment cell has ox = 0
+                    const int t0 = g - oxn, t1 = 8 + g - oxn;
+                    x0 = (t0 >= 0) ? __ldg(tr + t0) : 0.0;
+                    x1 = (t1 < W) ? __ldg(tr + t1) : 0.0;
+                } else {                                     // rows are the cell's tx
+                    x0 = __ldg(tr + g);
+                    x1 = (8 + g < W) ? __ldg(tr + 8 + g) : 0.0;
+                }
                 const double2* y2 = reinterpret_cast<const double2*>(tr + W);
 #pragma unroll
                 for (int i = 0; i < 6; ++i) yy[i] = __ldg(y2 + i);
@@ -340,7 +350,7 @@ spread3_dmma_kernel(const SpreadItem* __restrict__ items, int nitems, const Cell
                     if (lane < 2) prefetch_l2(w0 + n0 + 16 * lane);
                 }
                 const double wu = (4 * s + q < seg.count) ? wn : 0.0;
-                const double a0 = wu * x0n, a1 = wu * x1n;           // A[tx = g | 8 + g][k = q]
+                const double a0 = wu * x0n, a1 = wu * x1n;           // A[row g | 8 + g][k = q]
                 double yv[W], zv[3];
 #pragma unroll
                 for (int i = 0; i < 6; ++i) { yv[2 * i] = yn[i].x; yv[2 * i + 1] = yn[i].y; }
@@ -357,12 +367,12 @@ spread3_dmma_kernel(const SpreadItem* __restrict__ items, int nitems, const Cell
                     dmma884(acc[1][nt][0], acc[1][nt][1], a1, b);
                 }
             }
-            // add the cell's W^3 block into the region at offset (ox, oy, oz)
+            // add the block (region rows 0..12, the cell's (oy, oz) columns) into the region
 #pragma unroll
             for (int mt = 0; mt < 2; ++mt) {
-                const int tx = 8 * mt + g;
-                if (tx < W) {
-                    double* rx = REGm + (ox + tx) * S * S + oy * S + oz;
+                const int tr_ = 8 * mt + g;
+                if (XP ? tr_ < S : tr_ < W) {
+                    double* rx = REGm + (XP ? tr_ : ox + tr_) * S * S + oy * S + oz;
 #pragma unroll
                     for (int nt = 0; nt < NTILE; ++nt)
 #pragma unroll

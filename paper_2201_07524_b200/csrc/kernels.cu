@@ -124,6 +124,7 @@ struct ScaleParams {
     double rho, n, r2max;
     int d, T, tiles_per_axis;
     int cell_minor;   // 1: key = tile * T^d + cell-within-tile index: nodes sorted by cell
+    int xminor;       // cell-within-tile digits with x least significant (d = 3 spread x-pairs)
     int Td;           // T^d
 };
 
@@ -145,7 +146,13 @@ __global__ void scale_key_kernel(const double* __restrict__ pts, long long count
             int tc = c / sp.T;
             tc = tc < 0 ? 0 : (tc >= sp.tiles_per_axis ? sp.tiles_per_axis - 1 : tc);
             k = k * sp.tiles_per_axis + tc;
-            sub = sub * sp.T + (c - tc * sp.T);
+            if (sp.xminor) {
+                int mul = 1;
+                for (int q = 0; q < a; ++q) mul *= sp.T;
+                sub += (c - tc * sp.T) * mul;
+            } else {
+                sub = sub * sp.T + (c - tc * sp.T);
+            }
         }
         if (!ok || !(r2 <= sp.r2max)) atomicMin(bad, (int)i);
         key[i] = sp.cell_minor ? k * sp.Td + sub : k;
@@ -166,6 +173,7 @@ int launch_scale_key(Plan& P, const double* pts, long long count, double* u_unso
     sp.T = P.tile_cells;
     sp.tiles_per_axis = P.tiles_per_axis;
     sp.cell_minor = P.dmma ? 1 : 0;
+    sp.xminor = P.spread_xpairs ? 1 : 0;
     sp.Td = 1;
     for (int a = 0; a < P.d; ++a) sp.Td *= P.tile_cells;
     scale_key_kernel<<<grid_for(count, 256), 256, 0, s>>>(pts, count, sp, u_unsorted, key, idx, bad);

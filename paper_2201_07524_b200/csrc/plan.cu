@@ -264,16 +264,42 @@ static int build_items(Plan& P, NodeSet& S, cudaStream_t s) {
 //   segs:    <= seg_max nodes of one cell (spread),
 //   sitems:  consecutive segs of one super-tile, <= item_max nodes (spread work unit of a
 //            warp, flushed once with coalesced atomics), sorted by size (stable) for balance.
-struct CellGeom { int d, n, tpa, T, Td; };
+struct CellGeom { int d, n, tpa, T, Td, xminor, xpairs; };
 
 __device__ __forceinline__ int cell_of_key(int key, const CellGeom g) {
     const int tile = key / g.Td;
     int sub = key % g.Td, rest = tile, tc[3], cc[3];
     for (int a = g.d - 1; a >= 0; --a) { tc[a] = rest % g.tpa; rest /= g.tpa; }
-    for (int a = g.d - 1; a >= 0; --a) { cc[a] = g.T * tc[a] + sub % g.T; sub /= g.T; }
+    if (g.xminor)   // x least significant (scale_key_kernel's xminor order)
+        for (int a = 0; a < g.d; ++a) { cc[a] = g.T * tc[a] + sub % g.T; sub /= g.T; }
+    else
+        for (int a = g.d - 1; a >= 0; --a) { cc[a] = g.T * tc[a] + sub % g.T; sub /= g.T; }
     int cell = 0;
     for (int a = 0; a < g.d; ++a) cell = cell * g.n + cc[a];
     return cell;
+}
+
+// Spread segments group the runs (cells) of a tile: with xpairs, the two cells of an x-pair
+// (same y, z; x digits 0 and 1, adjacent keys) form one group whose nodes are contiguous, the
+// x-digit-0 cell's nodes first; otherwise a group is one cell. Returns the run after the group.
+__device__ __forceinline__ int spread_group(const int* __restrict__ keys, const int* __restrict__ cnts,
+                                            int q, int nruns, int tile, const CellGeom g, int& count,
+                                            int& countA, int& key0) {
+    count = cnts[q];
+    countA = count;
+    key0 = keys[q];
+    if (!g.xpairs) return q + 1;
+    const int dx = (keys[q] % g.Td) % g.T;
+    if (dx != 0) {            // a lone x-digit-1 cell: all its nodes sit at x offset 1
+        countA = 0;
+        key0 = keys[q] - dx;
+        return q + 1;
+    }
+    if (q + 1 < nruns && keys[q + 1] / g.Td == tile && keys[q + 1] == keys[q] + 1) {
+        count += cnts[q + 1];
+        return q + 2;
+    }
+    return q + 1;
 }
 
 // per run: interp batches; per tile-head run: number of segs / items of its tile (greedy
@@ -288,13 +314,16 @@ __global__ void cell_counts_kernel(const int* __restrict__ keys, const int* __re
     int ns = 0, ni = 0;
     if (r == 0 || keys[r - 1] / g.Td != tile) {
         int fill = 0;
-        for (int q = r; q < nruns && keys[q] / g.Td == tile; ++q)
-            for (int b = 0; b < cnts[q]; b += seg_max) {
-                const int c = min(seg_max, cnts[q] - b);
+        for (int q = r; q < nruns && keys[q] / g.Td == tile;) {
+            int cnt, cntA, key0;
+            q = spread_group(keys, cnts, q, nruns, tile, g, cnt, cntA, key0);
+            for (int b = 0; b < cnt; b += seg_max) {
+                const int c = min(seg_max, cnt - b);
                 if (ni == 0 || fill + c > item_max) { ++ni; fill = 0; }
                 fill += c;
                 ++ns;
             }
+        }
     }
     nseg[r] = ns;
     nitem[r] = ni;
@@ -315,10 +344,13 @@ __global__ void cell_write_kernel(const int* __restrict__ keys, const int* __res
     if (!(r == 0 || keys[r - 1] / g.Td != tile)) return;
     int so = seg_off[r], io = item_off[r] - 1, fill = 0;
     bool first = true;
-    for (int q = r; q < nruns && keys[q] / g.Td == tile; ++q) {
-        const int cq = cell_of_key(keys[q], g);
-        for (int b = 0; b < cnts[q]; b += seg_max) {
-            const int c = min(seg_max, cnts[q] - b);
+    for (int q = r; q < nruns && keys[q] / g.Td == tile;) {
+        const int q0 = q;
+        int cnt, cntA, key0;
+        q = spread_group(keys, cnts, q, nruns, tile, g, cnt, cntA, key0);
+        const int cq = cell_of_key(key0, g);
+        for (int b = 0; b < cnt; b += seg_max) {
+            const int c = min(seg_max, cnt - b);
             if (first || fill + c > item_max) {
                 if (!first) { items[io].count = fill; item_cnt[io] = fill; }
                 ++io;
@@ -326,7 +358,8 @@ __global__ void cell_write_kernel(const int* __restrict__ keys, const int* __res
                 fill = 0;
                 first = false;
             }
-            segs[so++] = CellBatch{cq, rstart[q] + b, c, 0};
+            // pad = nodes of this piece in the x-digit-0 cell (the first ones)
+            segs[so++] = CellBatch{cq, rstart[q0] + b, c, g.xpairs ? min(max(cntA - b, 0), c) : c};
             items[io].seg_end = so;
             fill += c;
         }
@@ -350,7 +383,9 @@ static int build_cell_lists(Plan& P, NodeSet& S, cudaStream_t s) {
     const int d = P.d, n = P.n, tpa = P.tiles_per_axis, T = P.tile_cells;
     int Td = 1;
     for (int a = 0; a < d; ++a) Td *= T;
-    const CellGeom g{d, n, tpa, T, Td};
+    // x-pair spread segments pay where cells are sparse (few nodes per cell, so the per-segment
+    // region update dominates): decided per side once the cells are counted (below)
+    CellGeom g{d, n, tpa, T, Td, P.spread_xpairs ? 1 : 0, 0};
     // spread work-unit size: enough items to keep ~4 per resident warp busy (148 SMs x 8
     // warps), at most kSpreadItemMax nodes (one region flush per item)
     const int item_max = (int)std::max(128LL, std::min((long long)kSpreadItemMax, count / 4736));
@@ -373,6 +408,8 @@ static int build_cell_lists(Plan& P, NodeSet& S, cudaStream_t s) {
     SK_CUDA(cudaMemcpyAsync(&nruns, small, sizeof(int), cudaMemcpyDeviceToHost, s));
     SK_CUDA(cudaStreamSynchronize(s));
     const int thr = 256, blk = (nruns + thr - 1) / thr;
+    S.xpairs = P.spread_xpairs && (long long)kXPairMaxDensity * nruns > count;
+    g.xpairs = S.xpairs ? 1 : 0;
     SK_CUDA(cub::DeviceScan::ExclusiveSum(tmp, tb, cnts, rstart, nruns, s));
     cell_counts_kernel<<<blk, thr, 0, s>>>(keys, cnts, nruns, g, seg_max, item_max, nb, nseg, nitem);
     SK_CUDA(cudaGetLastError());
@@ -599,6 +636,7 @@ int build_plan(Ctx* ctx, Plan** out, int d, const double* x, long long n, const 
         // hybrid DMMA+DFMA spread (no padded rows): opt-in until it beats the padded kernel
         // (c5: 20.6 vs 15.5 ms under ncu, issue/latency-bound with 2 passes per segment)
         P->spread_hybrid = P->dmma && d == 3 && getenv("SK_SPREAD3_HYBRID") != nullptr;
+        P->spread_xpairs = P->dmma && d == 3 && !P->spread_hybrid && getenv("SK_NO_XPAIRS") == nullptr;
     }
     P->tile_cells = P->dmma ? (d == 3 ? 2 : kSup2) : choose_tile(d, ng, P->tiled);
     P->tiles_per_axis = ng / P->tile_cells;

@@ -13,6 +13,7 @@ namespace sk {
 
 constexpr int kMaxD = 3;
 constexpr int kMaxW = 16;            // 2 * m_w taps per axis, m_w <= 8
+constexpr int kXPairMaxDensity = 96; // x-pair spread segments when nodes per cell < this
 
 // Thread-local error message + status helpers (api.cu).
 int set_error(int code, const std::string& msg);
@@ -62,6 +63,7 @@ struct NodeSet {
     void* batches = nullptr;     // CellBatch[nbatches]: <= 32 nodes of one cell (interp)
     int nbatches = 0;
     int ncells = 0;              // non-empty cells
+    bool xpairs = false;         // spread segments span x-pairs of cells (sparse cells, d = 3)
     void* segs = nullptr;        // CellBatch[nsegs]: <= kSegMax nodes of one cell (spread)
     int nsegs = 0;
     void* sitems = nullptr;      // SpreadItem[nsitems]: segments of one 2^3 super-tile (spread)
@@ -133,6 +135,8 @@ struct Plan {
     bool tiled = false;       // v2 tiled spread/interp usable (d = 3, 2 m_w in {12, 16})
     bool dmma = false;        // FP64 tensor-core spread/interp (d = 3, 2 m_w = 12)
     bool spread_hybrid = false;  // d = 3 spread: DMMA rows 0..7 + DFMA rows 8..11 (no padding)
+    bool spread_xpairs = false;  // d = 3 padded spread: x-minor keys; sides with sparse cells group
+                                 // x-pairs of cells into one segment (13 of 16 rows)
     void* winpoly = nullptr;  // host WinPoly (window tap polynomials)
 };
 

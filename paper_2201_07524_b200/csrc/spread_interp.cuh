@@ -180,13 +180,15 @@ inline int spread_dispatch(Plan& P, const NodeSet& S, const double* w, double* g
         using C = SpreadDCfg;
         static bool attr = false;
         if (!attr) {
-            cudaFuncSetAttribute(spread3_dmma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM_BYTES);
+            cudaFuncSetAttribute(spread3_dmma_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM_BYTES);
+            cudaFuncSetAttribute(spread3_dmma_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM_BYTES);
             attr = true;
         }
         if (S.nsitems > 0) {
-            const int g = persistent_grid(spread3_dmma_kernel, C::NT, C::SMEM_BYTES, (S.nsitems + C::NWARP - 1) / C::NWARP);
-            spread3_dmma_kernel<<<g, C::NT, C::SMEM_BYTES, s>>>((const SpreadItem*)S.sitems, S.nsitems,
-                                                                (const CellBatch*)S.segs, S.taps, w, grid, P.n);
+            const auto kern = S.xpairs ? spread3_dmma_kernel<true> : spread3_dmma_kernel<false>;
+            const int g = persistent_grid(kern, C::NT, C::SMEM_BYTES, (S.nsitems + C::NWARP - 1) / C::NWARP);
+            kern<<<g, C::NT, C::SMEM_BYTES, s>>>((const SpreadItem*)S.sitems, S.nsitems,
+                                                 (const CellBatch*)S.segs, S.taps, w, grid, P.n);
             count_launch();
         }
         cudaError_t e = cudaGetLastError();
