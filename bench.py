@@ -298,26 +298,34 @@ def main():
         e2e = {"value": args.steps * cfg.iters / (float(t.item()) * 1e-3), "unit": "it/s",
                "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": 16}
 
-    # ---- fast-summation point-evaluations/s (one K v product, targets = all x)
+    # ---- fast-summation point-evaluations/s: per direction, median over reps of
+    # one fast summation each (CUDA events), max over ranks; also NUFFT points/s = (n_s + n_t)/t
     plan = capi.Plan(ctx, dx, dy, cfg.lam, cfg.N, cfg.sigma, cfg.m_w, cfg.eps_B, cfg.p)
-    w = torch.rand(hy.shape[0], dtype=torch.float64, device="cuda")
-    out = torch.empty(hx.shape[0], dtype=torch.float64, device="cuda")
-    for _ in range(2):
-        capi.fastsum_apply(plan, w, 0, 0, out)
-    torch.cuda.synchronize()
-    reps = 5
-    barrier()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record(stream)
-    for _ in range(reps):
-        capi.fastsum_apply(plan, w, 0, 0, out)
-    e1.record(stream)
-    torch.cuda.synchronize()
-    t = torch.tensor([e0.elapsed_time(e1) / reps], dtype=torch.float64, device="cuda")
-    if world > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    apply_ms = float(t.item())
+    wy = torch.rand(hy.shape[0], dtype=torch.float64, device="cuda")
+    wx = torch.rand(hx.shape[0], dtype=torch.float64, device="cuda")
+    ox = torch.empty(hx.shape[0], dtype=torch.float64, device="cuda")
+    oy = torch.empty(hy.shape[0], dtype=torch.float64, device="cuda")
+    reps = 20 if cfg.n + cfg.m <= 2e7 else 5
+    apply_dir = {}
+    for tr, (w_, o_) in ((0, (wy, ox)), (1, (wx, oy))):
+        for _ in range(2):
+            capi.fastsum_apply(plan, w_, tr, 0, o_)
+        torch.cuda.synchronize()
+        times = []
+        for _ in range(reps):
+            barrier()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            capi.fastsum_apply(plan, w_, tr, 0, o_)
+            e1.record(stream)
+            torch.cuda.synchronize()
+            times.append(e0.elapsed_time(e1))
+        t = torch.tensor([statistics.median(times)], dtype=torch.float64, device="cuda")
+        if world > 1:
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        apply_dir[tr] = float(t.item())
     plan.close()
+    apply_ms = apply_dir[0]
     point_evals = cfg.n / (apply_ms * 1e-3)
 
     # ---- roofline of the dominant kernel (from the live CUDA-event stage profile)
@@ -356,6 +364,11 @@ def main():
                    "l2": "256 MB buffer written between timed steps"},
         "fastsum_point_evals_per_s": point_evals,   # all n targets of one K v, max-over-ranks time
         "fastsum_apply_ms": apply_ms,
+        "fastsum": {"Kv": {"ms": apply_dir[0], "point_evals_per_s": cfg.n / (apply_dir[0] * 1e-3),
+                           "nufft_points_per_s": (cfg.n + cfg.m) / (apply_dir[0] * 1e-3)},
+                    "KTu": {"ms": apply_dir[1], "point_evals_per_s": cfg.m / (apply_dir[1] * 1e-3),
+                            "nufft_points_per_s": (cfg.n + cfg.m) / (apply_dir[1] * 1e-3)},
+                    "reps": reps, "statistic": "median"},
         "roofline": {"bound": "alu", "kernel": dom, "achieved": achieved, "peak": fp64_peak,
                      "unit": "TFLOP/s", "frac": achieved / fp64_peak, "traffic": traffic,
                      "traffic_source": traffic_src,
