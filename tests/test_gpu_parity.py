@@ -543,3 +543,38 @@ def test_empty_measure_is_rejected(capi, ctx):
     P = capi.Plan(ctx, dev(x), dev(np.zeros((0, 2))), 10.0, 32)
     t = capi.fastsum_apply(P, dev(np.zeros(0)), 0, 0).cpu().numpy()
     assert t.shape == (10,) and np.all(t == 0.0)
+
+
+def test_short_runs_and_rescale_policies(capi, ctx):
+    """iters = 1 and 2 run eagerly (no graph replay): the scalings equal the oracle's Alg. 1
+    after the same number of iterations; rescale policy 2 (v <- v / max v, reading Q4) is a pure
+    gauge like policy 1."""
+    cfg = get("c3").with_(n=3000, m=2500)
+    x, y, a, b = make_inputs(cfg)
+    a, b = a / a.sum(), b / b.sum()
+    P = capi.Plan(ctx, dev(x), dev(y), cfg.lam, cfg.N, cfg.sigma, cfg.m_w, cfg.eps_B, cfg.p)
+    for iters in (1, 2):
+        u, v, info = capi.sinkhorn_run(P, dev(a), dev(b), iters)
+        al, at, bad = dense.sinkhorn_plain(x, y, a, b, cfg.lam, iters)
+        assert bad == 0 and info.iters_done == iters
+        assert rel_linf(u.cpu().numpy(), al) <= 1e-10 and rel_linf(v.cpu().numpy(), at) <= 1e-10
+    s0 = capi.sinkhorn_divergence(P, dev(a), dev(b), *capi.sinkhorn_run(P, dev(a), dev(b), 25)[:2])
+    s2 = capi.sinkhorn_divergence(P, dev(a), dev(b), *capi.sinkhorn_run(P, dev(a), dev(b), 25, rescale_policy=2)[:2])
+    assert abs(s0[1] - s2[1]) <= 1e-11 * abs(s0[1]) and abs(s0[0] - s2[0]) <= 1e-11 * abs(s0[0])
+
+
+def test_independent_plans_interleaved(capi, ctx):
+    """Two live plans of different sizes (distinct cuFFT handles from the pool, distinct scratch)
+    applied alternately give the same results as each alone."""
+    c3 = get("c3").with_(n=4000, m=3000)
+    c2 = get("c2").with_(n=5000, m=4000)
+    x3, y3, a3, b3 = make_inputs(c3)
+    x2, y2, a2, b2 = make_inputs(c2)
+    P3 = capi.Plan(ctx, dev(x3), dev(y3), c3.lam, c3.N, c3.sigma, c3.m_w, c3.eps_B, c3.p)
+    t3 = capi.fastsum_apply(P3, dev(b3), 0, 0).cpu().numpy()
+    P2 = capi.Plan(ctx, dev(x2), dev(y2), c2.lam, c2.N, c2.sigma, c2.m_w, c2.eps_B, c2.p)
+    t2 = capi.fastsum_apply(P2, dev(b2), 0, 0).cpu().numpy()
+    for _ in range(3):
+        u3 = capi.fastsum_apply(P3, dev(b3), 0, 0).cpu().numpy()
+        u2 = capi.fastsum_apply(P2, dev(b2), 0, 0).cpu().numpy()
+        assert rel_linf(u3, t3) <= 1e-13 and rel_linf(u2, t2) <= 1e-13
