@@ -461,20 +461,30 @@ static int run_impl(sk_plan_t plan, const double* a, const double* b, int iters,
             SK_TRY(launch_scale_vec(P.v_s, Y.count, r, s));
         }
         if (last) SK_TRY(launch_reduce_sum_log(nullptr, P.v_s, Y.count, slot(P, SL_D), 1, s));
-        // odd Delta: t = K v, u = a / t   (Eq. (even_F_sink))
-        SK_TRY(apply_sorted(P, 0, 0, P.v_s, P.t_sorted));
-        prof_begin(ST_UPDATE, s);
-        SK_TRY(launch_update(P, 0, P.t_sorted, P.a_s, P.u_s, trace_dev ? 2 : ((tol > 0 || last) ? 1 : 0), it,
-                             iter_dev, s));
-        prof_end(ST_UPDATE, s);
+        // odd Delta: t = K v, u = a / t   (Eq. (even_F_sink)). Without a residual or
+        // trace to reduce, the division is fused into the interpolation epilogue (no t round
+        // trip through HBM, one kernel fewer); otherwise the update kernel also reduces.
+        const int want_u = trace_dev ? 2 : ((tol > 0 || last) ? 1 : 0);
+        FusedUpd fu_u;
+        fu_u.p = P.a_s; fu_u.x = P.u_s; fu_u.bad = P.flag; fu_u.iter_dev = iter_dev; fu_u.iter = it;
+        SK_TRY(apply_sorted(P, 0, 0, P.v_s, P.t_sorted, want_u ? nullptr : &fu_u));
+        if (want_u) {
+            prof_begin(ST_UPDATE, s);
+            SK_TRY(launch_update(P, 0, P.t_sorted, P.a_s, P.u_s, want_u, it, iter_dev, s));
+            prof_end(ST_UPDATE, s);
+        }
         if (tol > 0 || last) SK_TRY(finalize_update(P, slot(P, SL_UPD)));
         if (trace_dev) SK_TRY(record(it, 0));
         // even Delta: t~ = K^T u, v = b / t~   (Eq. (odd_F_sink))
-        SK_TRY(apply_sorted(P, 1, 0, P.u_s, P.t_sorted));
-        prof_begin(ST_UPDATE, s);
-        SK_TRY(launch_update(P, 1, P.t_sorted, P.b_s, P.v_s, trace_dev ? 2 : 0, it, iter_dev, s));
-        prof_end(ST_UPDATE, s);
-        if (trace_dev) SK_TRY(record(it, 1));
+        FusedUpd fu_v;
+        fu_v.p = P.b_s; fu_v.x = P.v_s; fu_v.bad = P.flag + 2; fu_v.iter_dev = iter_dev; fu_v.iter = it;
+        SK_TRY(apply_sorted(P, 1, 0, P.u_s, P.t_sorted, trace_dev ? nullptr : &fu_v));
+        if (trace_dev) {
+            prof_begin(ST_UPDATE, s);
+            SK_TRY(launch_update(P, 1, P.t_sorted, P.b_s, P.v_s, 2, it, iter_dev, s));
+            prof_end(ST_UPDATE, s);
+            SK_TRY(record(it, 1));
+        }
         return SK_OK;
     };
     int it0 = 0;

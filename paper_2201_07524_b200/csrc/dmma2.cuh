@@ -27,7 +27,7 @@ struct Interp2Cfg {
 
 __global__ void __launch_bounds__(128, 4)
 interp2_dmma_kernel(const CellBatch* __restrict__ batches, int nbatches, const double* __restrict__ taps,
-                    const double* __restrict__ grid, int n, double* __restrict__ t_out) {
+                    const double* __restrict__ grid, int n, double* __restrict__ t_out, const FusedUpd fu) {
     using C = Interp2Cfg;
     constexpr int W = C::W, KS = C::KS, m = W / 2, TS = C::TS;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -73,14 +73,17 @@ interp2_dmma_kernel(const CellBatch* __restrict__ batches, int nbatches, const d
                 v += __shfl_xor_sync(0xffffffffu, v, 16);
                 acc[nt][e] = v;
             }
-        if (g == 0) {
+        // every lane now holds the 8 sums of its q; lane (g, q) emits node 8 (g/2) + 2 q + g%2,
+        // so the 32 results (and the fused division) take one full-warp pass
+        {
+            double v = acc[0][0];
 #pragma unroll
             for (int nt = 0; nt < 4; ++nt)
 #pragma unroll
-                for (int e = 0; e < 2; ++e) {
-                    const int p = 8 * nt + 2 * q + e;
-                    if (p < B.count) t_out[B.start + p] = acc[nt][e];
-                }
+                for (int e = 0; e < 2; ++e)
+                    if (g == 2 * nt + e) v = acc[nt][e];
+            const int p = 8 * (g >> 1) + 2 * q + (g & 1);
+            if (p < B.count) emit_t(t_out, fu, B.start + p, v);
         }
     }
 }

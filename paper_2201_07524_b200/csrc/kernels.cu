@@ -721,10 +721,11 @@ int launch_spread(Plan& P, int side, const double* w_sorted, double* grid, cudaS
     return SK_OK;
 }
 
-int launch_interp(Plan& P, int side, const double* grid, double* t_sorted, cudaStream_t s) {
+int launch_interp(Plan& P, int side, const double* grid, double* t_sorted, cudaStream_t s,
+                  const FusedUpd& fu) {
     const NodeSet& S = P.side[side];
     if (S.count <= 0) return SK_OK;
-    SK_TRY(interp_dispatch(P, S, grid, t_sorted, s));
+    SK_TRY(interp_dispatch(P, S, grid, t_sorted, s, fu));
     return SK_OK;
 }
 

@@ -775,7 +775,8 @@ int destroy_plan(Plan* P) {
 }
 
 // One fast summation on sorted data: transpose 0: sources y (side 1) -> targets x (side 0).
-int apply_sorted(Plan& P, int transpose, int kernel, const double* w_sorted, double* t_sorted) {
+int apply_sorted(Plan& P, int transpose, int kernel, const double* w_sorted, double* t_sorted,
+                 const FusedUpd* fu) {
     cudaStream_t s = P.ctx->stream;
     const int src = transpose ? 0 : 1, dst = transpose ? 1 : 0;
     prof_begin(ST_SPREAD, s);
@@ -809,8 +810,19 @@ int apply_sorted(Plan& P, int transpose, int kernel, const double* w_sorted, dou
         prof_end(ST_FFT_INV, s);
     }
     prof_begin(ST_INTERP, s);
-    SK_TRY(launch_interp(P, dst, P.grid, t_sorted, s));
-    if (P.rpow == 1) SK_TRY(launch_nearfield(P, src, dst, kernel, w_sorted, t_sorted, s));
+    if (fu && fu->x) {
+        // the caller wants x = p / t: fused into the DMMA interpolation when it can be
+        if (P.dmma && P.rpow == 2) {
+            SK_TRY(launch_interp(P, dst, P.grid, t_sorted, s, *fu));
+        } else {
+            SK_TRY(launch_interp(P, dst, P.grid, t_sorted, s));
+            if (P.rpow == 1) SK_TRY(launch_nearfield(P, src, dst, kernel, w_sorted, t_sorted, s));
+            SK_TRY(launch_update(P, dst, t_sorted, fu->p, fu->x, 0, fu->iter, fu->iter_dev, s));
+        }
+    } else {
+        SK_TRY(launch_interp(P, dst, P.grid, t_sorted, s));
+        if (P.rpow == 1) SK_TRY(launch_nearfield(P, src, dst, kernel, w_sorted, t_sorted, s));
+    }
     prof_end(ST_INTERP, s);
     return SK_OK;
 }

@@ -140,6 +140,30 @@ struct Plan {
     void* winpoly = nullptr;  // host WinPoly (window tap polynomials)
 };
 
+// Optional u/v update fused into the interpolation epilogue (a7): with x != nullptr the
+// interpolation writes x[i] = p[i] / t_i instead of t_i and flags t_i <= 1e-300 (SK_ENONPOS,
+// first index / iteration via atomicMin). Used when no residual or trace is wanted.
+struct FusedUpd {
+    const double* p = nullptr;
+    double* x = nullptr;
+    int* bad = nullptr;            // [index, iteration] of the first non-positive t
+    const int* iter_dev = nullptr; // graph replay: iteration number on the device
+    int iter = 0;
+};
+#ifdef __CUDACC__
+__device__ __forceinline__ void emit_t(double* __restrict__ t_out, const FusedUpd& fu, long long idx, double t) {
+    if (fu.x) {
+        if (!(t > 1e-300) || !isfinite(t)) {
+            atomicMin(fu.bad, (int)idx);
+            atomicMin(fu.bad + 1, fu.iter_dev ? *fu.iter_dev : fu.iter);
+        }
+        fu.x[idx] = fu.p[idx] / t;
+    } else {
+        t_out[idx] = t;
+    }
+}
+#endif
+
 // ---- kernels.cu launchers ----
 int launch_bbox(const double* pts, long long count, int d, double* out_minmax /*device [2*d]*/,
                 cudaStream_t s);
@@ -151,7 +175,8 @@ int launch_tile_offsets(const int* sorted_keys, long long count, int ntiles, int
                         cudaStream_t s);
 int launch_spread(Plan& P, int side, const double* w_sorted, double* grid, cudaStream_t s);
 int launch_taps(Plan& P, int side, cudaStream_t s);
-int launch_interp(Plan& P, int side, const double* grid, double* t_sorted, cudaStream_t s);
+int launch_interp(Plan& P, int side, const double* grid, double* t_sorted, cudaStream_t s,
+                  const FusedUpd& fu = FusedUpd());   // fu.x only on the DMMA interps (P.dmma)
 int launch_multiply(Plan& P, int kernel, cudaStream_t s);
 int launch_permute_in(const double* src, const int* perm, long long count, double* dst, cudaStream_t s);
 int launch_permute_out(const double* src, const int* perm, long long count, double* dst, cudaStream_t s);
@@ -189,7 +214,8 @@ void pruned_fft_teardown(Plan& P, cudaStream_t s);
 int pruned_fft_apply(Plan& P, int kernel, cudaStream_t s);   // a4 + a5 + a6 on P.grid in place
 int fft_acquire(int d, int n, cufftType type, cudaStream_t s, cufftHandle* out, long long batch = 1);
 void fft_release(int d, int n, cufftType type, cufftHandle h, long long batch = 1);
-int apply_sorted(Plan& P, int transpose, int kernel, const double* w_sorted, double* t_sorted);
+int apply_sorted(Plan& P, int transpose, int kernel, const double* w_sorted, double* t_sorted,
+                 const FusedUpd* fu = nullptr);   // fu: update fused into a7 where supported
 
 // ---- stage profiling (api.cu): CUDA-event pairs around each stage when enabled ----
 enum Stage { ST_SPREAD = 0, ST_ALLREDUCE, ST_FFT_FWD, ST_MULTIPLY, ST_FFT_INV, ST_INTERP, ST_UPDATE, ST_PLAN, ST_COUNT };

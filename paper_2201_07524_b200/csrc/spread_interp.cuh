@@ -217,7 +217,8 @@ inline int spread_dispatch(Plan& P, const NodeSet& S, const double* w, double* g
     return SK_OK;
 }
 
-inline int interp_dispatch(Plan& P, const NodeSet& S, const double* grid, double* t, cudaStream_t s) {
+inline int interp_dispatch(Plan& P, const NodeSet& S, const double* grid, double* t, cudaStream_t s,
+                           const FusedUpd& fu) {
     if (P.dmma && P.d == 2) {
         using C = Interp2Cfg;
         static bool attr = false;
@@ -227,7 +228,7 @@ inline int interp_dispatch(Plan& P, const NodeSet& S, const double* grid, double
         }
         if (S.nbatches > 0) {
             const int g = persistent_grid(interp2_dmma_kernel, C::NT, C::SMEM_BYTES, (S.nbatches + C::NWARP - 1) / C::NWARP);
-            interp2_dmma_kernel<<<g, C::NT, C::SMEM_BYTES, s>>>((const CellBatch*)S.batches, S.nbatches, S.taps, grid, P.n, t);
+            interp2_dmma_kernel<<<g, C::NT, C::SMEM_BYTES, s>>>((const CellBatch*)S.batches, S.nbatches, S.taps, grid, P.n, t, fu);
             count_launch();
         }
         cudaError_t e = cudaGetLastError();
@@ -248,7 +249,7 @@ inline int interp_dispatch(Plan& P, const NodeSet& S, const double* grid, double
             const auto kern = stage ? interp3_dmma_kernel<true> : interp3_dmma_kernel<false>;
             const size_t sm = stage ? C::SMEM_BYTES : C::SMEM_BYTES_NOSTAGE;
             const int g = persistent_grid(kern, C::NT, sm, (S.nbatches + C::NWARP - 1) / C::NWARP);
-            kern<<<g, C::NT, sm, s>>>((const CellBatch*)S.batches, S.nbatches, S.taps, grid, P.n, t);
+            kern<<<g, C::NT, sm, s>>>((const CellBatch*)S.batches, S.nbatches, S.taps, grid, P.n, t, fu);
             count_launch();
         }
         cudaError_t e = cudaGetLastError();
