@@ -68,18 +68,27 @@ __device__ __forceinline__ void prefetch_range(const void* p, long long bytes, i
 
 // ------------------------------------------------------------------------------ taps
 // out[node][a][t] = phi(f_a + m - 1 - t), f_a = frac(u_a), t < W (even/odd tap polynomials).
+// A warp stages its 32 nodes' rows in shared memory and writes them out as one contiguous,
+// coalesced block (32 * D * W doubles) instead of 32 scattered row stores.
 template <int D, int W>
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(128)
 taps_precompute_kernel(const double* __restrict__ u, long long count, const __grid_constant__ WinPoly wp,
                        double* __restrict__ out) {
+    constexpr int ROW = D * W;                       // doubles per node
     __shared__ __align__(16) double csm[(W / 2) * kCoefRow];
+    __shared__ __align__(16) double stage[4][32 * ROW];   // 128 threads: 4 warps
     load_coefs<W>(wp, csm);
     __syncthreads();
-    for (long long j = blockIdx.x * (long long)blockDim.x + threadIdx.x; j < count;
-         j += (long long)gridDim.x * blockDim.x) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    double* st = stage[warp];
+    const long long nwarps = (long long)gridDim.x * (blockDim.x >> 5);
+    for (long long base = (blockIdx.x * (long long)(blockDim.x >> 5) + warp) * 32; base < count;
+         base += nwarps * 32) {
+        const long long j = base + lane;
+        const int nvalid = (int)min(32LL, count - base);
 #pragma unroll 1
         for (int a = 0; a < D; ++a) {
-            const double uv = u[a * count + j];
+            const double uv = j < count ? u[a * count + j] : 0.5;
             const double g = uv - floor(uv) - 0.5, g2 = g * g;
             double v[W];
 #pragma unroll
@@ -93,10 +102,15 @@ taps_precompute_kernel(const double* __restrict__ u, long long count, const __gr
                 v[t] = fma(g, O, E);
                 v[W - 1 - t] = fma(-g, O, E);
             }
-            double2* o = reinterpret_cast<double2*>(out + (j * D + a) * W);
+            double2* o = reinterpret_cast<double2*>(st + lane * ROW + a * W);
 #pragma unroll
             for (int t = 0; t < W / 2; ++t) o[t] = make_double2(v[2 * t], v[2 * t + 1]);
         }
+        __syncwarp();
+        const double2* src = reinterpret_cast<const double2*>(st);
+        double2* dst = reinterpret_cast<double2*>(out + base * ROW);
+        for (int i = lane; i < nvalid * ROW / 2; i += 32) dst[i] = src[i];
+        __syncwarp();
     }
 }
 

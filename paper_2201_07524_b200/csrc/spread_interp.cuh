@@ -131,10 +131,10 @@ inline int interp3_launch(Plan& P, const NodeSet& S, const double* grid, double*
 inline int taps_dispatch(Plan& P, NodeSet& S, cudaStream_t s) {
     if (S.count <= 0) return SK_OK;
     const WinPoly& wp = *(const WinPoly*)P.winpoly;
-    long long g = (S.count + 255) / 256;
-    if (g > 148LL * 8) g = 148LL * 8;
-    if (P.d == 3) taps_precompute_kernel<3, 12><<<(int)g, 256, 0, s>>>(S.u, S.count, wp, S.taps);
-    else taps_precompute_kernel<2, 16><<<(int)g, 256, 0, s>>>(S.u, S.count, wp, S.taps);
+    long long g = (S.count + 127) / 128;
+    if (g > 148LL * 16) g = 148LL * 16;
+    if (P.d == 3) taps_precompute_kernel<3, 12><<<(int)g, 128, 0, s>>>(S.u, S.count, wp, S.taps);
+    else taps_precompute_kernel<2, 16><<<(int)g, 128, 0, s>>>(S.u, S.count, wp, S.taps);
     count_launch();
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return set_error(SK_ECUDA, std::string("taps: ") + cudaGetErrorString(e));
