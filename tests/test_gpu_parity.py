@@ -578,3 +578,58 @@ def test_independent_plans_interleaved(capi, ctx):
         u3 = capi.fastsum_apply(P3, dev(b3), 0, 0).cpu().numpy()
         u2 = capi.fastsum_apply(P2, dev(b2), 0, 0).cpu().numpy()
         assert rel_linf(u3, t3) <= 1e-13 and rel_linf(u2, t2) <= 1e-13
+
+
+# ------------------------------------------------------------------ randomized breadth
+_RAND_CASES = [(d, seed) for d in (1, 2, 3) for seed in range(4)]
+
+
+@pytest.mark.parametrize("d,seed", _RAND_CASES)
+def test_random_configs_match_method_statement(capi, ctx, d, seed):
+    """Seeded random plans (dimension, sizes with ragged tails, lambda, N, m_w, point
+    distributions) through every code path the plan may pick (v1 / tiled / DMMA spread and
+    interp, x-pair segments, pruned FFT): the GPU fast summation equals the oracle's statement of
+    the same method with exact NDFTs (nfft_ref.fastsum_ndft) to the window error, and the direct
+    sum to the method error, for both kernels and directions."""
+    from oracle import nfft_ref
+    rng = np.random.default_rng(1000 * d + seed)
+    n, m = int(rng.integers(1, 260)), int(rng.integers(1, 260))
+    N = int(rng.choice([16, 24, 32])) if d == 3 else int(rng.choice([16, 32, 48, 64]))
+    m_w = int(rng.choice([6, 8])) if 2 * N >= 32 else 6
+    lam = float(rng.uniform(5.0, 60.0))
+    lo = rng.uniform(-2, 2, size=d)
+    span = rng.uniform(0.2, 3.0)
+    x = lo + span * rng.random((n, d)) ** float(rng.uniform(0.5, 2.0))   # skewed densities
+    y = lo + span * rng.random((m, d))
+    wy, wx = rng.random(m), rng.random(n)
+    P = capi.Plan(ctx, dev(x), dev(y), lam / span ** 2, N, 2.0, m_w)
+    window = 1e-13 if m_w == 8 else 1e-9   # per-mode KB window error at sigma = 2 (G2/G3)
+    for kernel in (0, 1):
+        t = capi.fastsum_apply(P, dev(wy), 0, kernel).cpu().numpy()
+        tt = capi.fastsum_apply(P, dev(wx), 1, kernel).cpu().numpy()
+        ref = nfft_ref.fastsum_ndft(x, y, wy, lam / span ** 2, N, 1 / 16, 8, kernel)
+        reft = nfft_ref.fastsum_ndft(y, x, wx, lam / span ** 2, N, 1 / 16, 8, kernel)
+        assert rel_linf(t, ref) <= window * d and rel_linf(tt, reft) <= window * d, \
+            (d, n, m, N, m_w, kernel, rel_linf(t, ref), rel_linf(tt, reft))
+
+
+@pytest.mark.parametrize("d,seed", [(1, 0), (1, 1), (2, 0), (2, 1), (3, 0)])
+def test_random_r1_configs_match_method_statement(capi, ctx, d, seed):
+    """r = 1 plans with seeded random sizes, lambda, N and near-field radius: GPU = the oracle's
+    statement of the method (laplace_ref.fastsum_ndft) to the window error."""
+    from oracle import laplace_ref as LR
+    rng = np.random.default_rng(2000 + 10 * d + seed)
+    n, m = int(rng.integers(1, 200)), int(rng.integers(1, 200))
+    N = int(rng.choice([32, 64])) if d < 3 else 32
+    near = int(rng.choice([8, 12, 16]))
+    lam = float(rng.uniform(5.0, 40.0))
+    x, y = rng.random((n, d)), rng.random((m, d))
+    wy, wx = rng.random(m), rng.random(n)
+    P = capi.Plan(ctx, dev(x), dev(y), lam, N, 2.0, 8 if d < 3 else 6, 1 / 16, 8, r=1, near_cells=near)
+    window = 1e-12 if d < 3 else 1e-9
+    for kernel in (0, 1):
+        t = capi.fastsum_apply(P, dev(wy), 0, kernel).cpu().numpy()
+        tt = capi.fastsum_apply(P, dev(wx), 1, kernel).cpu().numpy()
+        ref = LR.fastsum_ndft(x, y, wy, lam, N, 1 / 16, 8, near, kernel=kernel)
+        reft = LR.fastsum_ndft(y, x, wx, lam, N, 1 / 16, 8, near, kernel=kernel)
+        assert rel_linf(t, ref) <= window and rel_linf(tt, reft) <= window, (d, n, m, N, near, kernel)
