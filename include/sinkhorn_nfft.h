@@ -52,8 +52,10 @@ typedef struct sk_plan* sk_plan_t;  /* owns: sorted node copies, permutations, g
 
 typedef struct {
     int       iters_done;        /* full iterations completed (1 iteration = u- then v-update) */
-    double    residual;          /* ||pi 1 - a||_1 + ||pi^T 1 - b||_1 at the last iteration (the
-                                    second term is 0 after a v-update); global over ranks */
+    double    residual;          /* ||pi 1 - a||_1 + ||pi^T 1 - b||_1 (Eq. (Error)) of the
+                                    iterate entering the last iteration's u-update, i.e. after the
+                                    previous v-update (the second term is 0 there);
+                                    global over ranks */
     int       bad_iter;          /* SK_ENONPOS: iteration of the first non-positive denominator */
     long long bad_index;         /* SK_ENONPOS: its caller-order index (local to the rank) */
     double    kappa_log10_est;   /* log10( ||v||_1 / min_i (K v)_i ) at the last u-update: the
