@@ -36,6 +36,15 @@ __device__ __forceinline__ void dmma884(double& c0, double& c1, double a, double
     asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
         : "+d"(c0), "+d"(c1) : "d"(a), "d"(b));
 }
+// m16n8k4: A rows g (a0) and g + 8 (a1), one B operand; C rows g (c0, c1) and g + 8 (c2, c3)
+__device__ __forceinline__ void dmma1684(double& c0, double& c1, double& c2, double& c3, double a0, double a1,
+                                         double b) {
+    asm("mma.sync.aligned.m16n8k4.row.col.f64.f64.f64.f64 {%0,%1,%2,%3}, {%4,%5}, {%6}, {%0,%1,%2,%3};"
+        : "+d"(c0), "+d"(c1), "+d"(c2), "+d"(c3) : "d"(a0), "d"(a1), "d"(b));
+}
+#ifndef SK_SPREAD_M16
+#define SK_SPREAD_M16 1
+#endif
 
 // Work unit of the interp: up to 32 nodes of one cell.
 struct CellBatch {
@@ -380,8 +389,12 @@ spread3_dmma_kernel(const SpreadItem* __restrict__ items, int nitems, const Cell
                     const int ty = (r3 == 0) ? 2 * k3 : ((r3 == 1) ? 2 * k3 + (g >= 4 ? 1 : 0) : 2 * k3 + 1);
                     const double yvv = (r3 == 1) ? (g >= 4 ? yv[2 * k3 + 1] : yv[2 * k3]) : yv[ty];
                     const double b = yvv * zv[r3];
+#if SK_SPREAD_M16
+                    dmma1684(acc[0][nt][0], acc[0][nt][1], acc[1][nt][0], acc[1][nt][1], a0, a1, b);
+#else
                     dmma884(acc[0][nt][0], acc[0][nt][1], a0, b);
                     dmma884(acc[1][nt][0], acc[1][nt][1], a1, b);
+#endif
                 }
             }
             // add the block (region rows 0..12, the cell's (oy, oz) columns) into the region
