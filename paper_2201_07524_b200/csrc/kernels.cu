@@ -128,20 +128,25 @@ struct ScaleParams {
     int Td;           // T^d
 };
 
+// x' = rho (x - centre), u = n (x' + 1/2): the one definition both the key and the gather use
+// (bit-identical u in both kernels)
+__device__ __forceinline__ double scaled_x(const ScaleParams& sp, double x, int a) {
+    return sp.rho * (x - sp.centre[a]);
+}
+__device__ __forceinline__ double grid_u(const ScaleParams& sp, double xs) { return sp.n * (xs + 0.5); }
+
 __global__ void scale_key_kernel(const double* __restrict__ pts, long long count, ScaleParams sp,
-                                 double* __restrict__ u_out, int* __restrict__ key,
-                                 int* __restrict__ idx, int* __restrict__ bad) {
+                                 int* __restrict__ key, int* __restrict__ idx, int* __restrict__ bad) {
     for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < count;
          i += (long long)gridDim.x * blockDim.x) {
         double r2 = 0.0;
         int k = 0, sub = 0;
         bool ok = true;
         for (int a = 0; a < sp.d; ++a) {
-            double xs = sp.rho * (pts[i * sp.d + a] - sp.centre[a]);
+            const double xs = scaled_x(sp, pts[i * sp.d + a], a);
             ok = ok && isfinite(xs);
             r2 += xs * xs;
-            double u = sp.n * (xs + 0.5);
-            u_out[a * count + i] = u;
+            const double u = grid_u(sp, xs);
             int c = (int)floor(u);
             int tc = c / sp.T;
             tc = tc < 0 ? 0 : (tc >= sp.tiles_per_axis ? sp.tiles_per_axis - 1 : tc);
@@ -160,9 +165,7 @@ __global__ void scale_key_kernel(const double* __restrict__ pts, long long count
     }
 }
 
-int launch_scale_key(Plan& P, const double* pts, long long count, double* u_unsorted, int* key,
-                     int* idx, int* bad, cudaStream_t s) {
-    if (count <= 0) return SK_OK;
+static ScaleParams scale_params(const Plan& P) {
     ScaleParams sp;
     for (int a = 0; a < kMaxD; ++a) sp.centre[a] = P.centre[a];
     sp.rho = P.rho;
@@ -176,25 +179,35 @@ int launch_scale_key(Plan& P, const double* pts, long long count, double* u_unso
     sp.xminor = P.spread_xpairs ? 1 : 0;
     sp.Td = 1;
     for (int a = 0; a < P.d; ++a) sp.Td *= P.tile_cells;
-    scale_key_kernel<<<grid_for(count, 256), 256, 0, s>>>(pts, count, sp, u_unsorted, key, idx, bad);
+    return sp;
+}
+
+int launch_scale_key(Plan& P, const double* pts, long long count, int* key, int* idx, int* bad,
+                     cudaStream_t s) {
+    if (count <= 0) return SK_OK;
+    const ScaleParams sp = scale_params(P);
+    scale_key_kernel<<<grid_for(count, 256), 256, 0, s>>>(pts, count, sp, key, idx, bad);
     SK_LAUNCH_CHECK();
     return SK_OK;
 }
 
-__global__ void gather_coords_kernel(const double* __restrict__ u_unsorted,
-                                     const int* __restrict__ perm, long long count, int d,
-                                     double* __restrict__ u_sorted) {
+// sorted SoA grid coordinates: gather the caller's row-major point (d contiguous doubles, one
+// or two sectors) and rescale it, instead of gathering d scattered doubles of a scaled copy
+// (ncu: the scattered gather moved 15x its useful bytes)
+__global__ void gather_coords_kernel(const double* __restrict__ pts, const int* __restrict__ perm,
+                                     long long count, ScaleParams sp, double* __restrict__ u_sorted) {
     for (long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x; k < count;
          k += (long long)gridDim.x * blockDim.x) {
-        long long i = perm[k];
-        for (int a = 0; a < d; ++a) u_sorted[a * count + k] = u_unsorted[a * count + i];
+        const long long i = perm[k];
+        for (int a = 0; a < sp.d; ++a) u_sorted[a * count + k] = grid_u(sp, scaled_x(sp, pts[i * sp.d + a], a));
     }
 }
 
-int launch_gather_coords(Plan& P, const double* u_unsorted, const int* perm, long long count,
-                         double* u_sorted, cudaStream_t s) {
+int launch_gather_coords(Plan& P, const double* pts, const int* perm, long long count, double* u_sorted,
+                         cudaStream_t s) {
     if (count <= 0) return SK_OK;
-    gather_coords_kernel<<<grid_for(count, 256), 256, 0, s>>>(u_unsorted, perm, count, P.d, u_sorted);
+    const ScaleParams sp = scale_params(P);
+    gather_coords_kernel<<<grid_for(count, 256), 256, 0, s>>>(pts, perm, count, sp, u_sorted);
     SK_LAUNCH_CHECK();
     return SK_OK;
 }

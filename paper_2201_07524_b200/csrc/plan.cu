@@ -481,9 +481,7 @@ static int plan_side(Plan& P, int sidx, const double* pts, long long count, cuda
         SK_CUDA(cudaMemsetAsync(S.tile_start, 0, sizeof(int) * (S.ntiles + 1), s));
         return SK_OK;
     }
-    double* u_uns = nullptr;
     int *key_in = nullptr, *idx_in = nullptr, *bad = nullptr;
-    SK_TRY(alloc((void**)&u_uns, sizeof(double) * P.d * count));
     SK_TRY(alloc((void**)&key_in, sizeof(int) * count));
     SK_TRY(alloc((void**)&idx_in, sizeof(int) * count));
     SK_TRY(alloc((void**)&bad, sizeof(int)));
@@ -493,13 +491,13 @@ static int plan_side(Plan& P, int sidx, const double* pts, long long count, cuda
     const int big = 0x7fffffff;
     SK_CUDA(cudaMemcpyAsync(bad, &big, sizeof(int), cudaMemcpyHostToDevice, s));
     plan_trace("side: alloc", s);
-    SK_TRY(launch_scale_key(P, pts, count, u_uns, key_in, idx_in, bad, s));
+    SK_TRY(launch_scale_key(P, pts, count, key_in, idx_in, bad, s));
     plan_trace("side: scale_key", s);
     int hbad = 0;
     SK_CUDA(cudaMemcpyAsync(&hbad, bad, sizeof(int), cudaMemcpyDeviceToHost, s));
     SK_CUDA(cudaStreamSynchronize(s));
     if (hbad != big) {
-        sk_free(u_uns); sk_free(key_in); sk_free(idx_in); sk_free(bad);
+        sk_free(key_in); sk_free(idx_in); sk_free(bad);
         return set_error(SK_EGEOMETRY, "node " + std::to_string(hbad) + " of side " + std::to_string(sidx) +
                                            " is non-finite or outside the ball |x'| <= 1/4 - eps_B/2");
     }
@@ -517,7 +515,7 @@ static int plan_side(Plan& P, int sidx, const double* pts, long long count, cuda
                                             0, end_bit, s));
     count_launch(4);
     plan_trace("side: sort", s);
-    SK_TRY(launch_gather_coords(P, u_uns, S.perm, count, S.u, s));
+    SK_TRY(launch_gather_coords(P, pts, S.perm, count, S.u, s));
     plan_trace("side: gather", s);
     if (P.dmma) {
         SK_TRY(build_cell_lists(P, S, s));
@@ -531,7 +529,6 @@ static int plan_side(Plan& P, int sidx, const double* pts, long long count, cuda
         if (P.tiled) SK_TRY(build_items(P, S, s));
     }
     sk_free(tmp);
-    sk_free(u_uns);
     sk_free(key_in);
     sk_free(idx_in);
     sk_free(bad);

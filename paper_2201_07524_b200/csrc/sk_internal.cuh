@@ -167,10 +167,10 @@ __device__ __forceinline__ void emit_t(double* __restrict__ t_out, const FusedUp
 // ---- kernels.cu launchers ----
 int launch_bbox(const double* pts, long long count, int d, double* out_minmax /*device [2*d]*/,
                 cudaStream_t s);
-int launch_scale_key(Plan& P, const double* pts, long long count, double* u_unsorted,
-                     int* key, int* idx, int* bad, cudaStream_t s);
-int launch_gather_coords(Plan& P, const double* u_unsorted, const int* perm, long long count,
-                         double* u_sorted, cudaStream_t s);
+int launch_scale_key(Plan& P, const double* pts, long long count, int* key, int* idx, int* bad,
+                     cudaStream_t s);
+int launch_gather_coords(Plan& P, const double* pts, const int* perm, long long count, double* u_sorted,
+                         cudaStream_t s);   // rescales the caller's points in sorted order
 int launch_tile_offsets(const int* sorted_keys, long long count, int ntiles, int* tile_start,
                         cudaStream_t s);
 int launch_spread(Plan& P, int side, const double* w_sorted, double* grid, cudaStream_t s);
