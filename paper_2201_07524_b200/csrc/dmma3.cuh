@@ -62,6 +62,7 @@ struct SpreadItem {
 };
 constexpr int kSegMax = 1024;
 constexpr int kSegHybrid = 128;   // spread3_hybrid_kernel segments (two passes, L2-resident taps)
+constexpr int kSegTmaMax = 64;     // spread3_tma_kernel segments (one TMA-staged buffer each)
 constexpr int kSpreadItemMax = 4096;
 
 #ifndef SK_WORKLIST_ONLY   // plan.cu only needs the work-list types above
@@ -569,6 +570,188 @@ spread3_hybrid_kernel(const SpreadItem* __restrict__ items, int nitems, const Ce
             }
         }
         __syncwarp();
+    }
+}
+
+// ------------------------------------------------------------------------------ spread (TMA pair)
+// Warp-pair hybrid spread fed by TMA: every segment (<= kSegTma nodes of one cell) is copied
+// into shared memory with two 1-D bulk copies (cp.async.bulk: its taps rows and its weights)
+// completing on an mbarrier, double-buffered so the next segment streams in while the pair
+// computes on this one. Both warps of the pair read the staged operands (warp h owns the
+// columns with ty in 6h .. 6h+5); rows tx 0..7 run as one DMMA m-tile, rows 8..11 on DFMA, so
+// no tensor-core row is padding. Accumulators carry across consecutive segments of one cell;
+// the region update (reduce-scatter + shared-memory add) happens when the cell changes.
+constexpr int kSegTma = 64;
+struct SpreadTCfg {
+    static constexpr int W = 12, S = W + 1, NT = 128, NWARP = NT / 32, NPAIR = NWARP / 2, NTH = 9;
+    static constexpr int TS = 3 * W;
+    static constexpr int REG = S * S * S;                      // 2197
+    static constexpr int REGP = REG + 1;                       // keep the buffers 16-byte aligned
+    static constexpr int TBUF = kSegTma * TS;                  // doubles per taps buffer
+    static constexpr int WBUF = kSegTma + 4;                   // weights (aligned superset)
+    static constexpr int PAIR = 2 + REGP + 2 * TBUF + 2 * WBUF; // doubles per pair
+    static constexpr size_t SMEM_BYTES = sizeof(double) * NPAIR * PAIR;
+};
+
+__device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void pair_barrier(int pair) { asm volatile("bar.sync %0, 64;" ::"r"(pair + 1) : "memory"); }
+__device__ __forceinline__ void mbar_init(unsigned long long* mb, unsigned count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(mb)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long* mb, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(mb)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* mb, unsigned parity) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra WAIT_%=;\n}" ::"r"(smem_u32(mb)), "r"(parity) : "memory");
+}
+__device__ __forceinline__ void tma_load_1d(void* dst, const void* src, unsigned bytes, unsigned long long* mb) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                 ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(mb)) : "memory");
+}
+
+__global__ void __launch_bounds__(128, 2)
+spread3_tma_kernel(const SpreadItem* __restrict__ items, int nitems, const CellBatch* __restrict__ segs,
+                   const double* __restrict__ taps, const double* __restrict__ w,
+                   double* __restrict__ grid, int n) {
+    using C = SpreadTCfg;
+    constexpr int W = C::W, S = C::S, m = W / 2, NTH = C::NTH, TS = C::TS;
+    extern __shared__ __align__(16) double smem[];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int pair = warp >> 1, half = warp & 1;
+    const int g = lane >> 2, q = lane & 3;
+    const int plane = half * 32 + lane;
+    double* base = smem + pair * C::PAIR;
+    unsigned long long* mbar = reinterpret_cast<unsigned long long*>(base);
+    double* REGm = base + 2;
+    double* TB0 = base + 2 + C::REGP;
+    double* WB0 = TB0 + 2 * C::TBUF;
+    const int ns = n / 2;
+    const int gp = blockIdx.x * C::NPAIR + pair, np = gridDim.x * C::NPAIR;
+    const int z1 = (8 + g) % W;
+    const bool producer = half == 0 && lane == 0;
+
+    if (producer) {
+        mbar_init(&mbar[0], 1);
+        mbar_init(&mbar[1], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    pair_barrier(pair);
+    auto issue = [&](int sg, int b) {   // producer: stream segment sg into buffer b
+        const CellBatch sq = segs[sg];
+        const long long st = sq.start;
+        const long long w0 = st & ~1LL, w1 = (st + sq.count + 1) & ~1LL;
+        const unsigned tbytes = (unsigned)sq.count * TS * 8u, wbytes = (unsigned)(w1 - w0) * 8u;
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // generic reads before async writes
+        mbar_expect_tx(&mbar[b], tbytes + wbytes);
+        tma_load_1d(TB0 + b * C::TBUF, taps + st * TS, tbytes, &mbar[b]);
+        tma_load_1d(WB0 + b * C::WBUF, w + w0, wbytes, &mbar[b]);
+    };
+    unsigned uses0 = 0, uses1 = 0;
+    int t = 0;
+    if (producer && gp < nitems) issue(items[gp].seg_begin, 0);
+
+    for (int ii = gp; ii < nitems; ii += np) {
+        const SpreadItem it = items[ii];
+        const int sz = it.stile % ns, sy = (it.stile / ns) % ns, sx = it.stile / ns / ns;
+        for (int i = plane; i < C::REG; i += 64) REGm[i] = 0.0;
+        double acc[NTH][2], acc2[4][NTH];
+        bool fresh = true;
+        for (int sg = it.seg_begin; sg < it.seg_end; ++sg, ++t) {
+            const int b = t & 1;
+            const CellBatch seg = segs[sg];
+            int nsg = -1;
+            if (sg + 1 < it.seg_end) nsg = sg + 1;
+            else if (ii + np < nitems) nsg = items[ii + np].seg_begin;
+            pair_barrier(pair);   // segment t-1 done by both warps: buffer b^1 is free
+            if (producer && nsg >= 0) issue(nsg, b ^ 1);
+            if (b == 0) { mbar_wait(&mbar[0], uses0 & 1u); ++uses0; }
+            else { mbar_wait(&mbar[1], uses1 & 1u); ++uses1; }
+            const double* T0 = TB0 + b * C::TBUF;
+            const double* W0 = WB0 + b * C::WBUF + (seg.start & 1LL);
+            const int cz = seg.cell % n, cy = (seg.cell / n) % n, cx = seg.cell / n / n;
+            const int ox = cx - 2 * sx, oy = cy - 2 * sy, oz = cz - 2 * sz;   // in {0,1}
+            if (fresh) {
+#pragma unroll
+                for (int j = 0; j < NTH; ++j) {
+                    acc[j][0] = acc[j][1] = 0.0;
+#pragma unroll
+                    for (int r = 0; r < 4; ++r) acc2[r][j] = 0.0;
+                }
+                fresh = false;
+            }
+            const int nks = (seg.count + 3) >> 2;
+#pragma unroll 1
+            for (int s = 0; s < nks; ++s) {
+                const int jr = 4 * s + q;
+                const bool ok = jr < seg.count;
+                const double* tr = T0 + (ok ? jr : 0) * TS;
+                const double wu = ok ? W0[jr] : 0.0;
+                const double a0 = wu * tr[g];                              // A[tx = g][k = q]
+                const double2 x8a = *reinterpret_cast<const double2*>(tr + 8);
+                const double2 x8b = *reinterpret_cast<const double2*>(tr + 10);
+                const double xr[4] = {wu * x8a.x, wu * x8a.y, wu * x8b.x, wu * x8b.y};
+                double yv[6];
+                {
+                    const double2* y2 = reinterpret_cast<const double2*>(tr + W + 6 * half);
+#pragma unroll
+                    for (int i = 0; i < 3; ++i) { const double2 v2 = y2[i]; yv[2 * i] = v2.x; yv[2 * i + 1] = v2.y; }
+                }
+                const double zv[3] = {tr[2 * W + g], tr[2 * W + z1], tr[2 * W + 4 + g]};
+#pragma unroll
+                for (int j = 0; j < NTH; ++j) {
+                    const int k3 = j / 3, r3 = j % 3;
+                    const double yvv = (r3 == 0) ? yv[2 * k3]
+                                     : ((r3 == 1) ? (g >= 4 ? yv[2 * k3 + 1] : yv[2 * k3]) : yv[2 * k3 + 1]);
+                    const double bb = yvv * zv[r3];
+                    dmma884(acc[j][0], acc[j][1], a0, bb);
+#pragma unroll
+                    for (int r = 0; r < 4; ++r) acc2[r][j] = fma(xr[r], bb, acc2[r][j]);
+                }
+            }
+            const bool flush_cell = (sg + 1 >= it.seg_end) || (segs[sg + 1].cell != seg.cell);
+            if (flush_cell) {
+                const bool hi2 = (q & 2) != 0, hi1 = (q & 1) != 0;
+                double* rx = REGm + (ox + g) * S * S + oy * S + oz;
+#pragma unroll
+                for (int j = 0; j < NTH; ++j)
+#pragma unroll
+                    for (int e = 0; e < 2; ++e) {
+                        const int col = 8 * (NTH * half + j) + 2 * q + e;
+                        rx[(col / W) * S + (col % W)] += acc[j][e];
+                    }
+                double* r8 = REGm + (ox + 8 + q) * S * S + oy * S + oz;
+#pragma unroll
+                for (int j = 0; j < NTH; ++j) {
+                    double keep[2];
+#pragma unroll
+                    for (int rr = 0; rr < 2; ++rr) {
+                        const double send = hi2 ? acc2[rr][j] : acc2[2 + rr][j];
+                        const double mine = hi2 ? acc2[2 + rr][j] : acc2[rr][j];
+                        keep[rr] = mine + __shfl_xor_sync(0xffffffffu, send, 2);
+                    }
+                    const double send = hi1 ? keep[0] : keep[1];
+                    const double mine = hi1 ? keep[1] : keep[0];
+                    const double fin = mine + __shfl_xor_sync(0xffffffffu, send, 1);
+                    const int col = 8 * (NTH * half + j) + g;
+                    r8[(col / W) * S + (col % W)] += fin;
+                }
+                fresh = true;
+            }
+        }
+        pair_barrier(pair);
+        const int gx0 = 2 * sx - (m - 1), gy0 = 2 * sy - (m - 1), gz0 = 2 * sz - (m - 1);
+        for (int i = plane; i < C::REG; i += 64) {
+            const double v = REGm[i];
+            if (v != 0.0) {
+                const int rz = i % S, rest = i / S, ry = rest % S, rxx = rest / S;
+                atomicAdd(&grid[((long long)(gx0 + rxx) * n + (gy0 + ry)) * n + (gz0 + rz)], v);
+            }
+        }
+        pair_barrier(pair);
     }
 }
 

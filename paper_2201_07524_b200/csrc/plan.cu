@@ -389,7 +389,7 @@ static int build_cell_lists(Plan& P, NodeSet& S, cudaStream_t s) {
     // spread work-unit size: enough items to keep ~4 per resident warp busy (148 SMs x 8
     // warps), at most kSpreadItemMax nodes (one region flush per item)
     const int item_max = (int)std::max(128LL, std::min((long long)kSpreadItemMax, count / 4736));
-    const int seg_max = std::min(P.spread_hybrid ? kSegHybrid : kSegMax, item_max);
+    const int seg_max = std::min(P.spread_tma ? kSegTmaMax : (P.spread_hybrid ? kSegHybrid : kSegMax), item_max);
 
     // run-length encode the sorted keys; 7 int arrays of nruns (<= count) entries
     int* buf = nullptr;
@@ -633,7 +633,9 @@ int build_plan(Ctx* ctx, Plan** out, int d, const double* x, long long n, const 
         // hybrid DMMA+DFMA spread (no padded rows): opt-in until it beats the padded kernel
         // (c5: 20.6 vs 15.5 ms under ncu, issue/latency-bound with 2 passes per segment)
         P->spread_hybrid = P->dmma && d == 3 && getenv("SK_SPREAD3_HYBRID") != nullptr;
-        P->spread_xpairs = P->dmma && d == 3 && !P->spread_hybrid && getenv("SK_NO_XPAIRS") == nullptr;
+        P->spread_tma = P->dmma && d == 3 && !P->spread_hybrid && getenv("SK_SPREAD3_TMA") != nullptr;
+        P->spread_xpairs = P->dmma && d == 3 && !P->spread_hybrid && !P->spread_tma &&
+                           getenv("SK_NO_XPAIRS") == nullptr;
     }
     P->tile_cells = P->dmma ? (d == 3 ? 2 : kSup2) : choose_tile(d, ng, P->tiled);
     P->tiles_per_axis = ng / P->tile_cells;
@@ -725,12 +727,14 @@ int build_plan(Ctx* ctx, Plan** out, int d, const double* x, long long n, const 
     // ---- scratch
     P->max_count = std::max(n, m);
     long long mc = std::max(P->max_count, 1LL);
-    if ((st = alloc((void**)&P->w_sorted, sizeof(double) * mc))) return fail(st);
+    // spread weights (w_sorted, u_s, v_s) carry 2 doubles of slack: the TMA spread copies
+    // 16-byte aligned ranges that may extend one element past either end
+    if ((st = alloc((void**)&P->w_sorted, sizeof(double) * (mc + 2)))) return fail(st);
     if ((st = alloc((void**)&P->t_sorted, sizeof(double) * mc))) return fail(st);
     if ((st = alloc((void**)&P->a_s, sizeof(double) * std::max(n, 1LL)))) return fail(st);
-    if ((st = alloc((void**)&P->u_s, sizeof(double) * std::max(n, 1LL)))) return fail(st);
+    if ((st = alloc((void**)&P->u_s, sizeof(double) * (std::max(n, 1LL) + 2)))) return fail(st);
     if ((st = alloc((void**)&P->b_s, sizeof(double) * std::max(m, 1LL)))) return fail(st);
-    if ((st = alloc((void**)&P->v_s, sizeof(double) * std::max(m, 1LL)))) return fail(st);
+    if ((st = alloc((void**)&P->v_s, sizeof(double) * (std::max(m, 1LL) + 2)))) return fail(st);
     P->box_exchange = ctx->world > 1 || getenv("SK_FORCE_BOX_EXCHANGE") != nullptr;
     if (P->box_exchange && (st = alloc((void**)&P->box_buf, sizeof(double) * std::max(P->box_size, 1LL))))
         return fail(st);
