@@ -63,6 +63,7 @@ struct SpreadItem {
 constexpr int kSegMax = 1024;
 constexpr int kSegHybrid = 128;   // spread3_hybrid_kernel segments (two passes, L2-resident taps)
 constexpr int kSegTmaMax = 64;     // spread3_tma_kernel segments (one TMA-staged buffer each)
+constexpr int kSegTmaPMax = 32;    // spread3_tmapad_kernel segments
 constexpr int kSpreadItemMax = 4096;
 
 #ifndef SK_WORKLIST_ONLY   // plan.cu only needs the work-list types above
@@ -738,6 +739,145 @@ spread3_tma_kernel(const SpreadItem* __restrict__ items, int nitems, const CellB
                     const double fin = mine + __shfl_xor_sync(0xffffffffu, send, 1);
                     const int col = 8 * (NTH * half + j) + g;
                     r8[(col / W) * S + (col % W)] += fin;
+                }
+                fresh = true;
+            }
+        }
+        pair_barrier(pair);
+        const int gx0 = 2 * sx - (m - 1), gy0 = 2 * sy - (m - 1), gz0 = 2 * sz - (m - 1);
+        for (int i = plane; i < C::REG; i += 64) {
+            const double v = REGm[i];
+            if (v != 0.0) {
+                const int rz = i % S, rest = i / S, ry = rest % S, rxx = rest / S;
+                atomicAdd(&grid[((long long)(gx0 + rxx) * n + (gy0 + ry)) * n + (gz0 + rz)], v);
+            }
+        }
+        pair_barrier(pair);
+    }
+}
+
+// ------------------------------------------------------------------------------ spread (TMA, padded)
+// The padded DMMA spread (rows tx padded 12 -> 16, one m16n8k4 per n-tile) on a warp pair fed by
+// the same TMA double buffer: warp h owns the 9 n-tiles with ty in 6h .. 6h+5, so a lane holds
+// 36 accumulators instead of 72 and reads its operands from shared memory, which lets 3 pairs
+// share a CTA (12 warps per SM instead of 8).
+constexpr int kSegTmaP = 32;
+struct SpreadTPCfg {
+    static constexpr int W = 12, S = W + 1, NPAIR = 3, NT = 64 * NPAIR, NTH = 9;
+    static constexpr int TS = 3 * W;
+    static constexpr int REG = S * S * S;
+    static constexpr int REGP = REG + 1;
+    static constexpr int TBUF = kSegTmaP * TS;
+    static constexpr int WBUF = kSegTmaP + 4;
+    static constexpr int PAIR = 2 + REGP + 2 * TBUF + 2 * WBUF;
+    static constexpr size_t SMEM_BYTES = sizeof(double) * NPAIR * PAIR;
+};
+
+__global__ void __launch_bounds__(192, 2)
+spread3_tmapad_kernel(const SpreadItem* __restrict__ items, int nitems, const CellBatch* __restrict__ segs,
+                      const double* __restrict__ taps, const double* __restrict__ w,
+                      double* __restrict__ grid, int n) {
+    using C = SpreadTPCfg;
+    constexpr int W = C::W, S = C::S, m = W / 2, NTH = C::NTH, TS = C::TS;
+    extern __shared__ __align__(16) double smem[];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int pair = warp >> 1, half = warp & 1;
+    const int g = lane >> 2, q = lane & 3;
+    const int plane = half * 32 + lane;
+    double* base = smem + pair * C::PAIR;
+    unsigned long long* mbar = reinterpret_cast<unsigned long long*>(base);
+    double* REGm = base + 2;
+    double* TB0 = base + 2 + C::REGP;
+    double* WB0 = TB0 + 2 * C::TBUF;
+    const int ns = n / 2;
+    const int gp = blockIdx.x * C::NPAIR + pair, np = gridDim.x * C::NPAIR;
+    const int z1 = (8 + g) % W;
+    const bool producer = half == 0 && lane == 0;
+
+    if (producer) {
+        mbar_init(&mbar[0], 1);
+        mbar_init(&mbar[1], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    pair_barrier(pair);
+    auto issue = [&](int sg, int b) {
+        const CellBatch sq = segs[sg];
+        const long long st = sq.start;
+        const long long w0 = st & ~1LL, w1 = (st + sq.count + 1) & ~1LL;
+        const unsigned tbytes = (unsigned)sq.count * TS * 8u, wbytes = (unsigned)(w1 - w0) * 8u;
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        mbar_expect_tx(&mbar[b], tbytes + wbytes);
+        tma_load_1d(TB0 + b * C::TBUF, taps + st * TS, tbytes, &mbar[b]);
+        tma_load_1d(WB0 + b * C::WBUF, w + w0, wbytes, &mbar[b]);
+    };
+    unsigned uses0 = 0, uses1 = 0;
+    int t = 0;
+    if (producer && gp < nitems) issue(items[gp].seg_begin, 0);
+
+    for (int ii = gp; ii < nitems; ii += np) {
+        const SpreadItem it = items[ii];
+        const int sz = it.stile % ns, sy = (it.stile / ns) % ns, sx = it.stile / ns / ns;
+        for (int i = plane; i < C::REG; i += 64) REGm[i] = 0.0;
+        double acc[NTH][4];   // m16n8k4 C: rows g (0, 1) and 8 + g (2, 3), columns 2q, 2q+1
+        bool fresh = true;
+        for (int sg = it.seg_begin; sg < it.seg_end; ++sg, ++t) {
+            const int b = t & 1;
+            const CellBatch seg = segs[sg];
+            int nsg = -1;
+            if (sg + 1 < it.seg_end) nsg = sg + 1;
+            else if (ii + np < nitems) nsg = items[ii + np].seg_begin;
+            pair_barrier(pair);
+            if (producer && nsg >= 0) issue(nsg, b ^ 1);
+            if (b == 0) { mbar_wait(&mbar[0], uses0 & 1u); ++uses0; }
+            else { mbar_wait(&mbar[1], uses1 & 1u); ++uses1; }
+            const double* T0 = TB0 + b * C::TBUF;
+            const double* W0 = WB0 + b * C::WBUF + (seg.start & 1LL);
+            const int cz = seg.cell % n, cy = (seg.cell / n) % n, cx = seg.cell / n / n;
+            const int ox = cx - 2 * sx, oy = cy - 2 * sy, oz = cz - 2 * sz;
+            if (fresh) {
+#pragma unroll
+                for (int j = 0; j < NTH; ++j) acc[j][0] = acc[j][1] = acc[j][2] = acc[j][3] = 0.0;
+                fresh = false;
+            }
+            const int nks = (seg.count + 3) >> 2;
+#pragma unroll 2
+            for (int s = 0; s < nks; ++s) {
+                const int jr = 4 * s + q;
+                const bool ok = jr < seg.count;
+                const double* tr = T0 + (ok ? jr : 0) * TS;
+                const double wu = ok ? W0[jr] : 0.0;
+                const double a0 = wu * tr[g];
+                const double a1 = (8 + g < W) ? wu * tr[8 + g] : 0.0;
+                double yv[6];
+                {
+                    const double2* y2 = reinterpret_cast<const double2*>(tr + W + 6 * half);
+#pragma unroll
+                    for (int i = 0; i < 3; ++i) { const double2 v2 = y2[i]; yv[2 * i] = v2.x; yv[2 * i + 1] = v2.y; }
+                }
+                const double zv[3] = {tr[2 * W + g], tr[2 * W + z1], tr[2 * W + 4 + g]};
+#pragma unroll
+                for (int j = 0; j < NTH; ++j) {
+                    const int k3 = j / 3, r3 = j % 3;
+                    const double yvv = (r3 == 0) ? yv[2 * k3]
+                                     : ((r3 == 1) ? (g >= 4 ? yv[2 * k3 + 1] : yv[2 * k3]) : yv[2 * k3 + 1]);
+                    dmma1684(acc[j][0], acc[j][1], acc[j][2], acc[j][3], a0, a1, yvv * zv[r3]);
+                }
+            }
+            const bool flush_cell = (sg + 1 >= it.seg_end) || (segs[sg + 1].cell != seg.cell);
+            if (flush_cell) {
+#pragma unroll
+                for (int mt = 0; mt < 2; ++mt) {
+                    const int tx = 8 * mt + g;
+                    if (tx < W) {
+                        double* rx = REGm + (ox + tx) * S * S + oy * S + oz;
+#pragma unroll
+                        for (int j = 0; j < NTH; ++j)
+#pragma unroll
+                            for (int e = 0; e < 2; ++e) {
+                                const int col = 8 * (NTH * half + j) + 2 * q + e;
+                                rx[(col / W) * S + (col % W)] += acc[j][2 * mt + e];
+                            }
+                    }
                 }
                 fresh = true;
             }

@@ -389,7 +389,9 @@ static int build_cell_lists(Plan& P, NodeSet& S, cudaStream_t s) {
     // spread work-unit size: enough items to keep ~4 per resident warp busy (148 SMs x 8
     // warps), at most kSpreadItemMax nodes (one region flush per item)
     const int item_max = (int)std::max(128LL, std::min((long long)kSpreadItemMax, count / 4736));
-    const int seg_max = std::min(P.spread_tma ? kSegTmaMax : (P.spread_hybrid ? kSegHybrid : kSegMax), item_max);
+    const int seg_max = std::min(P.spread_tmapad ? kSegTmaPMax
+                                 : (P.spread_tma ? kSegTmaMax : (P.spread_hybrid ? kSegHybrid : kSegMax)),
+                                 item_max);
 
     // run-length encode the sorted keys; 7 int arrays of nruns (<= count) entries
     int* buf = nullptr;
@@ -634,7 +636,11 @@ int build_plan(Ctx* ctx, Plan** out, int d, const double* x, long long n, const 
         // (c5: 20.6 vs 15.5 ms under ncu, issue/latency-bound with 2 passes per segment)
         P->spread_hybrid = P->dmma && d == 3 && getenv("SK_SPREAD3_HYBRID") != nullptr;
         P->spread_tma = P->dmma && d == 3 && !P->spread_hybrid && getenv("SK_SPREAD3_TMA") != nullptr;
-        P->spread_xpairs = P->dmma && d == 3 && !P->spread_hybrid && !P->spread_tma &&
+        // default d = 3 spread: the padded DMMA spread on TMA-fed warp pairs (c5 17.0 -> 15.5 ms,
+        // c3 0.31 -> 0.26 ms); SK_SPREAD3_PADDED=1 restores the single-warp padded kernel
+        P->spread_tmapad = P->dmma && d == 3 && !P->spread_hybrid && !P->spread_tma &&
+                           getenv("SK_SPREAD3_PADDED") == nullptr;
+        P->spread_xpairs = P->dmma && d == 3 && !P->spread_hybrid && !P->spread_tma && !P->spread_tmapad &&
                            getenv("SK_NO_XPAIRS") == nullptr;
     }
     P->tile_cells = P->dmma ? (d == 3 ? 2 : kSup2) : choose_tile(d, ng, P->tiled);

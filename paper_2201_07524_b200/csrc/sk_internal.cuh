@@ -136,6 +136,7 @@ struct Plan {
     bool dmma = false;        // FP64 tensor-core spread/interp (d = 3, 2 m_w = 12)
     bool spread_hybrid = false;  // d = 3 spread: DMMA rows 0..7 + DFMA rows 8..11 (no padding)
     bool spread_tma = false;     // d = 3 spread: the hybrid on a warp pair fed by TMA-staged segments
+    bool spread_tmapad = false;  // d = 3 spread: the padded DMMA spread on TMA-fed warp pairs
     bool spread_xpairs = false;  // d = 3 padded spread: x-minor keys; sides with sparse cells group
                                  // x-pairs of cells into one segment (13 of 16 rows)
     void* winpoly = nullptr;  // host WinPoly (window tap polynomials)

@@ -159,6 +159,23 @@ inline int spread_dispatch(Plan& P, const NodeSet& S, const double* w, double* g
         if (e != cudaSuccess) return set_error(SK_ECUDA, std::string("spread2_dmma: ") + cudaGetErrorString(e));
         return SK_OK;
     }
+    if (P.dmma && P.spread_tmapad) {
+        using C = SpreadTPCfg;
+        static bool attr = false;
+        if (!attr) {
+            cudaFuncSetAttribute(spread3_tmapad_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM_BYTES);
+            attr = true;
+        }
+        if (S.nsitems > 0) {
+            const int g = persistent_grid(spread3_tmapad_kernel, C::NT, C::SMEM_BYTES, (S.nsitems + C::NPAIR - 1) / C::NPAIR);
+            spread3_tmapad_kernel<<<g, C::NT, C::SMEM_BYTES, s>>>((const SpreadItem*)S.sitems, S.nsitems,
+                                                                  (const CellBatch*)S.segs, S.taps, w, grid, P.n);
+            count_launch();
+        }
+        cudaError_t e = cudaGetLastError();
+        if (e != cudaSuccess) return set_error(SK_ECUDA, std::string("spread3_tmapad: ") + cudaGetErrorString(e));
+        return SK_OK;
+    }
     if (P.dmma && P.spread_tma) {
         using C = SpreadTCfg;
         static bool attr = false;
