@@ -60,6 +60,10 @@ struct SpreadItem {
     int seg_end;
     int count;      // nodes
 };
+#ifndef SK_INTERP_NB
+#define SK_INTERP_NB 32
+#endif
+constexpr int kInterpBatch3 = SK_INTERP_NB;   // d = 3 interp batch (nodes of one cell per warp pass)
 constexpr int kSegMax = 1024;
 constexpr int kSegHybrid = 128;   // spread3_hybrid_kernel segments (two passes, L2-resident taps)
 constexpr int kSegTmaMax = 64;     // spread3_tma_kernel segments (one TMA-staged buffer each)
@@ -133,12 +137,16 @@ taps_precompute_kernel(const double* __restrict__ u, long long count, const __gr
 #define SK_INTERP3_KUNROLL 1
 #endif
 constexpr int kInterpKUnroll = SK_INTERP3_KUNROLL;
+#ifndef SK_INTERP_NT
+#define SK_INTERP_NT 128
+#endif
 struct InterpDCfg {
-    static constexpr int W = 12, KS = W / 4, NT = 128, NWARP = NT / 32, TS = 3 * W;
+    static constexpr int W = 12, KS = W / 4, NT = SK_INTERP_NT, NWARP = NT / 32, TS = 3 * W;
+    static constexpr int NB = kInterpBatch3, NTN = NB / 8;   // nodes / n-tiles per batch
     static constexpr int XS = W + 2;                          // phi_x row stride (doubles)
     static constexpr int GBLK = W * W * W;                    // the cell's 12^3 grid block
-    static constexpr size_t SMEM_BYTES = sizeof(double) * NWARP * (32 * XS + GBLK);   // STAGE
-    static constexpr size_t SMEM_BYTES_NOSTAGE = sizeof(double) * NWARP * 32 * XS;     // more L1
+    static constexpr size_t SMEM_BYTES = sizeof(double) * NWARP * (NB * XS + GBLK);   // STAGE
+    static constexpr size_t SMEM_BYTES_NOSTAGE = sizeof(double) * NWARP * NB * XS;     // more L1
 };
 
 __device__ __forceinline__ void cp_async8(void* smem_dst, const void* gmem_src) {
@@ -151,18 +159,18 @@ __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wai
 // there (pays when cells hold several batches: c5 interp 16.1 -> 14.2 ms); otherwise read them
 // through L1 straight from the grid.
 template <bool STAGE>
-__global__ void __launch_bounds__(128, SK_INTERP3_MINB)
+__global__ void __launch_bounds__(SK_INTERP_NT, SK_INTERP3_MINB)
 interp3_dmma_kernel(const CellBatch* __restrict__ batches, int nbatches, const double* __restrict__ taps,
                     const double* __restrict__ grid, int n, double* __restrict__ t_out, const FusedUpd fu) {
     using C = InterpDCfg;
-    constexpr int W = C::W, KS = C::KS, m = W / 2, TS = C::TS;
+    constexpr int W = C::W, KS = C::KS, m = W / 2, TS = C::TS, NB = C::NB, NTN = C::NTN;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int g = lane >> 2, q = lane & 3;
     const long long n2 = (long long)n * n;
     const int gw = blockIdx.x * C::NWARP + warp, nw = gridDim.x * C::NWARP;
     extern __shared__ __align__(16) double smem[];
-    double* XT = smem + warp * (STAGE ? 32 * C::XS + C::GBLK : 32 * C::XS);   // [node][XS] phi_x rows
-    double* GB = XT + 32 * C::XS;                          // [tx][ty][tz] grid block of the cell
+    double* XT = smem + warp * (STAGE ? NB * C::XS + C::GBLK : NB * C::XS);   // [node][XS] phi_x rows
+    double* GB = XT + NB * C::XS;                          // [tx][ty][tz] grid block of the cell
     int cur_cell = -1;
     // contiguous slice of the cell-sorted batch list per warp: consecutive batches of one
     // cell reuse its 12^3 grid block from L1, and the taps stream sequentially
@@ -191,9 +199,9 @@ interp3_dmma_kernel(const CellBatch* __restrict__ batches, int nbatches, const d
         if (bi + 1 < b_hi)   // next batch of this warp: stream its taps into L2
             prefetch_range(taps + (long long)Bnext.start * TS, (long long)Bnext.count * TS * 8, lane);
         // B fragments: phi_z of node 8 nt + g at tz = 4 s + q
-        double bf[KS][4];
+        double bf[KS][NTN];
 #pragma unroll
-        for (int nt = 0; nt < 4; ++nt) {
+        for (int nt = 0; nt < NTN; ++nt) {
             const double* tz = T0 + min(8 * nt + g, last) * TS + 2 * W;
 #pragma unroll
             for (int s = 0; s < KS; ++s) bf[s][nt] = __ldg(tz + 4 * s + q);
@@ -205,8 +213,8 @@ interp3_dmma_kernel(const CellBatch* __restrict__ batches, int nbatches, const d
         // 2k + 1 (r3 = 2, and r3 = 1 when g >= 4): accumulate phi_y * E per (node, tx) and apply
         // phi_x once per k with one 16-byte load of (phi_x[2k], phi_x[2k+1]).
         const int ty1 = (8 + g) % W, txo1 = (g >= 4) ? 1 : 0;
-        double yv[4][2][3];   // phi_y at ty = g, (8+g)%12, 4+g
-        {   // stage the batch's phi_x rows (lane = node) in this warp's shared table
+        double yv[NTN][2][3];   // phi_y at ty = g, (8+g)%12, 4+g
+        if (lane < NB) {   // stage the batch's phi_x rows (lane = node) in this warp's shared table
             const double2* src = reinterpret_cast<const double2*>(T0 + min(lane, last) * TS);
             double2* dst = reinterpret_cast<double2*>(XT + lane * C::XS);
 #pragma unroll
@@ -214,7 +222,7 @@ interp3_dmma_kernel(const CellBatch* __restrict__ batches, int nbatches, const d
         }
         __syncwarp();
 #pragma unroll
-        for (int nt = 0; nt < 4; ++nt)
+        for (int nt = 0; nt < NTN; ++nt)
 #pragma unroll
             for (int e = 0; e < 2; ++e) {
                 const double* tr = T0 + min(8 * nt + 2 * q + e, last) * TS;
@@ -222,9 +230,9 @@ interp3_dmma_kernel(const CellBatch* __restrict__ batches, int nbatches, const d
                 yv[nt][e][1] = __ldg(tr + W + ty1);
                 yv[nt][e][2] = __ldg(tr + W + 4 + g);
             }
-        double acc[4][2];
+        double acc[NTN][2];
 #pragma unroll
-        for (int nt = 0; nt < 4; ++nt) acc[nt][0] = acc[nt][1] = 0.0;
+        for (int nt = 0; nt < NTN; ++nt) acc[nt][0] = acc[nt][1] = 0.0;
         if (new_cell) cp_async_wait_all();
         __syncwarp();
         const double* Hb = STAGE ? GB + q
@@ -247,19 +255,19 @@ interp3_dmma_kernel(const CellBatch* __restrict__ batches, int nbatches, const d
 #pragma unroll
                 for (int s = 0; s < KS; ++s) a[r3][s] = STAGE ? Hrow[4 * s] : __ldg(Hrow + 4 * s);
             }
-            double d[3][4][2];
+            double d[3][NTN][2];
 #pragma unroll
             for (int r3 = 0; r3 < 3; ++r3)
 #pragma unroll
-                for (int nt = 0; nt < 4; ++nt) d[r3][nt][0] = d[r3][nt][1] = 0.0;
+                for (int nt = 0; nt < NTN; ++nt) d[r3][nt][0] = d[r3][nt][1] = 0.0;
 #pragma unroll
             for (int s = 0; s < KS; ++s)
 #pragma unroll
                 for (int r3 = 0; r3 < 3; ++r3)
 #pragma unroll
-                    for (int nt = 0; nt < 4; ++nt) dmma884(d[r3][nt][0], d[r3][nt][1], a[r3][s], bf[s][nt]);
+                    for (int nt = 0; nt < NTN; ++nt) dmma884(d[r3][nt][0], d[r3][nt][1], a[r3][s], bf[s][nt]);
 #pragma unroll
-            for (int nt = 0; nt < 4; ++nt)
+            for (int nt = 0; nt < NTN; ++nt)
 #pragma unroll
                 for (int e = 0; e < 2; ++e) {
                     // phi_x[2k], phi_x[2k+1] of the node in one 16-byte load
@@ -272,7 +280,7 @@ interp3_dmma_kernel(const CellBatch* __restrict__ batches, int nbatches, const d
         }
         // sum over the 8 rows g held by lanes q, q+4, ..., q+28
 #pragma unroll
-        for (int nt = 0; nt < 4; ++nt)
+        for (int nt = 0; nt < NTN; ++nt)
 #pragma unroll
             for (int e = 0; e < 2; ++e) {
                 double v = acc[nt][e];
@@ -286,12 +294,12 @@ interp3_dmma_kernel(const CellBatch* __restrict__ batches, int nbatches, const d
         {
             double v = acc[0][0];
 #pragma unroll
-            for (int nt = 0; nt < 4; ++nt)
+            for (int nt = 0; nt < NTN; ++nt)
 #pragma unroll
                 for (int e = 0; e < 2; ++e)
                     if (g == 2 * nt + e) v = acc[nt][e];
             const int p = 8 * (g >> 1) + 2 * q + (g & 1);
-            if (p < B.count) emit_t(t_out, fu, B.start + p, v);
+            if ((g >> 1) < NTN && p < B.count) emit_t(t_out, fu, B.start + p, v);
         }
         __syncwarp();   // XT is rewritten by the next batch
     }

@@ -305,11 +305,11 @@ __device__ __forceinline__ int spread_group(const int* __restrict__ keys, const 
 // per run: interp batches; per tile-head run: number of segs / items of its tile (greedy
 // fill in run order, exactly the sequential rule)
 __global__ void cell_counts_kernel(const int* __restrict__ keys, const int* __restrict__ cnts, int nruns,
-                                   CellGeom g, int seg_max, int item_max, int* __restrict__ nb,
+                                   CellGeom g, int seg_max, int item_max, int bmax, int* __restrict__ nb,
                                    int* __restrict__ nseg, int* __restrict__ nitem) {
     const int r = blockIdx.x * blockDim.x + threadIdx.x;
     if (r >= nruns) return;
-    nb[r] = (cnts[r] + 31) / 32;
+    nb[r] = (cnts[r] + bmax - 1) / bmax;
     const int tile = keys[r] / g.Td;
     int ns = 0, ni = 0;
     if (r == 0 || keys[r - 1] / g.Td != tile) {
@@ -331,7 +331,7 @@ __global__ void cell_counts_kernel(const int* __restrict__ keys, const int* __re
 
 __global__ void cell_write_kernel(const int* __restrict__ keys, const int* __restrict__ cnts,
                                   const int* __restrict__ rstart, int nruns, CellGeom g, int seg_max,
-                                  int item_max, const int* __restrict__ nb_off, const int* __restrict__ seg_off,
+                                  int item_max, int bmax, const int* __restrict__ nb_off, const int* __restrict__ seg_off,
                                   const int* __restrict__ item_off, CellBatch* __restrict__ batches,
                                   CellBatch* __restrict__ segs, SpreadItem* __restrict__ items,
                                   int* __restrict__ item_cnt) {
@@ -339,7 +339,7 @@ __global__ void cell_write_kernel(const int* __restrict__ keys, const int* __res
     if (r >= nruns) return;
     const int cell = cell_of_key(keys[r], g), cnt = cnts[r], st = rstart[r];
     int o = nb_off[r];
-    for (int b = 0; b < cnt; b += 32) batches[o++] = CellBatch{cell, st + b, min(32, cnt - b), 0};
+    for (int b = 0; b < cnt; b += bmax) batches[o++] = CellBatch{cell, st + b, min(bmax, cnt - b), 0};
     const int tile = keys[r] / g.Td;
     if (!(r == 0 || keys[r - 1] / g.Td != tile)) return;
     int so = seg_off[r], io = item_off[r] - 1, fill = 0;
@@ -413,7 +413,8 @@ static int build_cell_lists(Plan& P, NodeSet& S, cudaStream_t s) {
     S.xpairs = P.spread_xpairs && (long long)kXPairMaxDensity * nruns > count;
     g.xpairs = S.xpairs ? 1 : 0;
     SK_CUDA(cub::DeviceScan::ExclusiveSum(tmp, tb, cnts, rstart, nruns, s));
-    cell_counts_kernel<<<blk, thr, 0, s>>>(keys, cnts, nruns, g, seg_max, item_max, nb, nseg, nitem);
+    const int bmax = d == 3 ? kInterpBatch3 : 32;   // interp batch: nodes of one cell per warp pass
+    cell_counts_kernel<<<blk, thr, 0, s>>>(keys, cnts, nruns, g, seg_max, item_max, bmax, nb, nseg, nitem);
     SK_CUDA(cudaGetLastError());
     // totals = last exclusive prefix + last count (in-place scans)
     int last[3];
@@ -445,7 +446,7 @@ static int build_cell_lists(Plan& P, NodeSet& S, cudaStream_t s) {
     SK_TRY(alloc((void**)&icnt_sorted, sizeof(int) * 3 * std::max(S.nsitems, 1)));
     ord = icnt_sorted + std::max(S.nsitems, 1);
     ord_sorted = ord + std::max(S.nsitems, 1);
-    cell_write_kernel<<<blk, thr, 0, s>>>(keys, cnts, rstart, nruns, g, seg_max, item_max, nb, nseg, nitem,
+    cell_write_kernel<<<blk, thr, 0, s>>>(keys, cnts, rstart, nruns, g, seg_max, item_max, bmax, nb, nseg, nitem,
                                           (CellBatch*)S.batches, (CellBatch*)S.segs, items_unsorted, icnt);
     SK_CUDA(cudaGetLastError());
     count_launch(2);
