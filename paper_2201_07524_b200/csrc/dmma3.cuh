@@ -63,11 +63,14 @@ struct SpreadItem {
 #ifndef SK_INTERP_NB
 #define SK_INTERP_NB 32
 #endif
+#ifndef SK_TP_SEG_MAX
+#define SK_TP_SEG_MAX 32
+#endif
 constexpr int kInterpBatch3 = SK_INTERP_NB;   // d = 3 interp batch (nodes of one cell per warp pass)
 constexpr int kSegMax = 1024;
 constexpr int kSegHybrid = 128;   // spread3_hybrid_kernel segments (two passes, L2-resident taps)
 constexpr int kSegTmaMax = 64;     // spread3_tma_kernel segments (one TMA-staged buffer each)
-constexpr int kSegTmaPMax = 32;    // spread3_tmapad_kernel segments
+constexpr int kSegTmaPMax = SK_TP_SEG_MAX;   // spread3_tmapad_kernel segments
 constexpr int kSpreadItemMax = 4096;
 
 #ifndef SK_WORKLIST_ONLY   // plan.cu only needs the work-list types above
@@ -769,9 +772,15 @@ spread3_tma_kernel(const SpreadItem* __restrict__ items, int nitems, const CellB
 // the same TMA double buffer: warp h owns the 9 n-tiles with ty in 6h .. 6h+5, so a lane holds
 // 36 accumulators instead of 72 and reads its operands from shared memory, which lets 3 pairs
 // share a CTA (12 warps per SM instead of 8).
-constexpr int kSegTmaP = 32;
+#ifndef SK_TP_SEG
+#define SK_TP_SEG 32
+#endif
+#ifndef SK_TP_NPAIR
+#define SK_TP_NPAIR 3
+#endif
+constexpr int kSegTmaP = SK_TP_SEG;
 struct SpreadTPCfg {
-    static constexpr int W = 12, S = W + 1, NPAIR = 3, NT = 64 * NPAIR, NTH = 9;
+    static constexpr int W = 12, S = W + 1, NPAIR = SK_TP_NPAIR, NT = 64 * NPAIR, NTH = 9;
     static constexpr int TS = 3 * W;
     static constexpr int REG = S * S * S;
     static constexpr int REGP = REG + 1;
@@ -781,7 +790,7 @@ struct SpreadTPCfg {
     static constexpr size_t SMEM_BYTES = sizeof(double) * NPAIR * PAIR;
 };
 
-__global__ void __launch_bounds__(192, 2)
+__global__ void __launch_bounds__(64 * SK_TP_NPAIR, 2)
 spread3_tmapad_kernel(const SpreadItem* __restrict__ items, int nitems, const CellBatch* __restrict__ segs,
                       const double* __restrict__ taps, const double* __restrict__ w,
                       double* __restrict__ grid, int n) {
