@@ -344,6 +344,16 @@ def main():
     bytes_alg = pts_per_launch * 8 * (cfg.d + 1) + (cfg.N * cfg.sigma) ** cfg.d * 8
     step_ms = total_ms / args.steps
     stage_share = {s: round(v[1] / prof_step_ms, 4) for s, v in stage_ms.items()} if prof_step_ms else {}
+    G = (cfg.N * cfg.sigma) ** cfg.d
+    n_avg = (cfg.n + cfg.m) / 2 / world
+    alg_bytes = {"spread": n_avg * (cfg.d + 1) * 8 + G * 8, "interp": G * 8 + n_avg * (8 * cfg.d + 24),
+                 "fft_fwd": 2 * G * 8, "fft_inv": 2 * G * 8}
+    stage_hbm = {}
+    for st_name, by in alg_bytes.items():
+        c_, ms_ = stage_ms.get(st_name, (0, 0.0))
+        if c_ > 0 and ms_ > 0:
+            stage_hbm[st_name] = {"alg_bytes_per_launch": by, "avg_launch_ms": ms_ / c_,
+                                  "frac": by / (ms_ / c_ * 1e-3) / (pk["hbm_gbs"] * 1e9)}
     traffic, traffic_src = None, None
     try:
         with open(os.path.join(ROOT, "profiles", "traffic.json")) as fh:
@@ -391,6 +401,11 @@ def main():
                           "stage_ms": {s: v[1] for s, v in stage_ms.items()},
                           "launches": {s: v[0] for s, v in stage_ms.items()}},
         "stage_share_of_step": stage_share,
+        # SURVEY §8(d) per-stage HBM fraction (BJ metric "% HBM roofline for the spread, FFT and
+        # interpolate stages"): algorithmic bytes per launch / measured launch time / HBM peak.
+        # spread: n_s (d+1) 8 + G 8; interp: G 8 + n_t (8d + 24); FFT: 2 G 8 per transform (full
+        # grid; the pruned d = 3 path moves less than this definition charges)
+        "stage_hbm_frac": stage_hbm,
         "gpu_launches": int(launches),
         "clocks": clk,
         "divergence": {"s_dual": results[0], "s_cost": results[1]} if results else None,
