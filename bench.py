@@ -114,6 +114,16 @@ class ClockSampler:
 
 
 # ---------------------------------------------------------------------------- CPU oracle
+def cpu_model() -> str:
+    try:
+        for ln in open("/proc/cpuinfo"):
+            if ln.startswith("model name"):
+                return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
 def cpu_oracle_rate(cfg, budget_s: float):
     """Time the oracle (dense log-domain Alg. 1, as it stands) on a bounded seeded subsample
     of the workload; return (it/s extrapolated to the full workload, description)."""
@@ -171,7 +181,8 @@ def run_reference(args):
         "ms_per_step": 1e3 * cfg.iters / value, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic", "config": {"workload": cfg.name, "n": cfg.n, "m": cfg.m, "d": cfg.d,
                                         "lambda": cfg.lam, "N": cfg.N, "iters": cfg.iters},
-        "cpu_baseline": {"value": value, "unit": "it/s", "cores": cores, "kind": "oracle", "sample": descs[-1]},
+        "cpu_baseline": {"value": value, "unit": "it/s", "cores": cores, "kind": "oracle", "sample": descs[-1],
+                         "cpu_model": cpu_model(), "nproc": os.cpu_count()},
         "e2e": {"value": value, "unit": "it/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line))
@@ -418,7 +429,8 @@ def main():
         line["e2e"] = e2e
     if rank == 0 and not args.no_cpu_baseline:
         v, desc, cores, _ = cpu_oracle_rate(cfg, args.cpu_seconds)
-        line["cpu_baseline"] = {"value": v, "unit": "it/s", "cores": cores, "kind": "oracle", "sample": desc}
+        line["cpu_baseline"] = {"value": v, "unit": "it/s", "cores": cores, "kind": "oracle", "sample": desc,
+                                "cpu_model": cpu_model(), "nproc": os.cpu_count()}
     if rank == 0:
         print(json.dumps(line), flush=True)
     ctx.close()
