@@ -33,6 +33,7 @@ import numpy as np  # noqa: E402
 from synthetic import get, make_inputs, shard_range  # noqa: E402
 
 DEFAULT_CONFIG = os.environ.get("SK_BENCH_CONFIG", "c5")
+ORACLE_PAIRS_PER_S = None   # set by cpu_oracle_rate
 SMI_MS = int(os.environ.get("SK_BENCH_SMI_MS", "200"))          # clock sampling period
 STAGE_PROFILE = os.environ.get("SK_BENCH_STAGE_PROFILE", "1") != "0"
 FP64_FMA_PER_CLK_PER_SM = 64      # B200 FP64 vector rate
@@ -151,6 +152,12 @@ def cpu_oracle_rate(cfg, budget_s: float):
     dt = time.perf_counter() - t0
     rate_sample = iters / dt
     rate_full = rate_sample * (ks * ks) / (cfg.n * cfg.m)
+    # oracle direct-sum throughput (pair evaluations/s of the matvec checks)
+    kr = min(512, xs.shape[0])
+    t0 = time.perf_counter()
+    dense.direct_sum(xs[:kr], ys, bs, cfg.lam, 0)
+    global ORACLE_PAIRS_PER_S
+    ORACLE_PAIRS_PER_S = kr * ys.shape[0] / (time.perf_counter() - t0)
     desc = (f"{iters} log-domain Alg. 1 iterations on the first {ks}+{ks} points of {cfg.name} "
             f"({dt:.1f} s); value = sample it/s x ({ks}*{ks})/({cfg.n}*{cfg.m}) (quadratic extrapolation "
             f"to the full workload)")
@@ -182,7 +189,8 @@ def run_reference(args):
         "data": "synthetic", "config": {"workload": cfg.name, "n": cfg.n, "m": cfg.m, "d": cfg.d,
                                         "lambda": cfg.lam, "N": cfg.N, "iters": cfg.iters},
         "cpu_baseline": {"value": value, "unit": "it/s", "cores": cores, "kind": "oracle", "sample": descs[-1],
-                         "cpu_model": cpu_model(), "nproc": os.cpu_count()},
+                         "cpu_model": cpu_model(), "nproc": os.cpu_count(),
+                         "direct_sum_pair_evals_per_s": ORACLE_PAIRS_PER_S},
         "e2e": {"value": value, "unit": "it/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line))
@@ -430,7 +438,8 @@ def main():
     if rank == 0 and not args.no_cpu_baseline:
         v, desc, cores, _ = cpu_oracle_rate(cfg, args.cpu_seconds)
         line["cpu_baseline"] = {"value": v, "unit": "it/s", "cores": cores, "kind": "oracle", "sample": desc,
-                                "cpu_model": cpu_model(), "nproc": os.cpu_count()}
+                                "cpu_model": cpu_model(), "nproc": os.cpu_count(),
+                                "direct_sum_pair_evals_per_s": ORACLE_PAIRS_PER_S}
     if rank == 0:
         print(json.dumps(line), flush=True)
     ctx.close()
