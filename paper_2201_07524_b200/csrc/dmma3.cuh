@@ -140,6 +140,9 @@ taps_precompute_kernel(const double* __restrict__ u, long long count, const __gr
 #define SK_INTERP3_KUNROLL 1
 #endif
 constexpr int kInterpKUnroll = SK_INTERP3_KUNROLL;
+#ifndef SK_INTERP3_ACCTY
+#define SK_INTERP3_ACCTY 1
+#endif
 #ifndef SK_INTERP_NT
 #define SK_INTERP_NT 128
 #endif
@@ -216,7 +219,9 @@ interp3_dmma_kernel(const CellBatch* __restrict__ batches, int nbatches, const d
         // 2k + 1 (r3 = 2, and r3 = 1 when g >= 4): accumulate phi_y * E per (node, tx) and apply
         // phi_x once per k with one 16-byte load of (phi_x[2k], phi_x[2k+1]).
         const int ty1 = (8 + g) % W, txo1 = (g >= 4) ? 1 : 0;
+#if !SK_INTERP3_ACCTY
         double yv[NTN][2][3];   // phi_y at ty = g, (8+g)%12, 4+g
+#endif
         if (lane < NB) {   // stage the batch's phi_x rows (lane = node) in this warp's shared table
             const double2* src = reinterpret_cast<const double2*>(T0 + min(lane, last) * TS);
             double2* dst = reinterpret_cast<double2*>(XT + lane * C::XS);
@@ -224,6 +229,15 @@ interp3_dmma_kernel(const CellBatch* __restrict__ batches, int nbatches, const d
             for (int i = 0; i < W / 2; ++i) dst[i] = __ldg(src + i);
         }
         __syncwarp();
+#if SK_INTERP3_ACCTY
+        // per (node, ty) partial sums over tx: phi_y is applied once after the k loop, so each
+        // E value costs one DFMA in the loop (24 per k-step instead of 40)
+        double acc3[NTN][2][3];
+#pragma unroll
+        for (int nt = 0; nt < NTN; ++nt)
+#pragma unroll
+            for (int e = 0; e < 2; ++e) acc3[nt][e][0] = acc3[nt][e][1] = acc3[nt][e][2] = 0.0;
+#else
 #pragma unroll
         for (int nt = 0; nt < NTN; ++nt)
 #pragma unroll
@@ -233,6 +247,7 @@ interp3_dmma_kernel(const CellBatch* __restrict__ batches, int nbatches, const d
                 yv[nt][e][1] = __ldg(tr + W + ty1);
                 yv[nt][e][2] = __ldg(tr + W + 4 + g);
             }
+#endif
         double acc[NTN][2];
 #pragma unroll
         for (int nt = 0; nt < NTN; ++nt) acc[nt][0] = acc[nt][1] = 0.0;
@@ -275,12 +290,28 @@ interp3_dmma_kernel(const CellBatch* __restrict__ batches, int nbatches, const d
                 for (int e = 0; e < 2; ++e) {
                     // phi_x[2k], phi_x[2k+1] of the node in one 16-byte load
                     const double2 xx = reinterpret_cast<const double2*>(XT + (8 * nt + 2 * q + e) * C::XS)[k];
+#if SK_INTERP3_ACCTY
+                    acc3[nt][e][0] = fma(xx.x, d[0][nt][e], acc3[nt][e][0]);
+                    acc3[nt][e][1] = fma(txo1 ? xx.y : xx.x, d[1][nt][e], acc3[nt][e][1]);
+                    acc3[nt][e][2] = fma(xx.y, d[2][nt][e], acc3[nt][e][2]);
+#else
                     const double t1 = yv[nt][e][1] * d[1][nt][e];
                     const double sa = fma(yv[nt][e][0], d[0][nt][e], txo1 ? 0.0 : t1);
                     const double sb = fma(yv[nt][e][2], d[2][nt][e], txo1 ? t1 : 0.0);
                     acc[nt][e] = fma(xx.x, sa, fma(xx.y, sb, acc[nt][e]));
+#endif
                 }
         }
+#if SK_INTERP3_ACCTY
+#pragma unroll
+        for (int nt = 0; nt < NTN; ++nt)
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+                const double* tr = T0 + min(8 * nt + 2 * q + e, last) * TS + W;
+                acc[nt][e] = fma(__ldg(tr + g), acc3[nt][e][0],
+                                 fma(__ldg(tr + ty1), acc3[nt][e][1], __ldg(tr + 4 + g) * acc3[nt][e][2]));
+            }
+#endif
         // sum over the 8 rows g held by lanes q, q+4, ..., q+28
 #pragma unroll
         for (int nt = 0; nt < NTN; ++nt)
