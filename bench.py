@@ -51,6 +51,9 @@ def parse():
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--cpu-seconds", type=float, default=15.0, help="budget of the cpu_baseline sample")
+    p.add_argument("--nccl-self", action="store_true",
+                   help="N=1 through a one-rank NCCL communicator: the box exchange and scalar sums "
+                        "run through ncclAllReduce as on N>1 (checks and times the multi-GPU path)")
     return p.parse_args()
 
 
@@ -222,7 +225,12 @@ def main():
     dev = lambda z: torch.from_numpy(z).cuda()  # noqa: E731
     dx, dy, da, db = dev(hx), dev(hy), dev(ha), dev(hb)
     stream = torch.cuda.current_stream()
-    ctx = capi.init_distributed_context(local, stream) if world > 1 else capi.Context(local, stream=stream)
+    if world > 1:
+        ctx = capi.init_distributed_context(local, stream)
+    elif args.nccl_self:
+        ctx = capi.Context(local, 0, 1, capi.sk_nccl_unique_id(), stream)
+    else:
+        ctx = capi.Context(local, stream=stream)
     solve = lambda: capi.sinkhorn_solve(ctx, dx, dy, da, db, cfg.lam, cfg.N, cfg.sigma, cfg.m_w,  # noqa: E731
                                         cfg.eps_B, cfg.p, cfg.iters)
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")   # 256 MB > L2
@@ -389,7 +397,8 @@ def main():
         "config": {"workload": cfg.name, "n": cfg.n, "m": cfg.m, "d": cfg.d, "lambda": cfg.lam, "N": cfg.N,
                    "sigma": cfg.sigma, "m_w": cfg.m_w, "eps_B": cfg.eps_B, "iters_per_step": cfg.iters,
                    "step": "plan + iters x (K v, K^T u) + divergence (2 applies)",
-                   "parallelism": f"dp{world} (point shards + grid all-reduce)",
+                   "parallelism": f"dp{world} (point shards + grid all-reduce)"
+                                  + (", one-rank NCCL communicator" if args.nccl_self and world == 1 else ""),
                    "l2": "256 MB buffer written between timed steps"},
         "fastsum_point_evals_per_s": point_evals,   # all n targets of one K v, max-over-ranks time
         "fastsum_apply_ms": apply_ms,

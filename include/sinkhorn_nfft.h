@@ -66,7 +66,10 @@ typedef struct {
 
 /* Create a context on `device` (the current CUDA device is switched to it). rank/world_size
  * describe the SPMD job; nccl_unique_id: 128-byte ncclUniqueId (host) from
- * sk_nccl_unique_id() on rank 0, broadcast by the caller; NULL iff world_size == 1.
+ * sk_nccl_unique_id() on rank 0, broadcast by the caller; required when world_size > 1. With
+ * world_size == 1 it may be NULL (no communicator) or an id, which creates a one-rank NCCL
+ * communicator: every collective (bbox min/max, box exchange, scalar sums) then runs through
+ * NCCL as the identity, i.e. the multi-rank NCCL code path on one GPU.
  * cuda_stream: cudaStream_t to enqueue on (NULL = legacy default stream).
  * Test hook: with world_size == 1 and the environment variable SK_EMULATE_WORLD=k (k >= 2) the
  * context behaves as k ranks holding identical shards (every sum over ranks is k times the

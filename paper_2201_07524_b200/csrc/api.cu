@@ -147,9 +147,12 @@ static int nccl_load() {
 
 // Emulated world (SK_EMULATE_WORLD=k on a one-process context): k ranks that hold identical
 // shards, so a sum over ranks is k times the local value and min/max are the local ones.
+// A one-rank NCCL communicator (world_size 1 with an ncclUniqueId) runs every collective
+// through NCCL as the identity.
 int allreduce_sum(Ctx* c, double* buf, long long count) {
-    if (c->world <= 1 || count <= 0) return SK_OK;
+    if (count <= 0) return SK_OK;
     if (c->emulated) return launch_scale_const(buf, count, (double)c->world, c->stream);
+    if (!c->nccl_comm) return SK_OK;   // one rank, no communicator
     SK_NCCL(g_nccl.allReduce(buf, buf, (size_t)count, ncclFloat64, ncclSum, (ncclComm_t)c->nccl_comm,
                              c->stream));
     count_launch();
@@ -157,7 +160,7 @@ int allreduce_sum(Ctx* c, double* buf, long long count) {
 }
 
 int allreduce_minmax(Ctx* c, double* mins, double* maxs, int count) {
-    if (c->world <= 1 || count <= 0 || c->emulated) return SK_OK;
+    if (count <= 0 || c->emulated || !c->nccl_comm) return SK_OK;
     SK_NCCL(g_nccl.allReduce(mins, mins, (size_t)count, ncclFloat64, ncclMin, (ncclComm_t)c->nccl_comm,
                              c->stream));
     SK_NCCL(g_nccl.allReduce(maxs, maxs, (size_t)count, ncclFloat64, ncclMax, (ncclComm_t)c->nccl_comm,
@@ -275,14 +278,14 @@ int sinkhorn_init(sk_ctx_t* ctx, int device, int rank, int world_size, const voi
     c->c.rank = rank;
     c->c.world = world_size;
     c->c.stream = (cudaStream_t)cuda_stream;
-    if (world_size == 1) {
+    if (world_size == 1 && !nccl_unique_id) {
         const char* ew = getenv("SK_EMULATE_WORLD");
         if (ew && atoi(ew) > 1) {   // test hook, see allreduce_sum
             c->c.world = atoi(ew);
             c->c.emulated = true;
         }
     }
-    if (world_size > 1) {
+    if (nccl_unique_id) {   // world_size > 1, or the one-rank NCCL path
         int st = nccl_load();
         if (st) { delete c; return st; }
         ncclUniqueId id;

@@ -742,7 +742,7 @@ int build_plan(Ctx* ctx, Plan** out, int d, const double* x, long long n, const 
     if ((st = alloc((void**)&P->u_s, sizeof(double) * (std::max(n, 1LL) + 2)))) return fail(st);
     if ((st = alloc((void**)&P->b_s, sizeof(double) * std::max(m, 1LL)))) return fail(st);
     if ((st = alloc((void**)&P->v_s, sizeof(double) * (std::max(m, 1LL) + 2)))) return fail(st);
-    P->box_exchange = ctx->world > 1 || getenv("SK_FORCE_BOX_EXCHANGE") != nullptr;
+    P->box_exchange = ctx->world > 1 || ctx->nccl_comm || getenv("SK_FORCE_BOX_EXCHANGE") != nullptr;
     if (P->box_exchange && (st = alloc((void**)&P->box_buf, sizeof(double) * std::max(P->box_size, 1LL))))
         return fail(st);
     if ((st = alloc((void**)&P->red, sizeof(double) * 4096))) return fail(st);

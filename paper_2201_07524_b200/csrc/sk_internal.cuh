@@ -76,7 +76,7 @@ struct Ctx {
     int rank = 0;
     int world = 1;
     cudaStream_t stream = nullptr;
-    void* nccl_comm = nullptr;    // ncclComm_t when world > 1
+    void* nccl_comm = nullptr;    // ncclComm_t when world > 1 (or the one-rank NCCL path)
     bool emulated = false;        // SK_EMULATE_WORLD test hook: `world` identical ranks, no NCCL
 };
 

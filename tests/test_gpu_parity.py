@@ -447,6 +447,34 @@ def test_emulated_two_rank_world(capi):
         c.close()
 
 
+def test_nccl_one_rank_path(capi):
+    """world_size 1 with an ncclUniqueId: a real one-rank NCCL communicator, so the bbox min/max,
+    the box exchange of every fast summation and the scalar sums all run through ncclAllReduce
+    (dlopen'ed libnccl, inside the CUDA-graph capture of sinkhorn_run) as the identity. Results
+    equal the communicator-free context's to summation-order rounding."""
+    cfg = get("c3").with_(n=20000, m=15000)
+    x, y, a, b = make_inputs(cfg)
+    iters = 20
+    c1 = capi.Context(0)
+    c2 = capi.Context(0, 0, 1, capi.sk_nccl_unique_id())
+    out = []
+    for c in (c1, c2):
+        P = capi.Plan(c, dev(x), dev(y), cfg.lam, cfg.N, cfg.sigma, cfg.m_w, cfg.eps_B, cfg.p)
+        w = dev(uniform_test_weights(3, y.shape[0]))
+        t = capi.fastsum_apply(P, w, 0, 0)
+        u, v, _ = capi.sinkhorn_run(P, dev(a), dev(b), iters)
+        sd, sc = capi.sinkhorn_divergence(P, dev(a), dev(b), u, v)
+        out.append((t, u, v, sd, sc, P.info()))
+        P.close()
+    (t1, u1, v1, sd1, sc1, i1), (t2, u2, v2, sd2, sc2, i2) = out
+    assert i2["box_size"] == i1["box_size"] and i2["total_x"] == x.shape[0]
+    assert float(((t2 - t1).abs()).max() / t1.abs().max()) < 1e-13
+    assert float(((u2 - u1).abs() / u1).max()) < 1e-11 and float(((v2 - v1).abs() / v1).max()) < 1e-11
+    assert abs(sd2 - sd1) <= 1e-11 * abs(sd1) and abs(sc2 - sc1) <= 1e-11 * abs(sc1)
+    c2.close()
+    c1.close()
+
+
 # ------------------------------------------------------------------ NEXT-2: r = 1 (Laplace kernel + near field)
 @pytest.mark.parametrize("d,n,N", [(1, 300, 128), (2, 150, 128)])
 def test_r1_fastsum_matches_oracle(capi, ctx, d, n, N):
