@@ -161,6 +161,102 @@ __device__ __forceinline__ void cp_async8(void* smem_dst, const void* gmem_src) 
 }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
 
+// One batch (<= 32 nodes of one cell) with NT_ n-tiles of 8 nodes: ragged tail batches of sparse
+// cells run ceil(count / 8) n-tiles instead of 4 (c3 x nodes: 29 % fewer DMMAs).
+// Hb: the cell's 12^3 block (+ q), row strides sxs (tx) and ry[] (the lane's 3 ty rows).
+template <int NT_, bool STAGE>
+__device__ __forceinline__ void interp3_batch(const CellBatch& B, const double* __restrict__ taps,
+                                              const double* XT, const double* Hb, long long sxs,
+                                              const long long (&ry)[3], int ty1, int txo1, int g, int q,
+                                              double* __restrict__ t_out, const FusedUpd& fu) {
+    using C = InterpDCfg;
+    constexpr int W = C::W, KS = C::KS, TS = C::TS;
+    const double* T0 = taps + (long long)B.start * TS;
+    const int last = B.count - 1;
+    // B fragments: phi_z of node 8 nt + g at tz = 4 s + q
+    double bf[KS][NT_];
+#pragma unroll
+    for (int nt = 0; nt < NT_; ++nt) {
+        const double* tz = T0 + min(8 * nt + g, last) * TS + 2 * W;
+#pragma unroll
+        for (int s = 0; s < KS; ++s) bf[s][nt] = __ldg(tz + 4 * s + q);
+    }
+    // per (node, ty) partial sums over tx: phi_y is applied once after the k loop, so each
+    // E value costs one DFMA in the loop (24 per k-step at 4 n-tiles)
+    double acc3[NT_][2][3];
+#pragma unroll
+    for (int nt = 0; nt < NT_; ++nt)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) acc3[nt][e][0] = acc3[nt][e][1] = acc3[nt][e][2] = 0.0;
+#pragma unroll kInterpKUnroll
+    for (int k = 0; k < W / 2; ++k) {
+        // three m-tiles (one period of ty) per step, their DMMAs interleaved s-major so
+        // 3 NT_ independent accumulations separate dependent DMMAs
+        int txr[3];
+        txr[0] = 2 * k;
+        txr[1] = 2 * k + txo1;
+        txr[2] = 2 * k + 1;
+        double a[3][KS];
+#pragma unroll
+        for (int r3 = 0; r3 < 3; ++r3) {
+            const double* Hrow = Hb + txr[r3] * sxs + ry[r3];
+#pragma unroll
+            for (int s = 0; s < KS; ++s) a[r3][s] = STAGE ? Hrow[4 * s] : __ldg(Hrow + 4 * s);
+        }
+        double d[3][NT_][2];
+#pragma unroll
+        for (int r3 = 0; r3 < 3; ++r3)
+#pragma unroll
+            for (int nt = 0; nt < NT_; ++nt) d[r3][nt][0] = d[r3][nt][1] = 0.0;
+#pragma unroll
+        for (int s = 0; s < KS; ++s)
+#pragma unroll
+            for (int r3 = 0; r3 < 3; ++r3)
+#pragma unroll
+                for (int nt = 0; nt < NT_; ++nt) dmma884(d[r3][nt][0], d[r3][nt][1], a[r3][s], bf[s][nt]);
+#pragma unroll
+        for (int nt = 0; nt < NT_; ++nt)
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+                // phi_x[2k], phi_x[2k+1] of the node in one 16-byte load
+                const double2 xx = reinterpret_cast<const double2*>(XT + (8 * nt + 2 * q + e) * C::XS)[k];
+                acc3[nt][e][0] = fma(xx.x, d[0][nt][e], acc3[nt][e][0]);
+                acc3[nt][e][1] = fma(txo1 ? xx.y : xx.x, d[1][nt][e], acc3[nt][e][1]);
+                acc3[nt][e][2] = fma(xx.y, d[2][nt][e], acc3[nt][e][2]);
+            }
+    }
+    double acc[NT_][2];
+#pragma unroll
+    for (int nt = 0; nt < NT_; ++nt)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+            const double* tr = T0 + min(8 * nt + 2 * q + e, last) * TS + W;
+            acc[nt][e] = fma(__ldg(tr + g), acc3[nt][e][0],
+                             fma(__ldg(tr + ty1), acc3[nt][e][1], __ldg(tr + 4 + g) * acc3[nt][e][2]));
+        }
+    // sum over the 8 rows g held by lanes q, q+4, ..., q+28
+#pragma unroll
+    for (int nt = 0; nt < NT_; ++nt)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+            double v = acc[nt][e];
+            v += __shfl_xor_sync(0xffffffffu, v, 4);
+            v += __shfl_xor_sync(0xffffffffu, v, 8);
+            v += __shfl_xor_sync(0xffffffffu, v, 16);
+            acc[nt][e] = v;
+        }
+    // every lane now holds the sums of its q; lane (g, q) emits node 8 (g/2) + 2 q + g%2, so
+    // the results (and the fused division) take one full-warp pass
+    double v = acc[0][0];
+#pragma unroll
+    for (int nt = 0; nt < NT_; ++nt)
+#pragma unroll
+        for (int e = 0; e < 2; ++e)
+            if (g == 2 * nt + e) v = acc[nt][e];
+    const int p = 8 * (g >> 1) + 2 * q + (g & 1);
+    if ((g >> 1) < NT_ && p < B.count) emit_t(t_out, fu, B.start + p, v);
+}
+
 // STAGE: copy each cell's 12^3 grid block to shared memory once and read the A fragments from
 // there (pays when cells hold several batches: c5 interp 16.1 -> 14.2 ms); otherwise read them
 // through L1 straight from the grid.
@@ -169,7 +265,8 @@ __global__ void __launch_bounds__(SK_INTERP_NT, SK_INTERP3_MINB)
 interp3_dmma_kernel(const CellBatch* __restrict__ batches, int nbatches, const double* __restrict__ taps,
                     const double* __restrict__ grid, int n, double* __restrict__ t_out, const FusedUpd fu) {
     using C = InterpDCfg;
-    constexpr int W = C::W, KS = C::KS, m = W / 2, TS = C::TS, NB = C::NB, NTN = C::NTN;
+    constexpr int W = C::W, m = W / 2, TS = C::TS, NB = C::NB, NTN = C::NTN;
+    static_assert(NTN >= 1 && NTN <= 4, "interp3 batches hold 1..4 n-tiles");
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int g = lane >> 2, q = lane & 3;
     const long long n2 = (long long)n * n;
@@ -179,9 +276,17 @@ interp3_dmma_kernel(const CellBatch* __restrict__ batches, int nbatches, const d
     double* GB = XT + NB * C::XS;                          // [tx][ty][tz] grid block of the cell
     int cur_cell = -1;
     // contiguous slice of the cell-sorted batch list per warp: consecutive batches of one
-    // cell reuse its 12^3 grid block from L1, and the taps stream sequentially
+    // cell reuse its 12^3 grid block, and the taps stream sequentially
     const int per = (nbatches + nw - 1) / nw;
     const int b_lo = gw * per, b_hi = min(nbatches, b_lo + per);
+    // Rows of the DMMA are the flattened (tx, ty) pairs r = 8 mt + g, mt < 18 (no padding).
+    // For lane row g, ty = r % 12 cycles with period 3 in mt through {g, (8+g)%12, 4+g}.
+    // Within step k the lane's three rows have tx = 2k (r3 = 0, and r3 = 1 when g < 4) or
+    // 2k + 1 (r3 = 2, and r3 = 1 when g >= 4).
+    const int ty1 = (8 + g) % W, txo1 = (g >= 4) ? 1 : 0;
+    const long long sxs = STAGE ? W * W : n2;
+    const long long ry[3] = {STAGE ? g * W : (long long)g * n, STAGE ? ty1 * W : (long long)ty1 * n,
+                             STAGE ? (4 + g) * W : (long long)(4 + g) * n};
 
     CellBatch Bnext = b_lo < b_hi ? batches[b_lo] : CellBatch{0, 0, 0, 0};
     for (int bi = b_lo; bi < b_hi; ++bi) {
@@ -191,10 +296,9 @@ interp3_dmma_kernel(const CellBatch* __restrict__ batches, int nbatches, const d
         const double* T0 = taps + (long long)B.start * TS;
         const int last = B.count - 1;
         // a new cell: copy its 12^3 grid block to shared memory (async, overlapped with the
-        // batch's tap loads below); the following batches of the cell read it from there
+        // batch's tap loads); the following batches of the cell read it from there
         const bool new_cell = STAGE && B.cell != cur_cell;
         if (new_cell) {
-            __syncwarp();
             const double* Gb = grid + (long long)(cx - m + 1) * n2 + (long long)(cy - m + 1) * n + (cz - m + 1);
             for (int i = lane; i < C::GBLK; i += 32) {
                 const int r = i / W, c = i % W;
@@ -204,137 +308,21 @@ interp3_dmma_kernel(const CellBatch* __restrict__ batches, int nbatches, const d
         }
         if (bi + 1 < b_hi)   // next batch of this warp: stream its taps into L2
             prefetch_range(taps + (long long)Bnext.start * TS, (long long)Bnext.count * TS * 8, lane);
-        // B fragments: phi_z of node 8 nt + g at tz = 4 s + q
-        double bf[KS][NTN];
-#pragma unroll
-        for (int nt = 0; nt < NTN; ++nt) {
-            const double* tz = T0 + min(8 * nt + g, last) * TS + 2 * W;
-#pragma unroll
-            for (int s = 0; s < KS; ++s) bf[s][nt] = __ldg(tz + 4 * s + q);
-        }
-        // Rows of the DMMA are the flattened (tx, ty) pairs r = 8 mt + g, mt < 18 (no padding).
-        // For lane row g, ty = r % 12 cycles with period 3 in mt through {g, (8+g)%12, 4+g},
-        // so phi_y of the lane's 8 nodes lives in registers at just those 3 positions.
-        // Within step k the lane's three rows have tx = 2k (r3 = 0, and r3 = 1 when g < 4) or
-        // 2k + 1 (r3 = 2, and r3 = 1 when g >= 4): accumulate phi_y * E per (node, tx) and apply
-        // phi_x once per k with one 16-byte load of (phi_x[2k], phi_x[2k+1]).
-        const int ty1 = (8 + g) % W, txo1 = (g >= 4) ? 1 : 0;
-#if !SK_INTERP3_ACCTY
-        double yv[NTN][2][3];   // phi_y at ty = g, (8+g)%12, 4+g
-#endif
         if (lane < NB) {   // stage the batch's phi_x rows (lane = node) in this warp's shared table
             const double2* src = reinterpret_cast<const double2*>(T0 + min(lane, last) * TS);
             double2* dst = reinterpret_cast<double2*>(XT + lane * C::XS);
 #pragma unroll
             for (int i = 0; i < W / 2; ++i) dst[i] = __ldg(src + i);
         }
-        __syncwarp();
-#if SK_INTERP3_ACCTY
-        // per (node, ty) partial sums over tx: phi_y is applied once after the k loop, so each
-        // E value costs one DFMA in the loop (24 per k-step instead of 40)
-        double acc3[NTN][2][3];
-#pragma unroll
-        for (int nt = 0; nt < NTN; ++nt)
-#pragma unroll
-            for (int e = 0; e < 2; ++e) acc3[nt][e][0] = acc3[nt][e][1] = acc3[nt][e][2] = 0.0;
-#else
-#pragma unroll
-        for (int nt = 0; nt < NTN; ++nt)
-#pragma unroll
-            for (int e = 0; e < 2; ++e) {
-                const double* tr = T0 + min(8 * nt + 2 * q + e, last) * TS;
-                yv[nt][e][0] = __ldg(tr + W + g);
-                yv[nt][e][1] = __ldg(tr + W + ty1);
-                yv[nt][e][2] = __ldg(tr + W + 4 + g);
-            }
-#endif
-        double acc[NTN][2];
-#pragma unroll
-        for (int nt = 0; nt < NTN; ++nt) acc[nt][0] = acc[nt][1] = 0.0;
         if (new_cell) cp_async_wait_all();
         __syncwarp();
         const double* Hb = STAGE ? GB + q
                                  : grid + (long long)(cx - m + 1) * n2 + (long long)(cy - m + 1) * n + (cz - m + 1) + q;
-        const long long sxs = STAGE ? W * W : n2;
-        const long long ry[3] = {STAGE ? g * W : (long long)g * n, STAGE ? ty1 * W : (long long)ty1 * n,
-                                 STAGE ? (4 + g) * W : (long long)(4 + g) * n};
-#pragma unroll kInterpKUnroll
-        for (int k = 0; k < W / 2; ++k) {
-            // three m-tiles (one period of ty) per step, their DMMAs interleaved s-major so
-            // 12 independent accumulations separate dependent DMMAs
-            int txr[3];
-            txr[0] = 2 * k;
-            txr[1] = 2 * k + txo1;
-            txr[2] = 2 * k + 1;
-            double a[3][KS];
-#pragma unroll
-            for (int r3 = 0; r3 < 3; ++r3) {
-                const double* Hrow = Hb + txr[r3] * sxs + ry[r3];
-#pragma unroll
-                for (int s = 0; s < KS; ++s) a[r3][s] = STAGE ? Hrow[4 * s] : __ldg(Hrow + 4 * s);
-            }
-            double d[3][NTN][2];
-#pragma unroll
-            for (int r3 = 0; r3 < 3; ++r3)
-#pragma unroll
-                for (int nt = 0; nt < NTN; ++nt) d[r3][nt][0] = d[r3][nt][1] = 0.0;
-#pragma unroll
-            for (int s = 0; s < KS; ++s)
-#pragma unroll
-                for (int r3 = 0; r3 < 3; ++r3)
-#pragma unroll
-                    for (int nt = 0; nt < NTN; ++nt) dmma884(d[r3][nt][0], d[r3][nt][1], a[r3][s], bf[s][nt]);
-#pragma unroll
-            for (int nt = 0; nt < NTN; ++nt)
-#pragma unroll
-                for (int e = 0; e < 2; ++e) {
-                    // phi_x[2k], phi_x[2k+1] of the node in one 16-byte load
-                    const double2 xx = reinterpret_cast<const double2*>(XT + (8 * nt + 2 * q + e) * C::XS)[k];
-#if SK_INTERP3_ACCTY
-                    acc3[nt][e][0] = fma(xx.x, d[0][nt][e], acc3[nt][e][0]);
-                    acc3[nt][e][1] = fma(txo1 ? xx.y : xx.x, d[1][nt][e], acc3[nt][e][1]);
-                    acc3[nt][e][2] = fma(xx.y, d[2][nt][e], acc3[nt][e][2]);
-#else
-                    const double t1 = yv[nt][e][1] * d[1][nt][e];
-                    const double sa = fma(yv[nt][e][0], d[0][nt][e], txo1 ? 0.0 : t1);
-                    const double sb = fma(yv[nt][e][2], d[2][nt][e], txo1 ? t1 : 0.0);
-                    acc[nt][e] = fma(xx.x, sa, fma(xx.y, sb, acc[nt][e]));
-#endif
-                }
-        }
-#if SK_INTERP3_ACCTY
-#pragma unroll
-        for (int nt = 0; nt < NTN; ++nt)
-#pragma unroll
-            for (int e = 0; e < 2; ++e) {
-                const double* tr = T0 + min(8 * nt + 2 * q + e, last) * TS + W;
-                acc[nt][e] = fma(__ldg(tr + g), acc3[nt][e][0],
-                                 fma(__ldg(tr + ty1), acc3[nt][e][1], __ldg(tr + 4 + g) * acc3[nt][e][2]));
-            }
-#endif
-        // sum over the 8 rows g held by lanes q, q+4, ..., q+28
-#pragma unroll
-        for (int nt = 0; nt < NTN; ++nt)
-#pragma unroll
-            for (int e = 0; e < 2; ++e) {
-                double v = acc[nt][e];
-                v += __shfl_xor_sync(0xffffffffu, v, 4);
-                v += __shfl_xor_sync(0xffffffffu, v, 8);
-                v += __shfl_xor_sync(0xffffffffu, v, 16);
-                acc[nt][e] = v;
-            }
-        // every lane now holds the 8 sums of its q; lane (g, q) emits node 8 (g/2) + 2 q + g%2,
-        // so the 32 results (and the fused division) take one full-warp pass
-        {
-            double v = acc[0][0];
-#pragma unroll
-            for (int nt = 0; nt < NTN; ++nt)
-#pragma unroll
-                for (int e = 0; e < 2; ++e)
-                    if (g == 2 * nt + e) v = acc[nt][e];
-            const int p = 8 * (g >> 1) + 2 * q + (g & 1);
-            if ((g >> 1) < NTN && p < B.count) emit_t(t_out, fu, B.start + p, v);
-        }
+        const int ntn = min(NTN, (B.count + 7) >> 3);   // warp-uniform
+        if (ntn >= 4 && NTN >= 4) interp3_batch<(NTN >= 4 ? 4 : 1), STAGE>(B, taps, XT, Hb, sxs, ry, ty1, txo1, g, q, t_out, fu);
+        else if (ntn == 3 && NTN >= 3) interp3_batch<(NTN >= 3 ? 3 : 1), STAGE>(B, taps, XT, Hb, sxs, ry, ty1, txo1, g, q, t_out, fu);
+        else if (ntn == 2 && NTN >= 2) interp3_batch<(NTN >= 2 ? 2 : 1), STAGE>(B, taps, XT, Hb, sxs, ry, ty1, txo1, g, q, t_out, fu);
+        else interp3_batch<1, STAGE>(B, taps, XT, Hb, sxs, ry, ty1, txo1, g, q, t_out, fu);
         __syncwarp();   // XT is rewritten by the next batch
     }
 }
