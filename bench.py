@@ -381,12 +381,13 @@ def main():
         if c_ > 0 and ms_ > 0:
             stage_hbm[st_name] = {"alg_bytes_per_launch": by, "avg_launch_ms": ms_ / c_,
                                   "frac": by / (ms_ / c_ * 1e-3) / (pk["hbm_gbs"] * 1e9)}
-    traffic, traffic_src = None, None
+    traffic, traffic_src, traffic_note = None, None, None
     try:
         with open(os.path.join(ROOT, "profiles", "traffic.json")) as fh:
             tr = json.load(fh).get(cfg.name, {}).get(dom)
         if tr and world == 1:
             traffic, traffic_src = float(tr["bytes_per_launch"]), tr["measured"]
+            traffic_note = tr.get("note")
     except (OSError, ValueError, KeyError):
         pass
     line = {
@@ -410,11 +411,10 @@ def main():
         "roofline": {"bound": "alu", "kernel": dom, "achieved": achieved, "peak": fp64_peak,
                      "unit": "TFLOP/s", "frac": achieved / fp64_peak, "traffic": traffic,
                      "traffic_source": traffic_src,
-                     "traffic_note": ("DRAM bytes are dominated by the plan-time window-tap table (d x 2m_w doubles "
-                                      "per node, read once per launch; DESIGN.md §6): evaluating the taps in the "
-                                      "kernel instead would add ~130 FP64 vector ops per lane and k-step to a "
-                                      "kernel bound by the shared FP64/DMMA pipe, while the table runs at ~20 % "
-                                      "of HBM bandwidth") if traffic else None,
+                     "traffic_note": traffic_note,
+                     # measured DRAM bytes (ncu) over the live launch time: how close the kernel's real
+                     # traffic runs to the HBM roof
+                     "traffic_hbm_frac": (traffic / (avg_ms * 1e-3) / (pk["hbm_gbs"] * 1e9)) if traffic else None,
                      "algorithmic": f"2*(2m_w)^d flops per node per launch, {pts_per_launch:.3g} nodes/launch",
                      "peak_source": f"{N_SM} SMs x {FP64_FMA_PER_CLK_PER_SM} FP64 FMA/clk x 2 x sm_max_mhz "
                                     f"{pk.get('sm_max_mhz')} (DESIGN.md)",
