@@ -70,6 +70,49 @@ def test_spread_interp_match_gridding_definition(capi, ctx, d, N, m_w, cnt):
     assert (np.abs(t - t_ref) <= 1e-14 * scale).all()
 
 
+@pytest.mark.parametrize("d,m_w", [(3, 6), (2, 8)])
+def test_cell_occupancies_match_gridding_definition(capi, ctx, d, m_w):
+    """Clusters of x nodes confined to single grid cells, one cluster per occupancy in
+    {1, 7, 8, 9, 16, 17, 24, 25, 31, 32, 33, 40, 64, 65, 97}: every per-cell batch shape of the
+    tensor-core kernels (1..4 n-tiles of 8 nodes, full and ragged 32-node batches, several
+    batches per cell) against the gridding definition. y holds the unit cube's corners, so the
+    geometry is fixed and cell centres are known in advance."""
+    rng = np.random.default_rng(7 + d)
+    N = 16
+    n = 2 * N
+    L = 0.5 - 1 / 16
+    rho = L / math.sqrt(d)
+    occ = [1, 7, 8, 9, 16, 17, 24, 25, 31, 32, 33, 40, 64, 65, 97]
+    lo, hi = int(math.ceil(n * (0.5 - rho / 2))) + 1, int(n * (0.5 + rho / 2)) - 2
+    cells = set()
+    while len(cells) < len(occ):
+        cells.add(tuple(rng.integers(lo, hi, size=d)))
+    pts = []
+    for k, c in zip(occ, sorted(cells)):
+        u = np.array(c, dtype=float) + 0.5 + rng.uniform(-0.35, 0.35, size=(k, d))   # inside the cell
+        pts.append(0.5 + (u / n - 0.5) / rho)
+    x = np.concatenate(pts)
+    corners = np.array(np.meshgrid(*[[0.0, 1.0]] * d, indexing="ij")).reshape(d, -1).T
+    y = np.concatenate([corners, rng.random((50, d))])
+    P = capi.Plan(ctx, dev(x), dev(y), 20.0, N, 2.0, m_w)
+    centre, rho_ref, _ = nfft_ref.geometry(x, y, 1 / 16)
+    assert abs(P.info()["rho"] - rho_ref) <= 1e-15 * rho_ref and abs(rho_ref - rho) <= 1e-15 * rho
+    xs = nfft_ref.scale(x, centre, rho_ref)
+    cell_of = np.floor(n * (xs + 0.5)).astype(int)
+    _, counts = np.unique(cell_of, axis=0, return_counts=True)
+    assert sorted(counts.tolist()) == sorted(occ)
+    G = rng.normal(size=(n,) * d)
+    t_ref = nfft_ref.grid_interp(G, xs, m_w, 2.0)
+    t = capi.nfft_interp(P, 0, dev(G)).cpu().numpy()
+    scale = nfft_ref.grid_interp(np.abs(G), xs, m_w, 2.0)
+    assert (np.abs(t - t_ref) <= 1e-14 * scale).all()
+    w = rng.random(x.shape[0])
+    g_ref = nfft_ref.grid_spread(xs, w, n, m_w, 2.0)
+    g = capi.nfft_spread(P, 0, dev(w)).cpu().numpy()
+    assert np.abs(g - g_ref).max() <= 1e-13 * np.abs(g_ref).max()
+    P.close()
+
+
 @pytest.mark.parametrize("name", ["c1", "c2", "c3", "c5"])
 def test_kernel_coefficients_match_oracle(capi, ctx, name):
     cfg = get(name)
