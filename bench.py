@@ -57,6 +57,13 @@ def parse():
     return p.parse_args()
 
 
+def workload_config(cfg):
+    """The `config` keys both arms report for a workload."""
+    return {"workload": cfg.name, "n": cfg.n, "m": cfg.m, "d": cfg.d, "lambda": cfg.lam, "N": cfg.N,
+            "sigma": cfg.sigma, "m_w": cfg.m_w, "eps_B": cfg.eps_B, "iters_per_step": cfg.iters,
+            "step": "plan + iters x (K v, K^T u) + divergence (2 applies)"}
+
+
 def peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
@@ -187,10 +194,9 @@ def run_reference(args):
     value = float(statistics.median(vals))
     line = {
         "impl": "reference", "metric": "sinkhorn_iterations_per_s", "value": value, "unit": "it/s",
-        "n_gpus": 0, "steps": args.steps, "warmup": args.warmup, "higher_is_better": True,
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "higher_is_better": True,
         "ms_per_step": 1e3 * cfg.iters / value, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic", "config": {"workload": cfg.name, "n": cfg.n, "m": cfg.m, "d": cfg.d,
-                                        "lambda": cfg.lam, "N": cfg.N, "iters": cfg.iters},
+        "data": "synthetic", "config": dict(workload_config(cfg), parallelism="host cores (CPU oracle, no GPU)"),
         "cpu_baseline": {"value": value, "unit": "it/s", "cores": cores, "kind": "oracle", "sample": descs[-1],
                          "cpu_model": cpu_model(), "nproc": os.cpu_count(),
                          "direct_sum_pair_evals_per_s": ORACLE_PAIRS_PER_S},
@@ -395,9 +401,7 @@ def main():
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": step_ms, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (seeded generators of BASELINE.json configs; see DESIGN.md input recipe)",
-        "config": {"workload": cfg.name, "n": cfg.n, "m": cfg.m, "d": cfg.d, "lambda": cfg.lam, "N": cfg.N,
-                   "sigma": cfg.sigma, "m_w": cfg.m_w, "eps_B": cfg.eps_B, "iters_per_step": cfg.iters,
-                   "step": "plan + iters x (K v, K^T u) + divergence (2 applies)",
+        "config": {**workload_config(cfg),
                    "parallelism": f"dp{world} (point shards + grid all-reduce)"
                                   + (", one-rank NCCL communicator" if args.nccl_self and world == 1 else ""),
                    "l2": "256 MB buffer written between timed steps"},

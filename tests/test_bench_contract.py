@@ -22,5 +22,6 @@ def test_reference_arm_json_line():
         assert k in d, k
     assert d["impl"] == "reference" and d["value"] > 0 and d["higher_is_better"] is True
     assert d["config"]["workload"] == "c1"
+    assert {"n", "m", "d", "lambda", "N", "sigma", "m_w", "eps_B", "iters_per_step", "step"} <= set(d["config"])
     assert d["cpu_baseline"]["kind"] == "oracle" and d["cpu_baseline"]["value"] == d["value"]
     assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["e2e"]["value"] == d["value"]
