@@ -70,7 +70,10 @@ constexpr int kInterpBatch3 = SK_INTERP_NB;   // d = 3 interp batch (nodes of on
 constexpr int kSegMax = 1024;
 constexpr int kSegHybrid = 128;   // spread3_hybrid_kernel segments (two passes, L2-resident taps)
 constexpr int kSegTmaMax = 64;     // spread3_tma_kernel segments (one TMA-staged buffer each)
-constexpr int kSegTmaPMax = SK_TP_SEG_MAX;   // spread3_tmapad_kernel segments
+constexpr int kSegTmaPMax = SK_TP_SEG_MAX;   // spread3_tmapad_kernel segments (sparse cells)
+constexpr int kSegTmaPDense = 64;             // spread3_tmapad_kernel segments (dense cells)
+constexpr int kSegDenseMinMean = 200;         // mean nodes per occupied cell for the dense shape
+                                              // (measured: c5 x 1793 / y 278 gain, c3 y 136 loses)
 constexpr int kSpreadItemMax = 4096;
 
 #ifndef SK_WORKLIST_ONLY   // plan.cu only needs the work-list types above
@@ -791,29 +794,29 @@ spread3_tma_kernel(const SpreadItem* __restrict__ items, int nitems, const CellB
 // the same TMA double buffer: warp h owns the 9 n-tiles with ty in 6h .. 6h+5, so a lane holds
 // 36 accumulators instead of 72 and reads its operands from shared memory, which lets 3 pairs
 // share a CTA (12 warps per SM instead of 8).
-#ifndef SK_TP_SEG
-#define SK_TP_SEG 32
-#endif
-#ifndef SK_TP_NPAIR
-#define SK_TP_NPAIR 3
-#endif
-constexpr int kSegTmaP = SK_TP_SEG;
+// Two shapes: 32-node segments on 3 pairs per CTA (12 warps per SM; sparse cells, where the
+// per-cell region update dominates) and 64-node segments on 2 pairs (8 warps per SM, half the
+// per-segment overhead; dense cells: c5 spread 15.48 -> 15.14 ms). The plan picks per node set.
+template <int SEG, int NPAIR_>
 struct SpreadTPCfg {
-    static constexpr int W = 12, S = W + 1, NPAIR = SK_TP_NPAIR, NT = 64 * NPAIR, NTH = 9;
+    static constexpr int W = 12, S = W + 1, NPAIR = NPAIR_, NT = 64 * NPAIR, NTH = 9;
     static constexpr int TS = 3 * W;
     static constexpr int REG = S * S * S;
     static constexpr int REGP = REG + 1;
-    static constexpr int TBUF = kSegTmaP * TS;
-    static constexpr int WBUF = kSegTmaP + 4;
+    static constexpr int TBUF = SEG * TS;
+    static constexpr int WBUF = SEG + 4;
     static constexpr int PAIR = 2 + REGP + 2 * TBUF + 2 * WBUF;
     static constexpr size_t SMEM_BYTES = sizeof(double) * NPAIR * PAIR;
 };
+using SpreadTPCfgSparse = SpreadTPCfg<kSegTmaPMax, 3>;
+using SpreadTPCfgDense = SpreadTPCfg<kSegTmaPDense, 2>;
 
-__global__ void __launch_bounds__(64 * SK_TP_NPAIR, 2)
+template <int SEG, int NPAIR_>
+__global__ void __launch_bounds__(64 * NPAIR_, 2)
 spread3_tmapad_kernel(const SpreadItem* __restrict__ items, int nitems, const CellBatch* __restrict__ segs,
                       const double* __restrict__ taps, const double* __restrict__ w,
                       double* __restrict__ grid, int n) {
-    using C = SpreadTPCfg;
+    using C = SpreadTPCfg<SEG, NPAIR_>;
     constexpr int W = C::W, S = C::S, m = W / 2, NTH = C::NTH, TS = C::TS;
     extern __shared__ __align__(16) double smem[];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;

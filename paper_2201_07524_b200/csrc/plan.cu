@@ -389,9 +389,6 @@ static int build_cell_lists(Plan& P, NodeSet& S, cudaStream_t s) {
     // spread work-unit size: enough items to keep ~4 per resident warp busy (148 SMs x 8
     // warps), at most kSpreadItemMax nodes (one region flush per item)
     const int item_max = (int)std::max(128LL, std::min((long long)kSpreadItemMax, count / 4736));
-    const int seg_max = std::min(P.spread_tmapad ? kSegTmaPMax
-                                 : (P.spread_tma ? kSegTmaMax : (P.spread_hybrid ? kSegHybrid : kSegMax)),
-                                 item_max);
 
     // run-length encode the sorted keys; 7 int arrays of nruns (<= count) entries
     int* buf = nullptr;
@@ -411,6 +408,16 @@ static int build_cell_lists(Plan& P, NodeSet& S, cudaStream_t s) {
     SK_CUDA(cudaStreamSynchronize(s));
     const int thr = 256, blk = (nruns + thr - 1) / thr;
     S.xpairs = P.spread_xpairs && (long long)kXPairMaxDensity * nruns > count;
+    // dense cells: longer TMA segments on fewer warp pairs (SK_SEG_DENSE_MIN overrides the mean
+    // nodes-per-cell threshold; 0 = always, a large value = never)
+    {
+        const char* ev = getenv("SK_SEG_DENSE_MIN");
+        const long long thr = ev ? atoll(ev) : (long long)kSegDenseMinMean;
+        S.seg_dense = P.spread_tmapad && P.d == 3 && count >= thr * (long long)nruns;
+    }
+    const int seg_max = std::min(P.spread_tmapad ? (S.seg_dense ? kSegTmaPDense : kSegTmaPMax)
+                                 : (P.spread_tma ? kSegTmaMax : (P.spread_hybrid ? kSegHybrid : kSegMax)),
+                                 item_max);
     g.xpairs = S.xpairs ? 1 : 0;
     SK_CUDA(cub::DeviceScan::ExclusiveSum(tmp, tb, cnts, rstart, nruns, s));
     const int bmax = d == 3 ? kInterpBatch3 : 32;   // interp batch: nodes of one cell per warp pass

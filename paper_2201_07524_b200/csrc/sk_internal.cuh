@@ -64,6 +64,7 @@ struct NodeSet {
     int nbatches = 0;
     int ncells = 0;              // non-empty cells
     bool xpairs = false;         // spread segments span x-pairs of cells (sparse cells, d = 3)
+    bool seg_dense = false;      // 64-node spread segments on 2 warp pairs (dense cells, d = 3)
     void* segs = nullptr;        // CellBatch[nsegs]: <= kSegMax nodes of one cell (spread)
     int nsegs = 0;
     void* sitems = nullptr;      // SpreadItem[nsitems]: segments of one 2^3 super-tile (spread)

@@ -160,16 +160,22 @@ inline int spread_dispatch(Plan& P, const NodeSet& S, const double* w, double* g
         return SK_OK;
     }
     if (P.dmma && P.spread_tmapad) {
-        using C = SpreadTPCfg;
         static bool attr = false;
         if (!attr) {
-            cudaFuncSetAttribute(spread3_tmapad_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM_BYTES);
+            cudaFuncSetAttribute(spread3_tmapad_kernel<kSegTmaPMax, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)SpreadTPCfgSparse::SMEM_BYTES);
+            cudaFuncSetAttribute(spread3_tmapad_kernel<kSegTmaPDense, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)SpreadTPCfgDense::SMEM_BYTES);
             attr = true;
         }
         if (S.nsitems > 0) {
-            const int g = persistent_grid(spread3_tmapad_kernel, C::NT, C::SMEM_BYTES, (S.nsitems + C::NPAIR - 1) / C::NPAIR);
-            spread3_tmapad_kernel<<<g, C::NT, C::SMEM_BYTES, s>>>((const SpreadItem*)S.sitems, S.nsitems,
-                                                                  (const CellBatch*)S.segs, S.taps, w, grid, P.n);
+            const auto kern = S.seg_dense ? spread3_tmapad_kernel<kSegTmaPDense, 2> : spread3_tmapad_kernel<kSegTmaPMax, 3>;
+            const int np = S.seg_dense ? SpreadTPCfgDense::NPAIR : SpreadTPCfgSparse::NPAIR;
+            const int nt = S.seg_dense ? SpreadTPCfgDense::NT : SpreadTPCfgSparse::NT;
+            const size_t sm = S.seg_dense ? SpreadTPCfgDense::SMEM_BYTES : SpreadTPCfgSparse::SMEM_BYTES;
+            const int g = persistent_grid(kern, nt, sm, (S.nsitems + np - 1) / np);
+            kern<<<g, nt, sm, s>>>((const SpreadItem*)S.sitems, S.nsitems, (const CellBatch*)S.segs, S.taps, w, grid,
+                                   P.n);
             count_launch();
         }
         cudaError_t e = cudaGetLastError();
