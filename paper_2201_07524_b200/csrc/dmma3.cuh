@@ -811,7 +811,10 @@ struct SpreadTPCfg {
 using SpreadTPCfgSparse = SpreadTPCfg<kSegTmaPMax, 3>;
 using SpreadTPCfgDense = SpreadTPCfg<kSegTmaPDense, 2>;
 
-template <int SEG, int NPAIR_>
+// XP: segments may hold the nodes of an x-pair of cells (seg.cell is the x-digit-0 cell, its
+// seg.pad nodes come first, the rest sit one row lower): 13 of the 16 padded DMMA rows, so a
+// sparse pair costs one accumulator flush instead of two at no extra DMMA work.
+template <int SEG, int NPAIR_, bool XP>
 __global__ void __launch_bounds__(64 * NPAIR_, 2)
 spread3_tmapad_kernel(const SpreadItem* __restrict__ items, int nitems, const CellBatch* __restrict__ segs,
                       const double* __restrict__ taps, const double* __restrict__ w,
@@ -885,8 +888,15 @@ spread3_tmapad_kernel(const SpreadItem* __restrict__ items, int nitems, const Ce
                 const bool ok = jr < seg.count;
                 const double* tr = T0 + (ok ? jr : 0) * TS;
                 const double wu = ok ? W0[jr] : 0.0;
-                const double a0 = wu * tr[g];
-                const double a1 = (8 + g < W) ? wu * tr[8 + g] : 0.0;
+                double a0, a1;
+                if constexpr (XP) {   // A rows are region rows tx + (node in the x-digit-1 cell)
+                    const int oxn = jr >= seg.pad ? 1 : 0;
+                    a0 = (g - oxn >= 0) ? wu * tr[g - oxn] : 0.0;
+                    a1 = (8 + g - oxn < W) ? wu * tr[8 + g - oxn] : 0.0;
+                } else {
+                    a0 = wu * tr[g];
+                    a1 = (8 + g < W) ? wu * tr[8 + g] : 0.0;
+                }
                 double yv[6];
                 {
                     const double2* y2 = reinterpret_cast<const double2*>(tr + W + 6 * half);
@@ -907,7 +917,7 @@ spread3_tmapad_kernel(const SpreadItem* __restrict__ items, int nitems, const Ce
 #pragma unroll
                 for (int mt = 0; mt < 2; ++mt) {
                     const int tx = 8 * mt + g;
-                    if (tx < W) {
+                    if (XP ? tx < S : tx < W) {   // XP: seg.cell has ox = 0, rows 0..12
                         double* rx = REGm + (ox + tx) * S * S + oy * S + oz;
 #pragma unroll
                         for (int j = 0; j < NTH; ++j)

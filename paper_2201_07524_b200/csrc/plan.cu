@@ -413,7 +413,7 @@ static int build_cell_lists(Plan& P, NodeSet& S, cudaStream_t s) {
     {
         const char* ev = getenv("SK_SEG_DENSE_MIN");
         const long long thr = ev ? atoll(ev) : (long long)kSegDenseMinMean;
-        S.seg_dense = P.spread_tmapad && P.d == 3 && count >= thr * (long long)nruns;
+        S.seg_dense = P.spread_tmapad && P.d == 3 && !S.xpairs && count >= thr * (long long)nruns;
     }
     const int seg_max = std::min(P.spread_tmapad ? (S.seg_dense ? kSegTmaPDense : kSegTmaPMax)
                                  : (P.spread_tma ? kSegTmaMax : (P.spread_hybrid ? kSegHybrid : kSegMax)),
@@ -648,7 +648,7 @@ int build_plan(Ctx* ctx, Plan** out, int d, const double* x, long long n, const 
         // c3 0.31 -> 0.26 ms); SK_SPREAD3_PADDED=1 restores the single-warp padded kernel
         P->spread_tmapad = P->dmma && d == 3 && !P->spread_hybrid && !P->spread_tma &&
                            getenv("SK_SPREAD3_PADDED") == nullptr;
-        P->spread_xpairs = P->dmma && d == 3 && !P->spread_hybrid && !P->spread_tma && !P->spread_tmapad &&
+        P->spread_xpairs = P->dmma && d == 3 && !P->spread_hybrid && !P->spread_tma &&
                            getenv("SK_NO_XPAIRS") == nullptr;
     }
     P->tile_cells = P->dmma ? (d == 3 ? 2 : kSup2) : choose_tile(d, ng, P->tiled);

@@ -162,14 +162,18 @@ inline int spread_dispatch(Plan& P, const NodeSet& S, const double* w, double* g
     if (P.dmma && P.spread_tmapad) {
         static bool attr = false;
         if (!attr) {
-            cudaFuncSetAttribute(spread3_tmapad_kernel<kSegTmaPMax, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)SpreadTPCfgSparse::SMEM_BYTES);
-            cudaFuncSetAttribute(spread3_tmapad_kernel<kSegTmaPDense, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)SpreadTPCfgDense::SMEM_BYTES);
+            cudaFuncSetAttribute(spread3_tmapad_kernel<kSegTmaPMax, 3, false>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SpreadTPCfgSparse::SMEM_BYTES);
+            cudaFuncSetAttribute(spread3_tmapad_kernel<kSegTmaPMax, 3, true>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SpreadTPCfgSparse::SMEM_BYTES);
+            cudaFuncSetAttribute(spread3_tmapad_kernel<kSegTmaPDense, 2, false>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SpreadTPCfgDense::SMEM_BYTES);
             attr = true;
         }
         if (S.nsitems > 0) {
-            const auto kern = S.seg_dense ? spread3_tmapad_kernel<kSegTmaPDense, 2> : spread3_tmapad_kernel<kSegTmaPMax, 3>;
+            const auto kern = S.seg_dense ? spread3_tmapad_kernel<kSegTmaPDense, 2, false>
+                              : (S.xpairs ? spread3_tmapad_kernel<kSegTmaPMax, 3, true>
+                                          : spread3_tmapad_kernel<kSegTmaPMax, 3, false>);
             const int np = S.seg_dense ? SpreadTPCfgDense::NPAIR : SpreadTPCfgSparse::NPAIR;
             const int nt = S.seg_dense ? SpreadTPCfgDense::NT : SpreadTPCfgSparse::NT;
             const size_t sm = S.seg_dense ? SpreadTPCfgDense::SMEM_BYTES : SpreadTPCfgSparse::SMEM_BYTES;
