@@ -8,6 +8,7 @@
 // v1 (this file): one thread per node, window values evaluated on the fly; spread
 // accumulates with FP64 atomics into the global grid, interp reads it through L1/L2.
 #pragma once
+#include <atomic>
 #include "sk_internal.cuh"
 #include "tiled3.cuh"
 #include "dmma3.cuh"
@@ -15,6 +16,15 @@
 #include "window.cuh"
 
 namespace sk {
+
+// cudaFuncSetAttribute is per device: set the kernel attributes once on every device a
+// process launches on (one bit per device ordinal)
+inline bool first_on_device(std::atomic<unsigned long long>& mask) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    const unsigned long long bit = 1ULL << (dev & 63);
+    return !(mask.fetch_or(bit) & bit);
+}
 
 template <int D>
 __global__ void spread_v1_kernel(const double* __restrict__ u, long long count,
@@ -102,10 +112,9 @@ inline int persistent_grid(K kernel, int threads, size_t smem, int nitems) {
 template <int W>
 inline int spread3_launch(Plan& P, const NodeSet& S, const double* w, double* grid, cudaStream_t s) {
     using C = Spread3Cfg<W>;
-    static bool attr = false;
-    if (!attr) {
+    static std::atomic<unsigned long long> attr{0};
+    if (first_on_device(attr)) {
         cudaFuncSetAttribute(spread3_v2_kernel<W>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM_BYTES);
-        attr = true;
     }
     const int g = persistent_grid(spread3_v2_kernel<W>, C::NT, C::SMEM_BYTES, S.nitems);
     spread3_v2_kernel<W><<<g, C::NT, C::SMEM_BYTES, s>>>((const TileItem*)S.items, S.nitems, S.u, w, S.count,
@@ -116,10 +125,9 @@ inline int spread3_launch(Plan& P, const NodeSet& S, const double* w, double* gr
 template <int W>
 inline int interp3_launch(Plan& P, const NodeSet& S, const double* grid, double* t, cudaStream_t s) {
     using C = Interp3Cfg<W>;
-    static bool attr = false;
-    if (!attr) {
+    static std::atomic<unsigned long long> attr{0};
+    if (first_on_device(attr)) {
         cudaFuncSetAttribute(interp3_v2_kernel<W>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM_BYTES);
-        attr = true;
     }
     const int g = persistent_grid(interp3_v2_kernel<W>, C::NT, C::SMEM_BYTES, S.nitems);
     interp3_v2_kernel<W><<<g, C::NT, C::SMEM_BYTES, s>>>((const TileItem*)S.items, S.nitems, S.u, S.count, grid,
@@ -144,10 +152,9 @@ inline int taps_dispatch(Plan& P, NodeSet& S, cudaStream_t s) {
 inline int spread_dispatch(Plan& P, const NodeSet& S, const double* w, double* grid, cudaStream_t s) {
     if (P.dmma && P.d == 2) {
         using C = Spread2Cfg;
-        static bool attr = false;
-        if (!attr) {
+        static std::atomic<unsigned long long> attr{0};
+        if (first_on_device(attr)) {
             cudaFuncSetAttribute(spread2_dmma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM_BYTES);
-            attr = true;
         }
         if (S.nsitems > 0) {
             const int g = persistent_grid(spread2_dmma_kernel, C::NT, C::SMEM_BYTES, (S.nsitems + C::NWARP - 1) / C::NWARP);
@@ -160,15 +167,14 @@ inline int spread_dispatch(Plan& P, const NodeSet& S, const double* w, double* g
         return SK_OK;
     }
     if (P.dmma && P.spread_tmapad) {
-        static bool attr = false;
-        if (!attr) {
+        static std::atomic<unsigned long long> attr{0};
+        if (first_on_device(attr)) {
             cudaFuncSetAttribute(spread3_tmapad_kernel<kSegTmaPMax, 3, false>,
                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SpreadTPCfgSparse::SMEM_BYTES);
             cudaFuncSetAttribute(spread3_tmapad_kernel<kSegTmaPMax, 3, true>,
                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SpreadTPCfgSparse::SMEM_BYTES);
             cudaFuncSetAttribute(spread3_tmapad_kernel<kSegTmaPDense, 2, false>,
                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SpreadTPCfgDense::SMEM_BYTES);
-            attr = true;
         }
         if (S.nsitems > 0) {
             const auto kern = S.seg_dense ? spread3_tmapad_kernel<kSegTmaPDense, 2, false>
@@ -188,10 +194,9 @@ inline int spread_dispatch(Plan& P, const NodeSet& S, const double* w, double* g
     }
     if (P.dmma && P.spread_tma) {
         using C = SpreadTCfg;
-        static bool attr = false;
-        if (!attr) {
+        static std::atomic<unsigned long long> attr{0};
+        if (first_on_device(attr)) {
             cudaFuncSetAttribute(spread3_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM_BYTES);
-            attr = true;
         }
         if (S.nsitems > 0) {
             const int g = persistent_grid(spread3_tma_kernel, C::NT, C::SMEM_BYTES, (S.nsitems + C::NPAIR - 1) / C::NPAIR);
@@ -205,10 +210,9 @@ inline int spread_dispatch(Plan& P, const NodeSet& S, const double* w, double* g
     }
     if (P.dmma && P.spread_hybrid) {
         using C = SpreadHCfg;
-        static bool attr = false;
-        if (!attr) {
+        static std::atomic<unsigned long long> attr{0};
+        if (first_on_device(attr)) {
             cudaFuncSetAttribute(spread3_hybrid_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM_BYTES);
-            attr = true;
         }
         if (S.nsitems > 0) {
             const int g = persistent_grid(spread3_hybrid_kernel, C::NT, C::SMEM_BYTES, (S.nsitems + C::NWARP - 1) / C::NWARP);
@@ -222,11 +226,10 @@ inline int spread_dispatch(Plan& P, const NodeSet& S, const double* w, double* g
     }
     if (P.dmma) {
         using C = SpreadDCfg;
-        static bool attr = false;
-        if (!attr) {
+        static std::atomic<unsigned long long> attr{0};
+        if (first_on_device(attr)) {
             cudaFuncSetAttribute(spread3_dmma_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM_BYTES);
             cudaFuncSetAttribute(spread3_dmma_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM_BYTES);
-            attr = true;
         }
         if (S.nsitems > 0) {
             const auto kern = S.xpairs ? spread3_dmma_kernel<true> : spread3_dmma_kernel<false>;
@@ -265,10 +268,9 @@ inline int interp_dispatch(Plan& P, const NodeSet& S, const double* grid, double
                            const FusedUpd& fu) {
     if (P.dmma && P.d == 2) {
         using C = Interp2Cfg;
-        static bool attr = false;
-        if (!attr) {
+        static std::atomic<unsigned long long> attr{0};
+        if (first_on_device(attr)) {
             cudaFuncSetAttribute(interp2_dmma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM_BYTES);
-            attr = true;
         }
         if (S.nbatches > 0) {
             const int g = persistent_grid(interp2_dmma_kernel, C::NT, C::SMEM_BYTES, (S.nbatches + C::NWARP - 1) / C::NWARP);
@@ -281,11 +283,10 @@ inline int interp_dispatch(Plan& P, const NodeSet& S, const double* grid, double
     }
     if (P.dmma) {
         using C = InterpDCfg;
-        static bool attr = false;
-        if (!attr) {
+        static std::atomic<unsigned long long> attr{0};
+        if (first_on_device(attr)) {
             cudaFuncSetAttribute(interp3_dmma_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM_BYTES);
             cudaFuncSetAttribute(interp3_dmma_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM_BYTES);
-            attr = true;
         }
         if (S.nbatches > 0) {
             // stage grid blocks when cells average >= 1.5 batches (32 nodes each)
