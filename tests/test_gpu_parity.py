@@ -113,6 +113,62 @@ def test_cell_occupancies_match_gridding_definition(capi, ctx, d, m_w):
     P.close()
 
 
+_VARIANT_SETS = {}
+
+
+def _variant_sets():
+    """Three d = 3 node sets on the unit cube's geometry (N = 16, n = 32): dense (3000 nodes in
+    2^3 cells, ~375 per cell), mid (3000 in 3^3 cells, ~110 per cell) and sparse (300 spread
+    over the box), with their oracle gridding results (computed once)."""
+    if _VARIANT_SETS:
+        return _VARIANT_SETS
+    rng = np.random.default_rng(123)
+    d, n, m_w = 3, 32, 6
+    rho = (0.5 - 1 / 16) / math.sqrt(d)
+    corners = np.array(np.meshgrid(*[[0.0, 1.0]] * d, indexing="ij")).reshape(d, -1).T
+    y = np.concatenate([corners, rng.random((40, d))])
+    for name, k, width in (("dense", 3000, 2), ("mid", 3000, 3), ("sparse", 300, 0)):
+        if width:
+            u = 15.0 + width * rng.random((k, d))   # cells 15 .. 15 + width - 1 per axis
+            x = 0.5 + (u / n - 0.5) / rho
+        else:
+            x = 0.5 + (rng.random((k, d)) - 0.5) * 0.9
+        centre, rho_ref, _ = nfft_ref.geometry(x, y, 1 / 16)
+        xs = nfft_ref.scale(x, centre, rho_ref)
+        w = rng.random(k)
+        G = rng.normal(size=(n,) * d)
+        _VARIANT_SETS[name] = (x, y, w, G, nfft_ref.grid_spread(xs, w, n, m_w, 2.0),
+                               nfft_ref.grid_interp(G, xs, m_w, 2.0), nfft_ref.grid_interp(np.abs(G), xs, m_w, 2.0))
+    return _VARIANT_SETS
+
+
+@pytest.mark.parametrize("env", [{}, {"SK_SEG_DENSE_MIN": "0"}, {"SK_SEG_DENSE_MIN": "1000000000"},
+                                 {"SK_NO_XPAIRS": "1"}, {"SK_SPREAD3_PADDED": "1"}, {"SK_SPREAD3_TMA": "1"},
+                                 {"SK_SPREAD3_HYBRID": "1"}, {"SK_NO_DMMA": "1"}])
+def test_kernel_variants_match_gridding_definition(capi, ctx, env):
+    """Every d = 3 spread/interp variant the plan can select (default shapes, forced dense or
+    32-node segments, no x-pairs, the single-warp padded, TMA-hybrid and two-pass hybrid
+    spreads, the vector path without tensor cores) on dense, mid and sparse cells against the
+    gridding definition."""
+    sets = _variant_sets()
+    old = {k: os.environ.get(k) for k in env}
+    os.environ.update(env)
+    try:
+        for name, (x, y, w, G, g_ref, t_ref, scale) in sets.items():
+            P = capi.Plan(ctx, dev(x), dev(y), 20.0, 16, 2.0, 6)
+            g = capi.nfft_spread(P, 0, dev(w)).cpu().numpy()
+            assert np.abs(g - g_ref).max() <= 1e-13 * np.abs(g_ref).max(), (name, env)
+            t = capi.nfft_interp(P, 0, dev(G)).cpu().numpy()
+            assert (np.abs(t - t_ref) <= 1e-14 * scale).all(), (name, env)
+            P.close()
+    finally:
+        for k, v in old.items():
+            if v is None:
+                del os.environ[k]
+            else:
+                os.environ[k] = v
+
+
 @pytest.mark.parametrize("name", ["c1", "c2", "c3", "c5"])
 def test_kernel_coefficients_match_oracle(capi, ctx, name):
     cfg = get(name)
