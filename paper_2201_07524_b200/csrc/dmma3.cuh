@@ -71,7 +71,16 @@ constexpr int kSegMax = 1024;
 constexpr int kSegHybrid = 128;   // spread3_hybrid_kernel segments (two passes, L2-resident taps)
 constexpr int kSegTmaMax = 64;     // spread3_tma_kernel segments (one TMA-staged buffer each)
 constexpr int kSegTmaPMax = SK_TP_SEG_MAX;   // spread3_tmapad_kernel segments (sparse cells)
-constexpr int kSegTmaPDense = 64;             // spread3_tmapad_kernel segments (dense cells)
+#ifndef SK_TP_SEG_DENSE
+#define SK_TP_SEG_DENSE 64
+#endif
+#ifndef SK_SPREAD3_SUNROLL
+#define SK_SPREAD3_SUNROLL 0   // 0: per shape (see spread3_tmapad_kernel)
+#endif
+#ifndef SK_SPREAD3_PRODFIRST
+#define SK_SPREAD3_PRODFIRST 0
+#endif
+constexpr int kSegTmaPDense = SK_TP_SEG_DENSE;   // spread3_tmapad_kernel segments (dense cells)
 constexpr int kSegDenseMinMean = 200;         // mean nodes per occupied cell for the dense shape
                                               // (measured: c5 x 1793 / y 278 gain, c3 y 136 loses)
 constexpr int kSpreadItemMax = 4096;
@@ -835,6 +844,9 @@ spread3_tmapad_kernel(const SpreadItem* __restrict__ items, int nitems, const Ce
                       const double* __restrict__ taps, const double* __restrict__ w,
                       double* __restrict__ grid, int n) {
     using C = SpreadTPCfg<SEG, NPAIR_>;
+    // k-step unroll (measured): 4 for the dense shape (c5 spread 15.17 -> 14.71 ms with 2),
+    // 8 for the 32-node shape (c3 0.248 -> 0.243 ms)
+    constexpr int kSU = SK_SPREAD3_SUNROLL > 0 ? SK_SPREAD3_SUNROLL : (SEG >= 64 ? 4 : 8);
     constexpr int W = C::W, S = C::S, m = W / 2, NTH = C::NTH, TS = C::TS;
     extern __shared__ __align__(16) double smem[];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -897,7 +909,7 @@ spread3_tmapad_kernel(const SpreadItem* __restrict__ items, int nitems, const Ce
                 fresh = false;
             }
             const int nks = (seg.count + 3) >> 2;
-#pragma unroll 2
+#pragma unroll kSU
             for (int s = 0; s < nks; ++s) {
                 const int jr = 4 * s + q;
                 const bool ok = jr < seg.count;
@@ -919,6 +931,18 @@ spread3_tmapad_kernel(const SpreadItem* __restrict__ items, int nitems, const Ce
                     for (int i = 0; i < 3; ++i) { const double2 v2 = y2[i]; yv[2 * i] = v2.x; yv[2 * i + 1] = v2.y; }
                 }
                 const double zv[3] = {tr[2 * W + g], tr[2 * W + z1], tr[2 * W + 4 + g]};
+#if SK_SPREAD3_PRODFIRST
+                double bp[NTH];   // the k-step's 9 B products first, then its 9 DMMAs
+#pragma unroll
+                for (int j = 0; j < NTH; ++j) {
+                    const int k3 = j / 3, r3 = j % 3;
+                    const double yvv = (r3 == 0) ? yv[2 * k3]
+                                     : ((r3 == 1) ? (g >= 4 ? yv[2 * k3 + 1] : yv[2 * k3]) : yv[2 * k3 + 1]);
+                    bp[j] = yvv * zv[r3];
+                }
+#pragma unroll
+                for (int j = 0; j < NTH; ++j) dmma1684(acc[j][0], acc[j][1], acc[j][2], acc[j][3], a0, a1, bp[j]);
+#else
 #pragma unroll
                 for (int j = 0; j < NTH; ++j) {
                     const int k3 = j / 3, r3 = j % 3;
@@ -926,6 +950,7 @@ spread3_tmapad_kernel(const SpreadItem* __restrict__ items, int nitems, const Ce
                                      : ((r3 == 1) ? (g >= 4 ? yv[2 * k3 + 1] : yv[2 * k3]) : yv[2 * k3 + 1]);
                     dmma1684(acc[j][0], acc[j][1], acc[j][2], acc[j][3], a0, a1, yvv * zv[r3]);
                 }
+#endif
             }
             const bool flush_cell = (sg + 1 >= it.seg_end) || (segs[sg + 1].cell != seg.cell);
             if (flush_cell) {
