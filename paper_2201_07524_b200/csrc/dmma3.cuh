@@ -83,7 +83,10 @@ constexpr int kSegTmaPMax = SK_TP_SEG_MAX;   // spread3_tmapad_kernel segments (
 constexpr int kSegTmaPDense = SK_TP_SEG_DENSE;   // spread3_tmapad_kernel segments (dense cells)
 constexpr int kSegDenseMinMean = 200;         // mean nodes per occupied cell for the dense shape
                                               // (measured: c5 x 1793 / y 278 gain, c3 y 136 loses)
-constexpr int kSpreadItemMax = 4096;
+#ifndef SK_SPREAD_ITEM_MAX
+#define SK_SPREAD_ITEM_MAX 4096
+#endif
+constexpr int kSpreadItemMax = SK_SPREAD_ITEM_MAX;
 
 #ifndef SK_WORKLIST_ONLY   // plan.cu only needs the work-list types above
 
@@ -166,7 +169,13 @@ constexpr int kInterpKUnroll = SK_INTERP3_KUNROLL;
 struct InterpDCfg {
     static constexpr int W = 12, KS = W / 4, NT = SK_INTERP_NT, NWARP = NT / 32, TS = 3 * W;
     static constexpr int NB = kInterpBatch3, NTN = NB / 8;   // nodes / n-tiles per batch
-    static constexpr int XS = W + 2;                          // phi_x row stride (doubles)
+#ifndef SK_INTERP_PREFETCH
+#define SK_INTERP_PREFETCH 1
+#endif
+#ifndef SK_INTERP_XS
+#define SK_INTERP_XS 14
+#endif
+    static constexpr int XS = SK_INTERP_XS;                   // phi_x row stride (doubles)
     static constexpr int GBLK = W * W * W;                    // the cell's 12^3 grid block
     static constexpr size_t SMEM_BYTES = sizeof(double) * NWARP * (NB * XS + GBLK);   // STAGE
     static constexpr size_t SMEM_BYTES_NOSTAGE = sizeof(double) * NWARP * NB * XS;     // more L1
@@ -334,7 +343,7 @@ interp3_dmma_kernel(const CellBatch* __restrict__ batches, int nbatches, const d
             cur_cell = B.cell;
         }
         if (bi + 1 < b_hi)   // next batch of this warp: stream its taps into L2
-            prefetch_range(taps + (long long)Bnext.start * TS, (long long)Bnext.count * TS * 8, lane);
+            if (SK_INTERP_PREFETCH) prefetch_range(taps + (long long)Bnext.start * TS, (long long)Bnext.count * TS * 8, lane);
         if (lane < NB) {   // stage the batch's phi_x rows (lane = node) in this warp's shared table
             const double2* src = reinterpret_cast<const double2*>(T0 + min(lane, last) * TS);
             double2* dst = reinterpret_cast<double2*>(XT + lane * C::XS);
