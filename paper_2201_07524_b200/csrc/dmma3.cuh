@@ -841,7 +841,11 @@ struct SpreadTPCfg {
     static constexpr int PAIR = 2 + REGP + 2 * TBUF + 2 * WBUF;
     static constexpr size_t SMEM_BYTES = sizeof(double) * NPAIR * PAIR;
 };
-using SpreadTPCfgSparse = SpreadTPCfg<kSegTmaPMax, 3>;
+#ifndef SK_TP_NPAIR_SPARSE
+#define SK_TP_NPAIR_SPARSE 3
+#endif
+constexpr int kSparsePairs = SK_TP_NPAIR_SPARSE;   // warp pairs per CTA of the 32-node shape
+using SpreadTPCfgSparse = SpreadTPCfg<kSegTmaPMax, kSparsePairs>;
 using SpreadTPCfgDense = SpreadTPCfg<kSegTmaPDense, 2>;
 
 // XP: segments may hold the nodes of an x-pair of cells (seg.cell is the x-digit-0 cell, its

@@ -169,17 +169,17 @@ inline int spread_dispatch(Plan& P, const NodeSet& S, const double* w, double* g
     if (P.dmma && P.spread_tmapad) {
         static std::atomic<unsigned long long> attr{0};
         if (first_on_device(attr)) {
-            cudaFuncSetAttribute(spread3_tmapad_kernel<kSegTmaPMax, 3, false>,
+            cudaFuncSetAttribute(spread3_tmapad_kernel<kSegTmaPMax, kSparsePairs, false>,
                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SpreadTPCfgSparse::SMEM_BYTES);
-            cudaFuncSetAttribute(spread3_tmapad_kernel<kSegTmaPMax, 3, true>,
+            cudaFuncSetAttribute(spread3_tmapad_kernel<kSegTmaPMax, kSparsePairs, true>,
                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SpreadTPCfgSparse::SMEM_BYTES);
             cudaFuncSetAttribute(spread3_tmapad_kernel<kSegTmaPDense, 2, false>,
                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SpreadTPCfgDense::SMEM_BYTES);
         }
         if (S.nsitems > 0) {
             const auto kern = S.seg_dense ? spread3_tmapad_kernel<kSegTmaPDense, 2, false>
-                              : (S.xpairs ? spread3_tmapad_kernel<kSegTmaPMax, 3, true>
-                                          : spread3_tmapad_kernel<kSegTmaPMax, 3, false>);
+                              : (S.xpairs ? spread3_tmapad_kernel<kSegTmaPMax, kSparsePairs, true>
+                                          : spread3_tmapad_kernel<kSegTmaPMax, kSparsePairs, false>);
             const int np = S.seg_dense ? SpreadTPCfgDense::NPAIR : SpreadTPCfgSparse::NPAIR;
             const int nt = S.seg_dense ? SpreadTPCfgDense::NT : SpreadTPCfgSparse::NT;
             const size_t sm = S.seg_dense ? SpreadTPCfgDense::SMEM_BYTES : SpreadTPCfgSparse::SMEM_BYTES;
