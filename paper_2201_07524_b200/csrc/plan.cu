@@ -829,8 +829,8 @@ int apply_sorted(Plan& P, int transpose, int kernel, const double* w_sorted, dou
     }
     prof_begin(ST_INTERP, s);
     if (fu && fu->x) {
-        // the caller wants x = p / t: fused into the DMMA interpolation when it can be
-        if (P.dmma && P.rpow == 2) {
+        // the caller wants x = p / t: fused into the DMMA (or d = 1) interpolation when it can be
+        if ((P.dmma || P.d == 1) && P.rpow == 2) {
             SK_TRY(launch_interp(P, dst, P.grid, t_sorted, s, *fu));
         } else {
             SK_TRY(launch_interp(P, dst, P.grid, t_sorted, s));

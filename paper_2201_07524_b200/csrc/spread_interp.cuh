@@ -93,6 +93,38 @@ __global__ void interp_v1_kernel(const double* __restrict__ u, long long count, 
     }
 }
 
+// d = 1 (c1): one thread per (node, tap) for the spread and one warp per node for the interp,
+// so the 2m window evaluations (sqrt + sinh each) of a node run in parallel instead of in one
+// thread's dependent sequence (the d = 1 problems are small and latency-bound).
+__global__ void spread_d1_kernel(const double* __restrict__ u, long long count, const double* __restrict__ w,
+                                 Window win, double* __restrict__ grid) {
+    const int W = 2 * win.m;
+    const long long total = count * W;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
+         i += (long long)gridDim.x * blockDim.x) {
+        const long long j = i / W;
+        const int t = (int)(i - j * W);
+        const double uj = u[j], c = floor(uj);
+        const double phi = kb_phi(uj - c + (double)(win.m - 1 - t), win);
+        atomicAdd(&grid[(long long)c - win.m + 1 + t], w[j] * phi);
+    }
+}
+
+__global__ void interp_d1_kernel(const double* __restrict__ u, long long count, Window win,
+                                 const double* __restrict__ grid, double* __restrict__ t_out, const FusedUpd fu) {
+    const int W = 2 * win.m, lane = threadIdx.x & 31;
+    const long long nw = (long long)gridDim.x * (blockDim.x >> 5);
+    for (long long j = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5; j < count; j += nw) {
+        const double uj = u[j], c = floor(uj);
+        double v = 0.0;
+        for (int t = lane; t < W; t += 32)
+            v += kb_phi(uj - c + (double)(win.m - 1 - t), win) * __ldg(&grid[(long long)c - win.m + 1 + t]);
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+        if (lane == 0) emit_t(t_out, fu, j, v);
+    }
+}
+
 inline int v1_grid(long long count) {
     long long g = (count + 127) / 128;
     if (g > 148LL * 32) g = 148LL * 32;
@@ -252,6 +284,13 @@ inline int spread_dispatch(Plan& P, const NodeSet& S, const double* w, double* g
         if (e != cudaSuccess) return set_error(SK_ECUDA, std::string("spread3: ") + cudaGetErrorString(e));
         return SK_OK;
     }
+    if (P.d == 1) {
+        spread_d1_kernel<<<v1_grid(S.count * 2 * P.win.m), 128, 0, s>>>(S.u, S.count, w, P.win, grid);
+        count_launch();
+        cudaError_t e = cudaGetLastError();
+        if (e != cudaSuccess) return set_error(SK_ECUDA, std::string("spread_d1: ") + cudaGetErrorString(e));
+        return SK_OK;
+    }
     const int g = v1_grid(S.count);
     switch (P.d) {
         case 1: spread_v1_kernel<1><<<g, 128, 0, s>>>(S.u, S.count, w, P.win, P.n, grid); break;
@@ -309,6 +348,13 @@ inline int interp_dispatch(Plan& P, const NodeSet& S, const double* grid, double
         }
         cudaError_t e = cudaGetLastError();
         if (e != cudaSuccess) return set_error(SK_ECUDA, std::string("interp3: ") + cudaGetErrorString(e));
+        return SK_OK;
+    }
+    if (P.d == 1) {
+        interp_d1_kernel<<<v1_grid(S.count * 32), 128, 0, s>>>(S.u, S.count, P.win, grid, t, fu);
+        count_launch();
+        cudaError_t e = cudaGetLastError();
+        if (e != cudaSuccess) return set_error(SK_ECUDA, std::string("interp_d1: ") + cudaGetErrorString(e));
         return SK_OK;
     }
     const int g = v1_grid(S.count);
