@@ -27,8 +27,8 @@ import numpy as np
 from . import nfft_ref
 
 
-def geometry(x, y, eps_B):
-    centre, rho, L = nfft_ref.geometry(x, y, eps_B)
+def geometry(x, y, eps_B, lam=None):
+    centre, rho, L = nfft_ref.geometry(x, y, eps_B, lam, r=1)
     return centre, rho, L
 
 
@@ -97,7 +97,7 @@ def fastsum_ndft(x, y, w, lam, N, eps_B, p, near_cells, sigma=2.0, kernel=0):
     y = np.asarray(y, dtype=np.float64).reshape(len(y), -1)
     w = np.asarray(w, dtype=np.float64)
     d = x.shape[1]
-    centre, rho, L = geometry(x, y, eps_B)
+    centre, rho, L = geometry(x, y, eps_B, lam)
     lamp = lam / rho
     a = near_cells / (sigma * N)
     xs, ys = nfft_ref.scale(x, centre, rho), nfft_ref.scale(y, centre, rho)

@@ -40,14 +40,28 @@ from scipy import special
 
 
 # ----------------------------------------------------------------------------- geometry
-def geometry(x, y, eps_B):
-    """Return (centre, rho, L). Reading Q6 of P:L479-486."""
+LAMP_DEGENERATE = 1e-16
+
+
+def geometry(x, y, eps_B, lam=None, r=2):
+    """Return (centre, rho, L). Reading Q6 of P:L479-486.
+
+    Degenerate geometry (every atom at one point, diag = 0; reading Q6b): any rho
+    keeps the nodes in the ball, and as diag -> 0 the rule rho = L / diag sends lam' to 0, where
+    the kernel is constant and its Fourier series exact. The limit is taken at a finite point:
+    rho such that lam' = LAMP_DEGENERATE (lam / rho^2 for r = 2, lam / rho for r = 1), which needs
+    lam; without lam (no kernel involved) rho = 1."""
     pts = np.concatenate([np.asarray(x).reshape(len(x), -1), np.asarray(y).reshape(len(y), -1)])
     lo, hi = pts.min(axis=0), pts.max(axis=0)
     centre = 0.5 * (lo + hi)
     diag = float(np.sqrt(((hi - lo) ** 2).sum()))
     L = 0.5 - eps_B
-    rho = L / diag if diag > 0 else 1.0
+    if diag > 0:
+        rho = L / diag
+    elif lam is None:
+        rho = 1.0
+    else:
+        rho = math.sqrt(lam / LAMP_DEGENERATE) if r == 2 else lam / LAMP_DEGENERATE
     return centre, rho, L
 
 
@@ -238,7 +252,7 @@ def fastsum_ndft(x, y, w, lam, N, eps_B, p, kernel=0, use_closed_form=False):
     x = np.asarray(x).reshape(len(x), -1)
     y = np.asarray(y).reshape(len(y), -1)
     d = x.shape[1]
-    centre, rho, L = geometry(x, y, eps_B)
+    centre, rho, L = geometry(x, y, eps_B, lam)
     lamp = lam / rho ** 2
     xs, ys = scale(x, centre, rho), scale(y, centre, rho)
     ks, kw = band(N, d)
@@ -246,3 +260,100 @@ def fastsum_ndft(x, y, w, lam, N, eps_B, p, kernel=0, use_closed_form=False):
     bflat = B.reshape(-1)          # same itertools.product ordering as band()
     ahat = ndft_adjoint(ks, ys, w)
     return ndft_trafo(ks, kw * bflat * ahat, xs).real
+
+
+# ----------------------------------------------------------------------------- Alg. 2 on the method's operator
+def _axis_phases(pts, N):
+    """Per-axis NDFT phases E_a[i, k] = exp(2 pi i k x_ia), k = -N/2 .. N/2 (axis index k + N/2)."""
+    k1 = np.arange(-N // 2, N // 2 + 1, dtype=np.float64)
+    return [np.exp(2j * math.pi * np.outer(pts[:, a], k1)) for a in range(pts.shape[1])]
+
+
+class FastsumOperator:
+    """The fast summation of Eq. (fastsum) with exact NDFTs, as a reusable linear
+    operator on fixed node sets (the matrix-free form of fastsum_ndft):
+
+        (K~ w)_i = sum_{k in band} kw_k b_k a_k(w) e^{2 pi i k.x'_i},
+        a_k(w)   = sum_j w_j e^{-2 pi i k.y'_j},
+
+    band and weights kw of reading Q8, b_k = bk_sampled (reading Q9) for kernel 0 (exp(-lam c))
+    and kernel 1 (c exp(-lam c)); the transpose swaps the roles of x and y. The d-dimensional
+    NDFT is evaluated axis by axis (e^{2 pi i k.x} = prod_a e^{2 pi i k_a x_a}), so the cost is
+    O(n (N+1)^d) per product without an (N+1)^d x n phase matrix. Used by sinkhorn_fastsum."""
+
+    def __init__(self, x, y, lam, N, eps_B, p):
+        x = np.asarray(x, dtype=np.float64).reshape(len(x), -1)
+        y = np.asarray(y, dtype=np.float64).reshape(len(y), -1)
+        self.d = d = x.shape[1]
+        centre, rho, L = geometry(x, y, eps_B, lam)
+        lamp = lam / rho ** 2
+        self.Ex = _axis_phases(scale(x, centre, rho), N)
+        self.Ey = _axis_phases(scale(y, centre, rho), N)
+        k1 = np.arange(-N // 2, N // 2 + 1)
+        w1 = np.where(np.abs(k1) == N // 2, 0.5, 1.0)
+        kw = w1
+        for _ in range(d - 1):
+            kw = np.multiply.outer(kw, w1)
+        self.coef = [kw * bk_sampled(d, N, lamp, rho, kern, L, p).real for kern in (0, 1)]
+        self.N = N
+
+    @staticmethod
+    def _adjoint(E, w):
+        """a_k = sum_j w_j conj(prod_a E_a[j, k_a]) as an (N+1)^d array."""
+        Ec = [e.conj() for e in E]
+        if len(E) == 1:
+            return Ec[0].T @ w
+        if len(E) == 2:
+            return (Ec[0] * w[:, None]).T @ Ec[1]
+        K = Ec[0].shape[1]
+        yz = (Ec[1][:, :, None] * Ec[2][:, None, :]).reshape(-1, K * K)
+        return ((Ec[0] * w[:, None]).T @ yz).reshape(K, K, K)
+
+    @staticmethod
+    def _trafo(E, F):
+        """t_i = Re sum_k F_k prod_a E_a[i, k_a]."""
+        if len(E) == 1:
+            return (E[0] @ F).real
+        if len(E) == 2:
+            return ((E[0] @ F) * E[1]).sum(axis=1).real
+        K = E[0].shape[1]
+        G = (E[0] @ F.reshape(K, K * K)).reshape(-1, K, K)
+        return np.einsum("ibc,ib,ic->i", G, E[1], E[2]).real
+
+    def apply(self, w, transpose=False, kernel=0):
+        """transpose False: t = K~ w (w on y, t on x); True: t = K~^T w (w on x, t on y)."""
+        src, dst = (self.Ex, self.Ey) if transpose else (self.Ey, self.Ex)
+        w = np.asarray(w, dtype=np.float64)
+        return self._trafo(dst, self.coef[kernel] * self._adjoint(src, w))
+
+
+def sinkhorn_fastsum(x, y, a, b, lam, N, eps_B, p, iters):
+    """Alg. 2 with the method's own fast summation (FastsumOperator: Eq. (fastsum)
+    with exact NDFTs, i.e. the NFFT fast summation without the window error), in the plain
+    (scaling) domain exactly as Alg. 2 states it: alpha~ = 1, then per iteration
+    alpha = p / (K~ alpha~) (odd Delta, Eq. (even_F_sink)) and
+    alpha~ = p~ / (K~^T alpha) (even Delta, Eq. (odd_F_sink)). Returns
+    dict(s_dual, s_cost, alpha, alpha_t, min_t) with
+      s_dual = (1/lam)(1 + sum p log alpha + sum p~ log alpha~ - sum_j (K~^T alpha)_j alpha~_j)
+               (Eq. (14), the Alg. 2 result line P:L732),
+      s_cost = sum_i alpha_i ((c K)~ alpha~)_i  (s~ of Def 3.1 P:L137 through the c exp(-lam c)
+               fast summation).
+    This is the statement of the method whose only error against the dense Alg. 1 is the
+    regularised kernel's Fourier truncation and FP64 rounding of the sums: it isolates the
+    method's error from an implementation's (SURVEY.md §8(c) consequence (1))."""
+    op = FastsumOperator(x, y, lam, N, eps_B, p)
+    a = np.asarray(a, dtype=np.float64)
+    b = np.asarray(b, dtype=np.float64)
+    al, at = np.ones(a.shape[0]), np.ones(b.shape[0])
+    min_t = np.inf
+    for _ in range(iters):
+        t = op.apply(at, False, 0)
+        min_t = min(min_t, float(t.min()))
+        al = a / t
+        tt = op.apply(al, True, 0)
+        min_t = min(min_t, float(tt.min()))
+        at = b / tt
+    S3 = float(op.apply(al, True, 0) @ at)
+    s_dual = (1.0 + float(a @ np.log(al)) + float(b @ np.log(at)) - S3) / lam
+    s_cost = float(al @ op.apply(at, False, 1))
+    return dict(s_dual=s_dual, s_cost=s_cost, alpha=al, alpha_t=at, min_t=min_t)

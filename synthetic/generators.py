@@ -157,6 +157,18 @@ def subsample(cfg: Config, x, y, a, b, seed: int = 0):
             np.ascontiguousarray(a2), np.ascontiguousarray(b2))
 
 
+def small_subsample(cfg: Config, x, y, a, b, k: int):
+    """Seeded k-point subsample per side (stream 4, seed 1) with renormalised weights: the
+    oracle-sized cases of the conditioning tests (dense oracle and fast-summation oracle run
+    in seconds)."""
+    ci = CONFIG_INDEX.get(cfg.name, 0)
+    g = rng(ci, STREAM_SUB, 1)
+    ix = np.sort(g.choice(x.shape[0], size=min(k, x.shape[0]), replace=False))
+    iy = np.sort(g.choice(y.shape[0], size=min(k, y.shape[0]), replace=False))
+    return (np.ascontiguousarray(x[ix]), np.ascontiguousarray(y[iy]),
+            np.ascontiguousarray(a[ix] / a[ix].sum()), np.ascontiguousarray(b[iy] / b[iy].sum()))
+
+
 def check_rows(cfg_index: int, count: int, total: int, seed: int = 0):
     """Seeded sorted target rows for sampled matvec parity (4096 above 1e5 points)."""
     g = rng(cfg_index, STREAM_ROWS, seed)

@@ -340,3 +340,58 @@ def test_measures_examples():
     assert abs(measures.entropy([0.5, 0.25, 0.25]) - 1.5 * math.log(2)) < 1e-15
     assert abs(measures.kl([0.75, 0.25], [0.5, 0.5]) - (0.75 * math.log(1.5) + 0.25 * math.log(0.5))) < 1e-15
     assert measures.kl([0.5, 0.5], [0.5, 0.5]) == 0.0
+
+
+# ---------------------------------------------------------------- Alg. 2 on the method's fast summation
+@pytest.mark.parametrize("d,N", [(1, 32), (2, 16), (3, 12)])
+def test_fastsum_operator_matches_fastsum_ndft(d, N):
+    """FastsumOperator (axis-separable NDFTs) equals fastsum_ndft (one dense band x node phase
+    matrix, pinned against the direct sum above) for both kernels and directions."""
+    rng = np.random.default_rng(20 + d)
+    x, y = rng.random((37, d)), rng.random((41, d))
+    w, wx = rng.random(41), rng.random(37)
+    op = nfft_ref.FastsumOperator(x, y, 20.0, N, 1 / 16, 8)
+    for k in (0, 1):
+        ref = nfft_ref.fastsum_ndft(x, y, w, 20.0, N, 1 / 16, 8, k)
+        reft = nfft_ref.fastsum_ndft(y, x, wx, 20.0, N, 1 / 16, 8, k)
+        assert np.abs(op.apply(w, False, k) - ref).max() <= 1e-14 * np.abs(ref).max()
+        assert np.abs(op.apply(wx, True, k) - reft).max() <= 1e-14 * np.abs(reft).max()
+
+
+def test_sinkhorn_fastsum_equals_dense_when_resolved_and_not_otherwise():
+    """Alg. 2 on the method's operator (nfft_ref.sinkhorn_fastsum) equals the dense log-domain
+    Alg. 1 when the band resolves the kernel (c1 inputs, N = 96: truncation e^-43), and differs
+    from it when it does not (N = 40: the c exp(-lam c) kernel is truncated at ~e^-9), so the
+    function really runs the truncated method and not the exact kernel."""
+    cfg = get("c1")
+    x, y, a, b = make_inputs(cfg)
+    x, y, a, b = x[:300], y[:300], a[:300] / a[:300].sum(), b[:300] / b[:300].sum()
+    ref, _, _ = dense.sinkhorn_divergence(x, y, a, b, cfg.lam, 60)
+    good = nfft_ref.sinkhorn_fastsum(x, y, a, b, cfg.lam, 96, cfg.eps_B, cfg.p, 60)
+    assert abs(good["s_cost"] - ref["s_cost"]) <= 1e-9 * ref["s_cost"]
+    assert abs(good["s_dual"] - ref["s_dual"]) <= 1e-9 * abs(ref["s_dual"])
+    # the scalings are Alg. 1's: column marginal exact after the v-update (P:L336)
+    op = nfft_ref.FastsumOperator(x, y, cfg.lam, 96, cfg.eps_B, cfg.p)
+    col = good["alpha_t"] * op.apply(good["alpha"], True, 0)
+    assert np.abs(col - b).max() <= 1e-14
+    bad = nfft_ref.sinkhorn_fastsum(x, y, a, b, cfg.lam, 40, cfg.eps_B, cfg.p, 60)
+    assert abs(bad["s_cost"] - ref["s_cost"]) >= 1e-6 * ref["s_cost"]
+
+
+@pytest.mark.parametrize("d", [1, 2, 3])
+def test_degenerate_geometry_limit(d):
+    """Reading Q6b: all atoms at one point (diag = 0). The plan takes the limit diag -> 0 of
+    rho = L / diag (lam' = 1e-16), where K is constant: the fast summation returns sum_j w_j for
+    K and 0 for c K (c = 0) to rounding at any N, and Alg. 2 gives s~ = 0, s = -(H(a)+H(b))/lam."""
+    x, y = np.full((5, d), 0.3), np.full((4, d), 0.3)
+    w = np.random.default_rng(d).random(4)
+    c, rho, L = nfft_ref.geometry(x, y, 1 / 16, 7.0)
+    assert abs(7.0 / rho ** 2 - nfft_ref.LAMP_DEGENERATE) <= 1e-30
+    for N in (16, 32):
+        t0 = nfft_ref.fastsum_ndft(x, y, w, 7.0, N, 1 / 16, 8, 0)
+        t1 = nfft_ref.fastsum_ndft(x, y, w, 7.0, N, 1 / 16, 8, 1)
+        assert np.abs(t0 - w.sum()).max() <= 4e-16 * w.sum() and np.abs(t1).max() <= 1e-20
+    a, b = np.full(5, 0.2), np.full(4, 0.25)
+    r = nfft_ref.sinkhorn_fastsum(x, y, a, b, 7.0, 16, 1 / 16, 8, 3)
+    assert abs(r["s_cost"]) <= 1e-20
+    assert abs(r["s_dual"] + (math.log(5) + math.log(4)) / 7.0) <= 1e-15
