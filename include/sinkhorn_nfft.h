@@ -31,8 +31,10 @@ extern "C" {
 enum {
     SK_OK = 0,
     SK_EINVAL = 1,          /* bad argument: d not in {1,2,3}, N odd or < 2, sigma*N not an even
-                               integer, sigma*N < 4*m_w, m_w not in [2,8], lambda <= 0, eps_B not
-                               in (0,1/4), p_smooth < 1, count < 0, NULL pointer ... */
+                               integer, sigma*N < 4*m_w, (sigma*N)^d >= 2^31, m_w not in [2,8],
+                               lambda <= 0, eps_B not in (0,1/4), p_smooth < 1, count < 0, NULL
+                               pointer, weights a / b not all > 0 or not summing to 1 +- 1e-12
+                               over all ranks (sinkhorn_run, sinkhorn_solve) ... */
     SK_EGEOMETRY = 2,       /* a node is NaN/Inf or falls outside the ball |x'| <= 1/4 - eps_B/2
                                after scaling ("we assume that |x_j| <= L/2") */
     SK_ENONPOS = 3,         /* a fast-summation denominator t_i <= 1e-300 (or non-finite) in an
@@ -56,12 +58,19 @@ typedef struct {
                                     iterate entering the last iteration's u-update, i.e. after the
                                     previous v-update (the second term is 0 there);
                                     global over ranks */
-    int       bad_iter;          /* SK_ENONPOS: iteration of the first non-positive denominator */
-    long long bad_index;         /* SK_ENONPOS: its caller-order index (local to the rank) */
+    int       bad_iter;          /* SK_ENONPOS: iteration (0-based) of the first non-positive
+                                    denominator over all ranks; -1 otherwise */
+    long long bad_index;         /* SK_ENONPOS: its caller-order index, local to rank bad_rank
+                                    (-1 on the other ranks) */
     double    kappa_log10_est;   /* log10( ||v||_1 / min_i (K v)_i ) at the last u-update: the
                                     conditioning that amplifies the absolute fast-summation error
-                                     */
+                                    (DESIGN.md "Conditioning"); global over ranks */
     double    seconds;           /* device time of the iteration loop (CUDA events) */
+    double    kappa_u_log10_est; /* log10( ||u||_1 / min_j (K^T u)_j ) at the last v-update */
+    int       bad_side;          /* SK_ENONPOS: 0 = u-update (K v), 1 = v-update (K^T u); -1 otherwise */
+    int       bad_rank;          /* SK_ENONPOS: rank holding the node; -1 otherwise. (bad_iter,
+                                    bad_side, bad_rank, bad_index) describe one event: the earliest
+                                    iteration, u before v, then the lowest rank and sorted index */
 } sk_run_info;
 
 /* Create a context on `device` (the current CUDA device is switched to it). rank/world_size
@@ -131,7 +140,9 @@ int fastsum_apply(sk_plan_t plan, int transpose, int kernel, const double* w, do
  *   u <- a / (K v), v <- b / (K^T u)   (each K product = one fast summation)
  * u, v: in = starting values (all-ones for a cold start), out = final scalings,
  * caller order. tol > 0 stops early once the residual <= tol (checked every iteration);
- * tol == 0 runs exactly `iters`. rescale_policy (Eq. (scale), reading Q4):
+ * tol == 0 runs exactly `iters` (< 2^24). a and b are checked first: every entry > 0 and each
+ * summing to 1 +- 1e-12 over all ranks, else SK_EINVAL. SK_ENONPOS: some t_i <= 1e-300 (or
+ * non-finite) in an update; all ranks return it, info describes the first event. rescale_policy (Eq. (scale), reading Q4):
  * 0 none, 1 v <- v / geomean(v), 2 v <- v / max(v) before every u-update. info: host,
  * may be NULL. Synchronises the stream. */
 int sinkhorn_run(sk_plan_t plan, const double* a, const double* b, int iters, double tol,
@@ -183,7 +194,12 @@ int nfft_interp(sk_plan_t plan, int side, const double* grid, double* t);
  *   out[7] band length per axis (N+1), out[8] d, out[9] total nodes x (all ranks),
  *   out[10] total nodes y (all ranks), out[11..13] first grid index of the exchange box per
  *   axis, out[14..16] its extent per axis (the cells any node window touches; only this box
- *   is all-reduced across ranks), out[17] box cells. out must hold 18 doubles.
+ *   is all-reduced across ranks), out[17] box cells; accuracy report of the plan:
+ *   out[18], out[19] sum of |b_k| of K~ (kernel 0, 1) outside the N-band, measured on the (2N)^d
+ *   sampling grid (a pointwise bound on the Fourier truncation |K~ - K~_N|, absolute: kernel 0
+ *   has K(0) = 1); out[20] K(L) = exp(-lambda' L^r) (the regularisation K_B of P:L481-502 is
+ *   inert when this is negligible); out[21] exp(-pi^2 (N/2)^2 / lambda') (r = 2: the first
+ *   dropped Gaussian coefficient ratio; NaN for r = 1). out must hold 22 doubles.
  * fastsum_coefficients: b (host, (N+1)^d, index prod over axes of (k_a + N/2), row-major):
  *   the Fourier coefficients b_k of K~_per (kernel 0 or 1) on k in {-N/2..N/2}^d. */
 int fastsum_plan_info(sk_plan_t plan, double* out);

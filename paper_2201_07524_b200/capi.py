@@ -41,7 +41,8 @@ class PlanOpts(ctypes.Structure):
 class RunInfo(ctypes.Structure):
     _fields_ = [("iters_done", ctypes.c_int), ("residual", ctypes.c_double), ("bad_iter", ctypes.c_int),
                 ("bad_index", ctypes.c_longlong), ("kappa_log10_est", ctypes.c_double),
-                ("seconds", ctypes.c_double)]
+                ("seconds", ctypes.c_double), ("kappa_u_log10_est", ctypes.c_double), ("bad_side", ctypes.c_int),
+                ("bad_rank", ctypes.c_int)]
 
     def asdict(self):
         return {f: getattr(self, f) for f, _ in self._fields_}
@@ -98,6 +99,13 @@ def _ptr(t):
     if not t.is_cuda or t.dtype != torch.float64 or not t.is_contiguous():
         raise ValueError("expected a contiguous CUDA float64 tensor")
     return ctypes.c_void_p(t.data_ptr()) if t.numel() else None
+
+
+def _ptr_n(t, n, what):
+    """_ptr with a length check against the plan's node count (the library trusts lengths)."""
+    if t is not None and t.numel() != n:
+        raise ValueError(f"{what}: expected {n} elements, got {t.numel()}")
+    return _ptr(t)
 
 
 def _hptr(a):
@@ -207,12 +215,13 @@ class Plan:
             pass
 
     def info(self) -> dict:
-        out = (ctypes.c_double * 18)()
+        out = (ctypes.c_double * 22)()
         _check(_lib.fastsum_plan_info(self.handle, out))
         return dict(centre=list(out[0:3]), rho=out[3], lambda_p=out[4], L=out[5], n_grid=out[6],
                     band=out[7], d=out[8], total_x=out[9], total_y=out[10],
                     box_lo=[int(v) for v in out[11:14]], box_n=[int(v) for v in out[14:17]],
-                    box_size=int(out[17]))
+                    box_size=int(out[17]), band_tail=(out[18], out[19]), K_at_L=out[20],
+                    gauss_trunc=out[21])
 
     def coefficients(self, kernel: int = 0):
         import numpy as np
@@ -226,20 +235,21 @@ def fastsum_apply(plan: Plan, w: torch.Tensor, transpose: int = 0, kernel: int =
     """transpose 0: t = K w (w on y, t on x); 1: t = K^T w. kernel 0: exp(-lam c); 1: c exp(-lam c)."""
     cnt = plan.m if transpose else plan.n
     t = out if out is not None else torch.empty(cnt, dtype=torch.float64, device=w.device)
-    _check(_lib.fastsum_apply(plan.handle, int(transpose), int(kernel), _ptr(w), _ptr(t)))
+    _check(_lib.fastsum_apply(plan.handle, int(transpose), int(kernel), _ptr_n(w, plan.n if transpose else plan.m, "w"),
+                              _ptr_n(t, cnt, "t")))
     return t
 
 
 def nfft_spread(plan: Plan, side: int, w: torch.Tensor):
     g = torch.empty((plan.grid_n,) * plan.d, dtype=torch.float64, device=w.device)
-    _check(_lib.nfft_spread(plan.handle, int(side), _ptr(w), _ptr(g)))
+    _check(_lib.nfft_spread(plan.handle, int(side), _ptr_n(w, plan.n if side == 0 else plan.m, "w"), _ptr(g)))
     return g
 
 
 def nfft_interp(plan: Plan, side: int, grid: torch.Tensor):
     cnt = plan.n if side == 0 else plan.m
     t = torch.empty(cnt, dtype=torch.float64, device=grid.device)
-    _check(_lib.nfft_interp(plan.handle, int(side), _ptr(grid.contiguous()), _ptr(t)))
+    _check(_lib.nfft_interp(plan.handle, int(side), _ptr_n(grid.contiguous(), plan.grid_n ** plan.d, "grid"), _ptr(t)))
     return t
 
 
@@ -248,8 +258,8 @@ def sinkhorn_run(plan: Plan, a, b, iters: int, tol: float = 0.0, rescale_policy:
     u = torch.ones(plan.n, dtype=torch.float64, device=a.device) if u is None else u
     v = torch.ones(plan.m, dtype=torch.float64, device=a.device) if v is None else v
     info = RunInfo()
-    code = _lib.sinkhorn_run(plan.handle, _ptr(a), _ptr(b), int(iters), float(tol), int(rescale_policy),
-                             _ptr(u), _ptr(v), ctypes.byref(info))
+    code = _lib.sinkhorn_run(plan.handle, _ptr_n(a, plan.n, "a"), _ptr_n(b, plan.m, "b"), int(iters), float(tol),
+                             int(rescale_policy), _ptr_n(u, plan.n, "u"), _ptr_n(v, plan.m, "v"), ctypes.byref(info))
     _check(code, info)
     return u, v, info
 
@@ -265,8 +275,9 @@ def sinkhorn_run_trace(plan: Plan, a, b, iters: int, tol: float = 0.0, rescale_p
     v = torch.ones(plan.m, dtype=torch.float64, device=a.device) if v is None else v
     info = RunInfo()
     tr = np.empty((max(int(iters), 0), 6))
-    code = _lib.sinkhorn_run_trace(plan.handle, _ptr(a), _ptr(b), int(iters), float(tol), int(rescale_policy),
-                                   _ptr(u), _ptr(v), ctypes.byref(info), tr.ctypes.data_as(_dp))
+    code = _lib.sinkhorn_run_trace(plan.handle, _ptr_n(a, plan.n, "a"), _ptr_n(b, plan.m, "b"), int(iters),
+                                   float(tol), int(rescale_policy), _ptr_n(u, plan.n, "u"), _ptr_n(v, plan.m, "v"),
+                                   ctypes.byref(info), tr.ctypes.data_as(_dp))
     _check(code, info)
     return u, v, info, tr
 
@@ -274,8 +285,8 @@ def sinkhorn_run_trace(plan: Plan, a, b, iters: int, tol: float = 0.0, rescale_p
 def sinkhorn_divergence(plan: Plan, a, b, u, v):
     """Returns (s_dual, s_cost)."""
     sd, sc = ctypes.c_double(), ctypes.c_double()
-    _check(_lib.sinkhorn_divergence(plan.handle, _ptr(a), _ptr(b), _ptr(u), _ptr(v), ctypes.byref(sd),
-                                    ctypes.byref(sc)))
+    _check(_lib.sinkhorn_divergence(plan.handle, _ptr_n(a, plan.n, "a"), _ptr_n(b, plan.m, "b"),
+                                    _ptr_n(u, plan.n, "u"), _ptr_n(v, plan.m, "v"), ctypes.byref(sd), ctypes.byref(sc)))
     return sd.value, sc.value
 
 

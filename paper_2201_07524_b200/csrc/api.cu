@@ -395,6 +395,14 @@ int fastsum_plan_info(sk_plan_t plan, double* out) {
         out[14 + a] = a < P.d ? P.box_n[a] : 1.0;
     }
     out[17] = (double)P.box_size;
+    // accuracy report: the band's dropped Fourier mass per kernel (pointwise bound on the
+    // truncation of K~), K at the regularisation radius L (K_B is inert when tiny) and, for
+    // r = 2, the Gaussian's first dropped 1-D coefficient ratio exp(-pi^2 (N/2)^2 / lambda')
+    out[18] = P.acc_tail[0];
+    out[19] = P.acc_tail[1];
+    out[20] = P.rpow == 2 ? exp(-P.lambda_p * P.L * P.L) : exp(-P.lambda_p * P.L);
+    const double pi = 3.141592653589793238462643;
+    out[21] = P.rpow == 2 ? exp(-pi * pi * (P.N / 2.0) * (P.N / 2.0) / P.lambda_p) : NAN;
     return SK_OK;
 }
 
@@ -413,6 +421,44 @@ static int finalize_update(Plan& P, double* out) {
     return launch_finalize_partials(P.red, kUpdBlocks, kUpdVals, out, P.ctx->stream);
 }
 
+// Weight check of the boundary: a, b > 0 and each sums to 1 +- kWeightTol over all
+// ranks (the measures of Alg. 2 are probability vectors). a_s, b_s hold the sorted copies.
+constexpr double kWeightTol = 1e-12;
+static int check_weights(Plan& P) {
+    Ctx* C = P.ctx;
+    cudaStream_t s = C->stream;
+    double* r = slot(P, SL_SCALARS);   // [0] sum a, [1] sum b, [2] min a, [3] min b (+ scratch)
+    SK_TRY(launch_reduce_sum_log(nullptr, P.a_s, P.side[0].count, slot(P, SL_A), 1, s));
+    SK_TRY(launch_reduce_sum_log(nullptr, P.b_s, P.side[1].count, slot(P, SL_B), 1, s));
+    SK_TRY(launch_reduce_sum_log(nullptr, P.a_s, P.side[0].count, slot(P, SL_C), 5, s));
+    SK_TRY(launch_reduce_sum_log(nullptr, P.b_s, P.side[1].count, slot(P, SL_D), 5, s));
+    for (int k = 0; k < 4; ++k)
+        SK_CUDA(cudaMemcpyAsync(r + k, slot(P, SL_A + k), sizeof(double), cudaMemcpyDeviceToDevice, s));
+    SK_TRY(allreduce_sum(C, r, 2));
+    SK_TRY(allreduce_minmax(C, r + 2, r + 600, 2));
+    SK_CUDA(cudaMemcpyAsync(P.host_red, r, sizeof(double) * 4, cudaMemcpyDeviceToHost, s));
+    SK_CUDA(cudaStreamSynchronize(s));
+    const double* h = P.host_red;
+    if (!(h[2] > 0.0) || !(h[3] > 0.0))
+        return set_error(SK_EINVAL, "weights must be > 0 (min a = " + std::to_string(h[2]) +
+                                        ", min b = " + std::to_string(h[3]) + ")");
+    if (!(fabs(h[0] - 1.0) <= kWeightTol) || !(fabs(h[1] - 1.0) <= kWeightTol)) {
+        char msg[160];
+        snprintf(msg, sizeof(msg), "weights must sum to 1 +- 1e-12 over all ranks (sum a - 1 = %.3e, sum b - 1 = %.3e)",
+                 h[0] - 1.0, h[1] - 1.0);
+        return set_error(SK_EINVAL, msg);
+    }
+    return SK_OK;
+}
+
+// Min over ranks of the two packed SK_ENONPOS words (uint64; ncclUint64 ncclMin).
+static int allreduce_bad(Ctx* c, unsigned long long* bad) {
+    if (c->emulated || !c->nccl_comm) return SK_OK;
+    SK_NCCL(g_nccl.allReduce(bad, bad, 2, ncclUint64, ncclMin, (ncclComm_t)c->nccl_comm, c->stream));
+    count_launch();
+    return SK_OK;
+}
+
 // Alg. 2. trace (host, may be NULL): per iteration kTraceVals doubles, see
 // sinkhorn_run_trace in include/sinkhorn_nfft.h.
 constexpr int kTraceVals = 6;
@@ -426,15 +472,30 @@ static int run_impl(sk_plan_t plan, const double* a, const double* b, int iters,
     const NodeSet& Y = P.side[1];
     if (iters < 0 || tol < 0 || rescale_policy < 0 || rescale_policy > 2)
         return set_error(SK_EINVAL, "bad iters/tol/rescale_policy");
+    if (iters >= (1 << 24)) return set_error(SK_EINVAL, "iters must be < 2^24");
     if ((X.count > 0 && (!a || !u)) || (Y.count > 0 && (!b || !v))) return set_error(SK_EINVAL, "NULL a/b/u/v");
     SK_TRY(launch_permute_in(a, X.perm, X.count, P.a_s, s));
     SK_TRY(launch_permute_in(b, Y.perm, Y.count, P.b_s, s));
+    SK_TRY(check_weights(P));
     SK_TRY(launch_permute_in(u, X.perm, X.count, P.u_s, s));
     SK_TRY(launch_permute_in(v, Y.perm, Y.count, P.v_s, s));
-    int hflag[4] = {0x7fffffff, 0x7fffffff, 0x7fffffff, 0x7fffffff};
-    SK_CUDA(cudaMemcpyAsync(P.flag, hflag, sizeof(hflag), cudaMemcpyHostToDevice, s));
-    double* trace_dev = nullptr;
-    if (trace && iters > 0) SK_TRY(dev_alloc((void**)&trace_dev, sizeof(double) * kTraceVals * iters, s));
+    const unsigned long long nobad[2] = {kNoBad, kNoBad};
+    SK_CUDA(cudaMemcpyAsync(P.bad64, nobad, sizeof(nobad), cudaMemcpyHostToDevice, s));
+    // resources released on every exit path
+    struct Scoped {
+        cudaStream_t s;
+        cudaEvent_t e0 = nullptr, e1 = nullptr;
+        double* trace_dev = nullptr;
+        cudaGraphExec_t exec = nullptr;
+        ~Scoped() {
+            if (exec) cudaGraphExecDestroy(exec);
+            if (e0) cudaEventDestroy(e0);
+            if (e1) cudaEventDestroy(e1);
+            dev_free(trace_dev, s);
+        }
+    } R{s};
+    if (trace && iters > 0) SK_TRY(dev_alloc((void**)&R.trace_dev, sizeof(double) * kTraceVals * iters, s));
+    double* const trace_dev = R.trace_dev;
     // per half-step (residual, KL, sum p log x) from the finalized update slot
     auto record = [&](int it, int half) -> int {
         double* r = slot(P, SL_C);
@@ -444,11 +505,10 @@ static int run_impl(sk_plan_t plan, const double* a, const double* b, int iters,
         SK_CUDA(cudaMemcpyAsync(dst + 1, r + 2, 2 * sizeof(double), cudaMemcpyDeviceToDevice, s));
         return SK_OK;
     };
-    cudaEvent_t e0, e1;
-    cudaEventCreate(&e0);
-    cudaEventCreate(&e1);
-    cudaEventRecord(e0, s);
-    double resid = NAN, kappa = NAN;
+    SK_CUDA(cudaEventCreate(&R.e0));
+    SK_CUDA(cudaEventCreate(&R.e1));
+    SK_CUDA(cudaEventRecord(R.e0, s));
+    double resid = NAN, kappa = NAN, kappa_u = NAN;
     int done = 0;
     // one iteration of Alg. 2; it < 0: inside a CUDA graph, the iteration number for error
     // reports comes from the device counter P.flag[4]
@@ -469,7 +529,8 @@ static int run_impl(sk_plan_t plan, const double* a, const double* b, int iters,
         // trip through HBM, one kernel fewer); otherwise the update kernel also reduces.
         const int want_u = trace_dev ? 2 : ((tol > 0 || last) ? 1 : 0);
         FusedUpd fu_u;
-        fu_u.p = P.a_s; fu_u.x = P.u_s; fu_u.bad = P.flag; fu_u.iter_dev = iter_dev; fu_u.iter = it;
+        fu_u.p = P.a_s; fu_u.x = P.u_s; fu_u.bad = P.bad64; fu_u.iter_dev = iter_dev; fu_u.iter = it;
+        fu_u.rank = C->rank;
         SK_TRY(apply_sorted(P, 0, 0, P.v_s, P.t_sorted, want_u ? nullptr : &fu_u));
         if (want_u) {
             prof_begin(ST_UPDATE, s);
@@ -478,16 +539,21 @@ static int run_impl(sk_plan_t plan, const double* a, const double* b, int iters,
         }
         if (tol > 0 || last) SK_TRY(finalize_update(P, slot(P, SL_UPD)));
         if (trace_dev) SK_TRY(record(it, 0));
-        // even Delta: t~ = K^T u, v = b / t~   (Eq. (odd_F_sink))
+        // even Delta: t~ = K^T u, v = b / t~   (Eq. (odd_F_sink)); the last one also
+        // reduces min t~ and ||u||_1 for the u-side conditioning estimate
+        if (last) SK_TRY(launch_reduce_sum_log(nullptr, P.u_s, X.count, slot(P, SL_A), 1, s));
+        const int want_v = trace_dev ? 2 : (last ? 1 : 0);
         FusedUpd fu_v;
-        fu_v.p = P.b_s; fu_v.x = P.v_s; fu_v.bad = P.flag + 2; fu_v.iter_dev = iter_dev; fu_v.iter = it;
-        SK_TRY(apply_sorted(P, 1, 0, P.u_s, P.t_sorted, trace_dev ? nullptr : &fu_v));
-        if (trace_dev) {
+        fu_v.p = P.b_s; fu_v.x = P.v_s; fu_v.bad = P.bad64 + 1; fu_v.iter_dev = iter_dev; fu_v.iter = it;
+        fu_v.rank = C->rank;
+        SK_TRY(apply_sorted(P, 1, 0, P.u_s, P.t_sorted, want_v ? nullptr : &fu_v));
+        if (want_v) {
             prof_begin(ST_UPDATE, s);
-            SK_TRY(launch_update(P, 1, P.t_sorted, P.b_s, P.v_s, 2, it, iter_dev, s));
+            SK_TRY(launch_update(P, 1, P.t_sorted, P.b_s, P.v_s, want_v, it, iter_dev, s));
             prof_end(ST_UPDATE, s);
-            SK_TRY(record(it, 1));
         }
+        if (last) SK_TRY(finalize_update(P, slot(P, SL_B)));
+        if (trace_dev) SK_TRY(record(it, 1));
         return SK_OK;
     };
     int it0 = 0;
@@ -499,7 +565,6 @@ static int run_impl(sk_plan_t plan, const double* a, const double* b, int iters,
         int zero = 0;
         SK_CUDA(cudaMemcpyAsync(P.flag + 4, &zero, sizeof(int), cudaMemcpyHostToDevice, s));
         cudaGraph_t graph = nullptr;
-        cudaGraphExec_t exec = nullptr;
         const long long l0 = g_launches.load();
         // capture on the plan's private stream (the caller's may be the legacy default stream,
         // which cannot be captured); the graph is then launched on the caller's stream
@@ -520,15 +585,14 @@ static int run_impl(sk_plan_t plan, const double* a, const double* b, int iters,
         if (st) { if (graph) cudaGraphDestroy(graph); return st; }
         if (ce != cudaSuccess) return set_error(SK_ECUDA, std::string("graph capture: ") + cudaGetErrorString(ce));
         const long long per_iter = g_launches.load() - l0;
-        ce = cudaGraphInstantiate(&exec, graph, 0);
+        ce = cudaGraphInstantiate(&R.exec, graph, 0);
         cudaGraphDestroy(graph);
         if (ce != cudaSuccess) return set_error(SK_ECUDA, std::string("graph instantiate: ") + cudaGetErrorString(ce));
         for (int it = 0; it < iters - 1; ++it) {
-            ce = cudaGraphLaunch(exec, s);
-            if (ce != cudaSuccess) { cudaGraphExecDestroy(exec); return set_error(SK_ECUDA, std::string("graph launch: ") + cudaGetErrorString(ce)); }
+            ce = cudaGraphLaunch(R.exec, s);
+            if (ce != cudaSuccess) return set_error(SK_ECUDA, std::string("graph launch: ") + cudaGetErrorString(ce));
         }
         count_launch(per_iter * (iters - 2));   // the capture counted one iteration's kernels
-        cudaGraphExecDestroy(exec);
         it0 = iters - 1;
         done = iters - 1;
     }
@@ -541,51 +605,70 @@ static int run_impl(sk_plan_t plan, const double* a, const double* b, int iters,
             // residual: sum over ranks; min t: min over ranks; ||v||_1: sum over ranks
             SK_TRY(allreduce_sum(C, r, 1));
             SK_TRY(allreduce_minmax(C, r + 1, r + 600, 1));
-            if (last) SK_TRY(allreduce_sum(C, slot(P, SL_D), 1));
+            if (last) {
+                SK_TRY(allreduce_sum(C, slot(P, SL_D), 1));
+                SK_TRY(allreduce_sum(C, slot(P, SL_A), 1));
+                SK_TRY(allreduce_minmax(C, slot(P, SL_B) + 1, slot(P, SL_B) + 600, 1));
+                SK_CUDA(cudaMemcpyAsync(P.host_red + 2, slot(P, SL_D), sizeof(double), cudaMemcpyDeviceToHost, s));
+                SK_CUDA(cudaMemcpyAsync(P.host_red + 3, slot(P, SL_A), sizeof(double), cudaMemcpyDeviceToHost, s));
+                SK_CUDA(cudaMemcpyAsync(P.host_red + 4, slot(P, SL_B) + 1, sizeof(double), cudaMemcpyDeviceToHost, s));
+            }
             SK_CUDA(cudaMemcpyAsync(P.host_red, r, sizeof(double) * 2, cudaMemcpyDeviceToHost, s));
-            if (last) SK_CUDA(cudaMemcpyAsync(P.host_red + 2, slot(P, SL_D), sizeof(double), cudaMemcpyDeviceToHost, s));
             SK_CUDA(cudaStreamSynchronize(s));
             resid = P.host_red[0];
-            if (last) kappa = log10(P.host_red[2] / P.host_red[1]);
+            if (last) {
+                kappa = log10(P.host_red[2] / P.host_red[1]);     // ||v||_1 / min (K v)
+                kappa_u = log10(P.host_red[3] / P.host_red[4]);   // ||u||_1 / min (K^T u)
+            }
             if (tol > 0 && resid <= tol) break;
         }
     }
-    cudaEventRecord(e1, s);
+    SK_CUDA(cudaEventRecord(R.e1, s));
     if (trace_dev) {
         // every trace entry is a sum over nodes: one all-reduce over ranks
         SK_TRY(allreduce_sum(C, trace_dev, (long long)kTraceVals * iters));
         for (int i = 0; i < kTraceVals * iters; ++i) trace[i] = NAN;
         SK_CUDA(cudaMemcpyAsync(trace, trace_dev, sizeof(double) * kTraceVals * done, cudaMemcpyDeviceToHost, s));
-        SK_CUDA(cudaStreamSynchronize(s));
-        dev_free(trace_dev, s);
     }
     SK_TRY(launch_permute_out(P.u_s, X.perm, X.count, u, s));
     SK_TRY(launch_permute_out(P.v_s, Y.perm, Y.count, v, s));
-    SK_CUDA(cudaMemcpyAsync(hflag, P.flag, sizeof(hflag), cudaMemcpyDeviceToHost, s));
+    // SK_ENONPOS decided on the global (min over ranks) event words, so every rank agrees
+    SK_TRY(allreduce_bad(C, P.bad64));
+    unsigned long long hbad[2];
+    SK_CUDA(cudaMemcpyAsync(hbad, P.bad64, sizeof(hbad), cudaMemcpyDeviceToHost, s));
     SK_CUDA(cudaStreamSynchronize(s));
     float ms = 0.f;
-    cudaEventElapsedTime(&ms, e0, e1);
-    cudaEventDestroy(e0);
-    cudaEventDestroy(e1);
+    cudaEventElapsedTime(&ms, R.e0, R.e1);
     if (info) {
         info->iters_done = done;
         info->residual = resid;
         info->kappa_log10_est = kappa;
+        info->kappa_u_log10_est = kappa_u;
         info->seconds = ms * 1e-3;
         info->bad_iter = -1;
         info->bad_index = -1;
+        info->bad_side = -1;
+        info->bad_rank = -1;
     }
-    if (hflag[0] != 0x7fffffff || hflag[2] != 0x7fffffff) {
-        int side = hflag[0] != 0x7fffffff ? 0 : 1;
-        int sidx = hflag[side * 2];
+    if (hbad[0] != kNoBad || hbad[1] != kNoBad) {
+        // the earlier iteration wins; within one iteration the u-update (side 0) comes first
+        const int it0b = (int)(hbad[0] >> 40), it1b = (int)(hbad[1] >> 40);
+        const int side = (hbad[0] != kNoBad && (hbad[1] == kNoBad || it0b <= it1b)) ? 0 : 1;
+        const unsigned long long w = hbad[side];
+        const int brank = (int)((w >> 32) & 0xff), sidx = (int)(w & 0xffffffffULL);
         int hperm = -1;
-        cudaMemcpy(&hperm, P.side[side].perm + sidx, sizeof(int), cudaMemcpyDeviceToHost);
+        if (brank == C->rank || C->emulated)
+            SK_CUDA(cudaMemcpy(&hperm, P.side[side].perm + sidx, sizeof(int), cudaMemcpyDeviceToHost));
         if (info) {
-            info->bad_iter = hflag[side * 2 + 1];
+            info->bad_iter = (int)(w >> 40);
             info->bad_index = hperm;
+            info->bad_side = side;
+            info->bad_rank = brank;
         }
-        return set_error(SK_ENONPOS, std::string("non-positive fast-summation denominator on side ") +
-                                         std::to_string(side) + " at caller index " + std::to_string(hperm));
+        return set_error(SK_ENONPOS, "non-positive fast-summation denominator in iteration " +
+                                         std::to_string((int)(w >> 40)) + " on side " + std::to_string(side) +
+                                         " at caller index " + std::to_string(hperm) + " of rank " +
+                                         std::to_string(brank));
     }
     if (tol > 0 && !(resid <= tol)) return set_error(SK_ENOTCONVERGED, "residual above tol");
     return SK_OK;

@@ -97,9 +97,10 @@ struct Spread2Cfg {
 
 __global__ void __launch_bounds__(128, 4)
 spread2_dmma_kernel(const SpreadItem* __restrict__ items, int nitems, const CellBatch* __restrict__ segs,
-                    const double* __restrict__ taps, const double* __restrict__ w,
-                    double* __restrict__ grid, int n) {
+                    const double* __restrict__ taps, const double* __restrict__ w, const GridAcc ga) {
     using C = Spread2Cfg;
+    const int n = ga.n;
+    const double gscale = grid_scale(ga);
     constexpr int W = C::W, S = C::S, m = W / 2, TS = C::TS;
     extern __shared__ __align__(16) double smem[];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -152,7 +153,7 @@ spread2_dmma_kernel(const SpreadItem* __restrict__ items, int nitems, const Cell
         const int gx0 = kSup2 * sx - (m - 1), gy0 = kSup2 * sy - (m - 1);
         for (int i = lane; i < C::REG; i += 32) {
             const double v = REGm[i];
-            if (v != 0.0) atomicAdd(&grid[(long long)(gx0 + i / S) * n + (gy0 + i % S)], v);
+            if (v != 0.0) grid_add<2>(ga, gscale, gx0 + i / S, gy0 + i % S, 0, v);
         }
         __syncwarp();
     }

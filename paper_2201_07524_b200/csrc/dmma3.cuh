@@ -68,7 +68,6 @@ struct SpreadItem {
 #endif
 constexpr int kInterpBatch3 = SK_INTERP_NB;   // d = 3 interp batch (nodes of one cell per warp pass)
 constexpr int kSegMax = 1024;
-constexpr int kSegHybrid = 128;   // spread3_hybrid_kernel segments (two passes, L2-resident taps)
 constexpr int kSegTmaMax = 64;     // spread3_tma_kernel segments (one TMA-staged buffer each)
 constexpr int kSegTmaPMax = SK_TP_SEG_MAX;   // spread3_tmapad_kernel segments (sparse cells)
 #ifndef SK_TP_SEG_DENSE
@@ -364,302 +363,7 @@ interp3_dmma_kernel(const CellBatch* __restrict__ batches, int nbatches, const d
 }
 
 // ------------------------------------------------------------------------------ spread
-struct SpreadDCfg {
-    static constexpr int W = 12, S = W + 1, NT = 128, NWARP = NT / 32, NTILE = (W * W) / 8;  // 18
-    static constexpr int TS = 3 * W;
-    static constexpr int REG = S * S * S;              // warp-private 2^3-super-tile region
-    static constexpr size_t SMEM_BYTES = sizeof(double) * (NWARP * REG);
-};
-
-template <bool XP>
-__global__ void __launch_bounds__(128, 2)
-spread3_dmma_kernel(const SpreadItem* __restrict__ items, int nitems, const CellBatch* __restrict__ segs,
-                    const double* __restrict__ taps, const double* __restrict__ w,
-                    double* __restrict__ grid, int n) {
-    using C = SpreadDCfg;
-    constexpr int W = C::W, S = C::S, m = W / 2, NTILE = C::NTILE, TS = C::TS;
-    extern __shared__ __align__(16) double smem[];
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int g = lane >> 2, q = lane & 3;
-    double* REGm = smem + warp * C::REG;
-    const int ns = n / 2;
-    const int gw = blockIdx.x * C::NWARP + warp, nw = gridDim.x * C::NWARP;
-
-    for (int ii = gw; ii < nitems; ii += nw) {
-        const SpreadItem it = items[ii];
-        const int sz = it.stile % ns, sy = (it.stile / ns) % ns, sx = it.stile / ns / ns;
-        for (int i = lane; i < C::REG; i += 32) REGm[i] = 0.0;
-        __syncwarp();
-        for (int sg = it.seg_begin; sg < it.seg_end; ++sg) {
-            const CellBatch seg = segs[sg];
-            const int cz = seg.cell % n, cy = (seg.cell / n) % n, cx = seg.cell / n / n;
-            const int ox = cx - 2 * sx, oy = cy - 2 * sy, oz = cz - 2 * sz;   // in {0,1}
-            double acc[2][NTILE][2];
-#pragma unroll
-            for (int mt = 0; mt < 2; ++mt)
-#pragma unroll
-                for (int nt = 0; nt < NTILE; ++nt) acc[mt][nt][0] = acc[mt][nt][1] = 0.0;
-            const double* T0 = taps + (long long)seg.start * TS;
-            const double* w0 = w + seg.start;
-            const int nks = (seg.count + 3) >> 2;
-            // the taps stream from HBM once per apply: keep L2 two 32-node chunks ahead
-            prefetch_range(T0, (long long)min(seg.count, 64) * TS * 8, lane);
-            if (lane < 4) prefetch_l2(w0 + 16 * lane);
-            // B[k = q][n = g] of n-tile nt is column 8 nt + g = (ty, tz) = divmod(8 nt + g, 12):
-            // tz cycles with period 3 in nt, so a lane needs only phi_z at 3 positions and the
-            // node's 12 phi_y values -> 12 loads per k-step instead of 36.
-            const int z1 = (8 + g) % W;
-            // operands of k-step s: w*phi_x (A, 2 rows), phi_y[0..12), phi_z at {g, z1, 4+g}
-            // A rows are region rows r = tx + ox_node: a segment may hold the nodes of an x-pair
-            // of cells (seg.pad = nodes of the first cell, ox = 0; the rest sit at ox = 1)
-            auto load_ops = [&](int s, double& wv, double& x0, double& x1, double2 (&yy)[6], double (&zz)[3]) {
-                const int jr = 4 * s + q;                            // node of this lane's A/B
-                const bool ok = jr < seg.count;
-                const double* tr = T0 + (ok ? jr : 0) * TS;
-                wv = __ldg(w0 + (ok ? jr : 0));   // masked at use: no predicated load to wait on
-                if constexpr (XP) {
-                    const int oxn = jr >= seg.pad ? 1 : 0;   // segment cell has ox = 0
-                    const int t0 = g - oxn, t1 = 8 + g - oxn;
-                    x0 = (t0 >= 0) ? __ldg(tr + t0) : 0.0;
-                    x1 = (t1 < W) ? __ldg(tr + t1) : 0.0;
-                } else {                                     // rows are the cell's tx
-                    x0 = __ldg(tr + g);
-                    x1 = (8 + g < W) ? __ldg(tr + 8 + g) : 0.0;
-                }
-                const double2* y2 = reinterpret_cast<const double2*>(tr + W);
-#pragma unroll
-                for (int i = 0; i < 6; ++i) yy[i] = __ldg(y2 + i);
-                zz[0] = __ldg(tr + 2 * W + g);
-                zz[1] = __ldg(tr + 2 * W + z1);
-                zz[2] = __ldg(tr + 2 * W + 4 + g);
-            };
-            double wn, x0n, x1n, zn[3];
-            double2 yn[6];
-            load_ops(0, wn, x0n, x1n, yn, zn);
-#pragma unroll 1
-            for (int s = 0; s < nks; ++s) {
-                if ((s & 7) == 0 && 4 * s + 64 < seg.count) {
-                    const int n0 = 4 * s + 64, n1 = min(seg.count, 4 * s + 96);
-                    prefetch_range(T0 + (long long)n0 * TS, (long long)(n1 - n0) * TS * 8, lane);
-                    if (lane < 2) prefetch_l2(w0 + n0 + 16 * lane);
-                }
-                const double wu = (4 * s + q < seg.count) ? wn : 0.0;
-                const double a0 = wu * x0n, a1 = wu * x1n;           // A[row g | 8 + g][k = q]
-                double yv[W], zv[3];
-#pragma unroll
-                for (int i = 0; i < 6; ++i) { yv[2 * i] = yn[i].x; yv[2 * i + 1] = yn[i].y; }
-                zv[0] = zn[0]; zv[1] = zn[1]; zv[2] = zn[2];
-                if (s + 1 < nks) load_ops(s + 1, wn, x0n, x1n, yn, zn);   // software pipeline
-#pragma unroll
-                for (int nt = 0; nt < NTILE; ++nt) {
-                    // column 8 nt + g: ty = (8 nt + g) / 12 (compile-time up to g < 4 vs >= 4)
-                    const int k3 = nt / 3, r3 = nt % 3;
-                    const int ty = (r3 == 0) ? 2 * k3 : ((r3 == 1) ? 2 * k3 + (g >= 4 ? 1 : 0) : 2 * k3 + 1);
-                    const double yvv = (r3 == 1) ? (g >= 4 ? yv[2 * k3 + 1] : yv[2 * k3]) : yv[ty];
-                    const double b = yvv * zv[r3];
-#if SK_SPREAD_M16
-                    dmma1684(acc[0][nt][0], acc[0][nt][1], acc[1][nt][0], acc[1][nt][1], a0, a1, b);
-#else
-                    dmma884(acc[0][nt][0], acc[0][nt][1], a0, b);
-                    dmma884(acc[1][nt][0], acc[1][nt][1], a1, b);
-#endif
-                }
-            }
-            // add the block (region rows 0..12, the cell's (oy, oz) columns) into the region
-#pragma unroll
-            for (int mt = 0; mt < 2; ++mt) {
-                const int tr_ = 8 * mt + g;
-                if (XP ? tr_ < S : tr_ < W) {
-                    double* rx = REGm + (XP ? tr_ : ox + tr_) * S * S + oy * S + oz;
-#pragma unroll
-                    for (int nt = 0; nt < NTILE; ++nt)
-#pragma unroll
-                        for (int e = 0; e < 2; ++e) {
-                            const int col = 8 * nt + 2 * q + e;
-                            rx[(col / W) * S + (col % W)] += acc[mt][nt][e];
-                        }
-                }
-            }
-            __syncwarp();
-        }
-        // flush the region: coalesced FP64 atomics along z rows
-        const int gx0 = 2 * sx - (m - 1), gy0 = 2 * sy - (m - 1), gz0 = 2 * sz - (m - 1);
-        for (int i = lane; i < C::REG; i += 32) {
-            const double v = REGm[i];
-            if (v != 0.0) {
-                const int rz = i % S, rest = i / S, ry = rest % S, rx = rest / S;
-                atomicAdd(&grid[((long long)(gx0 + rx) * n + (gy0 + ry)) * n + (gz0 + rz)], v);
-            }
-        }
-        __syncwarp();
-    }
-}
-
-// ------------------------------------------------------------------------------ spread (hybrid)
-// Same contraction as spread3_dmma_kernel without the padded tensor-core rows: rows tx = 0..7
-// are one DMMA m-tile, rows tx = 8..11 run on the FP64 vector pipe (DFMA) with per-lane
-// accumulators. Lane (g, q) owns B column 8 nt + g of node slot q, so its DFMA partials
-// acc2[r][nt] = sum over its nodes of (w phi_x[8+r]) (phi_y phi_z)[8 nt + g]; the four q-lanes
-// are reduced (reduce-scatter in 2 shuffle steps) when a segment ends. Every FP64 operation is
-// useful work (microbench: 26.3 vs 22.3 useful TFLOP/s for the padded mix).
-// Registers: all 18 n-tiles at once would need 108 FP64 accumulators (216 registers), so each
-// segment is swept twice, 9 n-tiles (ty in one half) per pass; segments are short (kSegHybrid
-// nodes) so the second pass finds the taps in L2.
-struct SpreadHCfg {
-    static constexpr int W = 12, S = W + 1, NT = 128, NWARP = NT / 32, NTH = 9;   // n-tiles per pass
-    static constexpr int TS = 3 * W;
-    static constexpr int REG = S * S * S;
-    static constexpr size_t SMEM_BYTES = sizeof(double) * (NWARP * REG);
-};
-
-__global__ void __launch_bounds__(128, 2)
-spread3_hybrid_kernel(const SpreadItem* __restrict__ items, int nitems, const CellBatch* __restrict__ segs,
-                      const double* __restrict__ taps, const double* __restrict__ w,
-                      double* __restrict__ grid, int n) {
-    using C = SpreadHCfg;
-    constexpr int W = C::W, S = C::S, m = W / 2, NTH = C::NTH, TS = C::TS;
-    extern __shared__ __align__(16) double smem[];
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int g = lane >> 2, q = lane & 3;
-    double* REGm = smem + warp * C::REG;
-    const int ns = n / 2;
-    const int gw = blockIdx.x * C::NWARP + warp, nw = gridDim.x * C::NWARP;
-    const int z1 = (8 + g) % W;
-
-    for (int ii = gw; ii < nitems; ii += nw) {
-        const SpreadItem it = items[ii];
-        const int sz = it.stile % ns, sy = (it.stile / ns) % ns, sx = it.stile / ns / ns;
-        for (int i = lane; i < C::REG; i += 32) REGm[i] = 0.0;
-        __syncwarp();
-        for (int sg = it.seg_begin; sg < it.seg_end; ++sg) {
-            const CellBatch seg = segs[sg];
-            const int cz = seg.cell % n, cy = (seg.cell / n) % n, cx = seg.cell / n / n;
-            const int ox = cx - 2 * sx, oy = cy - 2 * sy, oz = cz - 2 * sz;   // in {0,1}
-            const double* T0 = taps + (long long)seg.start * TS;
-            const double* w0 = w + seg.start;
-            const int nks = (seg.count + 3) >> 2;
-            prefetch_range(T0, (long long)seg.count * TS * 8, lane);
-            if (lane < 8) prefetch_l2(w0 + 16 * lane);
-#pragma unroll 1
-            for (int half = 0; half < 2; ++half) {
-                // pass over columns 72 half .. 72 half + 71: ty in 6 half .. 6 half + 5
-                double acc[NTH][2], acc2[4][NTH];
-#pragma unroll
-                for (int j = 0; j < NTH; ++j) {
-                    acc[j][0] = acc[j][1] = 0.0;
-#pragma unroll
-                    for (int r = 0; r < 4; ++r) acc2[r][j] = 0.0;
-                }
-                // operands of k-step s for node 4 s + q: w, phi_x[g], phi_x[8..11], the six
-                // phi_y of this half, phi_z at {g, z1, 4+g}
-                auto load_ops = [&](int s, double& wv, double& x0, double2 (&x8)[2], double2 (&yy)[3],
-                                    double (&zz)[3]) {
-                    const int jr = 4 * s + q;
-                    const bool ok = jr < seg.count;
-                    const double* tr = T0 + (ok ? jr : 0) * TS;
-                    wv = __ldg(w0 + (ok ? jr : 0));   // masked at use: no predicated load to wait on
-                    x0 = __ldg(tr + g);
-                    x8[0] = __ldg(reinterpret_cast<const double2*>(tr + 8));
-                    x8[1] = __ldg(reinterpret_cast<const double2*>(tr + 10));
-                    const double2* y2 = reinterpret_cast<const double2*>(tr + W + 6 * half);
-#pragma unroll
-                    for (int i = 0; i < 3; ++i) yy[i] = __ldg(y2 + i);
-                    zz[0] = __ldg(tr + 2 * W + g);
-                    zz[1] = __ldg(tr + 2 * W + z1);
-                    zz[2] = __ldg(tr + 2 * W + 4 + g);
-                };
-                double wn, x0n, zn[3];
-                double2 x8n[2], yn[3];
-                load_ops(0, wn, x0n, x8n, yn, zn);
-#pragma unroll 1
-                for (int s = 0; s < nks; ++s) {
-                    const double wu = (4 * s + q < seg.count) ? wn : 0.0;
-                    const double a0 = wu * x0n;                             // A[tx = g][k = q]
-                    const double xr[4] = {wu * x8n[0].x, wu * x8n[0].y, wu * x8n[1].x, wu * x8n[1].y};
-                    double yv[6], zv[3];
-#pragma unroll
-                    for (int i = 0; i < 3; ++i) { yv[2 * i] = yn[i].x; yv[2 * i + 1] = yn[i].y; }
-                    zv[0] = zn[0]; zv[1] = zn[1]; zv[2] = zn[2];
-                    if (s + 1 < nks) load_ops(s + 1, wn, x0n, x8n, yn, zn);   // software pipeline
-#pragma unroll
-                    for (int j = 0; j < NTH; ++j) {
-                        // column 8 (9 half + j) + g: ty = 6 half + 2 (j/3) + {0, g>=4, 1}[j%3]
-                        const int k3 = j / 3, r3 = j % 3;
-                        const double yvv = (r3 == 0) ? yv[2 * k3]
-                                         : ((r3 == 1) ? (g >= 4 ? yv[2 * k3 + 1] : yv[2 * k3]) : yv[2 * k3 + 1]);
-                        const double b = yvv * zv[r3];
-                        dmma884(acc[j][0], acc[j][1], a0, b);
-#pragma unroll
-                        for (int r = 0; r < 4; ++r) acc2[r][j] = fma(xr[r], b, acc2[r][j]);
-                    }
-                }
-                // DMMA rows tx = g: columns 8 nt + 2 q + e
-                {
-                    double* rx = REGm + (ox + g) * S * S + oy * S + oz;
-#pragma unroll
-                    for (int j = 0; j < NTH; ++j)
-#pragma unroll
-                        for (int e = 0; e < 2; ++e) {
-                            const int col = 8 * (NTH * half + j) + 2 * q + e;
-                            rx[(col / W) * S + (col % W)] += acc[j][e];
-                        }
-                }
-                // DFMA rows tx = 8 + r: reduce-scatter over the q-lanes, lane q keeps row 8 + q
-                {
-                    const bool hi2 = (q & 2) != 0, hi1 = (q & 1) != 0;
-                    double* rx = REGm + (ox + 8 + q) * S * S + oy * S + oz;
-#pragma unroll
-                    for (int j = 0; j < NTH; ++j) {
-                        double keep[2];
-#pragma unroll
-                        for (int rr = 0; rr < 2; ++rr) {
-                            const double send = hi2 ? acc2[rr][j] : acc2[2 + rr][j];
-                            const double mine = hi2 ? acc2[2 + rr][j] : acc2[rr][j];
-                            keep[rr] = mine + __shfl_xor_sync(0xffffffffu, send, 2);
-                        }
-                        const double send = hi1 ? keep[0] : keep[1];
-                        const double mine = hi1 ? keep[1] : keep[0];
-                        const double fin = mine + __shfl_xor_sync(0xffffffffu, send, 1);
-                        const int col = 8 * (NTH * half + j) + g;
-                        rx[(col / W) * S + (col % W)] += fin;
-                    }
-                }
-                __syncwarp();
-            }
-        }
-        // flush the region: coalesced FP64 atomics along z rows
-        const int gx0 = 2 * sx - (m - 1), gy0 = 2 * sy - (m - 1), gz0 = 2 * sz - (m - 1);
-        for (int i = lane; i < C::REG; i += 32) {
-            const double v = REGm[i];
-            if (v != 0.0) {
-                const int rz = i % S, rest = i / S, ry = rest % S, rx = rest / S;
-                atomicAdd(&grid[((long long)(gx0 + rx) * n + (gy0 + ry)) * n + (gz0 + rz)], v);
-            }
-        }
-        __syncwarp();
-    }
-}
-
-// ------------------------------------------------------------------------------ spread (TMA pair)
-// Warp-pair hybrid spread fed by TMA: every segment (<= kSegTma nodes of one cell) is copied
-// into shared memory with two 1-D bulk copies (cp.async.bulk: its taps rows and its weights)
-// completing on an mbarrier, double-buffered so the next segment streams in while the pair
-// computes on this one. Both warps of the pair read the staged operands (warp h owns the
-// columns with ty in 6h .. 6h+5); rows tx 0..7 run as one DMMA m-tile, rows 8..11 on DFMA, so
-// no tensor-core row is padding. Accumulators carry across consecutive segments of one cell;
-// the region update (reduce-scatter + shared-memory add) happens when the cell changes.
-constexpr int kSegTma = 64;
-struct SpreadTCfg {
-    static constexpr int W = 12, S = W + 1, NT = 128, NWARP = NT / 32, NPAIR = NWARP / 2, NTH = 9;
-    static constexpr int TS = 3 * W;
-    static constexpr int REG = S * S * S;                      // 2197
-    static constexpr int REGP = REG + 1;                       // keep the buffers 16-byte aligned
-    static constexpr int TBUF = kSegTma * TS;                  // doubles per taps buffer
-    static constexpr int WBUF = kSegTma + 4;                   // weights (aligned superset)
-    static constexpr int PAIR = 2 + REGP + 2 * TBUF + 2 * WBUF; // doubles per pair
-    static constexpr size_t SMEM_BYTES = sizeof(double) * NPAIR * PAIR;
-};
-
+// mbarrier / bulk-copy helpers of the TMA-fed spread.
 __device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
 __device__ __forceinline__ void pair_barrier(int pair) { asm volatile("bar.sync %0, 64;" ::"r"(pair + 1) : "memory"); }
 __device__ __forceinline__ void mbar_init(unsigned long long* mb, unsigned count) {
@@ -678,148 +382,6 @@ __device__ __forceinline__ void mbar_wait(unsigned long long* mb, unsigned parit
 __device__ __forceinline__ void tma_load_1d(void* dst, const void* src, unsigned bytes, unsigned long long* mb) {
     asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
                  ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(mb)) : "memory");
-}
-
-__global__ void __launch_bounds__(128, 2)
-spread3_tma_kernel(const SpreadItem* __restrict__ items, int nitems, const CellBatch* __restrict__ segs,
-                   const double* __restrict__ taps, const double* __restrict__ w,
-                   double* __restrict__ grid, int n) {
-    using C = SpreadTCfg;
-    constexpr int W = C::W, S = C::S, m = W / 2, NTH = C::NTH, TS = C::TS;
-    extern __shared__ __align__(16) double smem[];
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int pair = warp >> 1, half = warp & 1;
-    const int g = lane >> 2, q = lane & 3;
-    const int plane = half * 32 + lane;
-    double* base = smem + pair * C::PAIR;
-    unsigned long long* mbar = reinterpret_cast<unsigned long long*>(base);
-    double* REGm = base + 2;
-    double* TB0 = base + 2 + C::REGP;
-    double* WB0 = TB0 + 2 * C::TBUF;
-    const int ns = n / 2;
-    const int gp = blockIdx.x * C::NPAIR + pair, np = gridDim.x * C::NPAIR;
-    const int z1 = (8 + g) % W;
-    const bool producer = half == 0 && lane == 0;
-
-    if (producer) {
-        mbar_init(&mbar[0], 1);
-        mbar_init(&mbar[1], 1);
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    }
-    pair_barrier(pair);
-    auto issue = [&](int sg, int b) {   // producer: stream segment sg into buffer b
-        const CellBatch sq = segs[sg];
-        const long long st = sq.start;
-        const long long w0 = st & ~1LL, w1 = (st + sq.count + 1) & ~1LL;
-        const unsigned tbytes = (unsigned)sq.count * TS * 8u, wbytes = (unsigned)(w1 - w0) * 8u;
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // generic reads before async writes
-        mbar_expect_tx(&mbar[b], tbytes + wbytes);
-        tma_load_1d(TB0 + b * C::TBUF, taps + st * TS, tbytes, &mbar[b]);
-        tma_load_1d(WB0 + b * C::WBUF, w + w0, wbytes, &mbar[b]);
-    };
-    unsigned uses0 = 0, uses1 = 0;
-    int t = 0;
-    if (producer && gp < nitems) issue(items[gp].seg_begin, 0);
-
-    for (int ii = gp; ii < nitems; ii += np) {
-        const SpreadItem it = items[ii];
-        const int sz = it.stile % ns, sy = (it.stile / ns) % ns, sx = it.stile / ns / ns;
-        for (int i = plane; i < C::REG; i += 64) REGm[i] = 0.0;
-        double acc[NTH][2], acc2[4][NTH];
-        bool fresh = true;
-        for (int sg = it.seg_begin; sg < it.seg_end; ++sg, ++t) {
-            const int b = t & 1;
-            const CellBatch seg = segs[sg];
-            int nsg = -1;
-            if (sg + 1 < it.seg_end) nsg = sg + 1;
-            else if (ii + np < nitems) nsg = items[ii + np].seg_begin;
-            pair_barrier(pair);   // segment t-1 done by both warps: buffer b^1 is free
-            if (producer && nsg >= 0) issue(nsg, b ^ 1);
-            if (b == 0) { mbar_wait(&mbar[0], uses0 & 1u); ++uses0; }
-            else { mbar_wait(&mbar[1], uses1 & 1u); ++uses1; }
-            const double* T0 = TB0 + b * C::TBUF;
-            const double* W0 = WB0 + b * C::WBUF + (seg.start & 1LL);
-            const int cz = seg.cell % n, cy = (seg.cell / n) % n, cx = seg.cell / n / n;
-            const int ox = cx - 2 * sx, oy = cy - 2 * sy, oz = cz - 2 * sz;   // in {0,1}
-            if (fresh) {
-#pragma unroll
-                for (int j = 0; j < NTH; ++j) {
-                    acc[j][0] = acc[j][1] = 0.0;
-#pragma unroll
-                    for (int r = 0; r < 4; ++r) acc2[r][j] = 0.0;
-                }
-                fresh = false;
-            }
-            const int nks = (seg.count + 3) >> 2;
-#pragma unroll 1
-            for (int s = 0; s < nks; ++s) {
-                const int jr = 4 * s + q;
-                const bool ok = jr < seg.count;
-                const double* tr = T0 + (ok ? jr : 0) * TS;
-                const double wu = ok ? W0[jr] : 0.0;
-                const double a0 = wu * tr[g];                              // A[tx = g][k = q]
-                const double2 x8a = *reinterpret_cast<const double2*>(tr + 8);
-                const double2 x8b = *reinterpret_cast<const double2*>(tr + 10);
-                const double xr[4] = {wu * x8a.x, wu * x8a.y, wu * x8b.x, wu * x8b.y};
-                double yv[6];
-                {
-                    const double2* y2 = reinterpret_cast<const double2*>(tr + W + 6 * half);
-#pragma unroll
-                    for (int i = 0; i < 3; ++i) { const double2 v2 = y2[i]; yv[2 * i] = v2.x; yv[2 * i + 1] = v2.y; }
-                }
-                const double zv[3] = {tr[2 * W + g], tr[2 * W + z1], tr[2 * W + 4 + g]};
-#pragma unroll
-                for (int j = 0; j < NTH; ++j) {
-                    const int k3 = j / 3, r3 = j % 3;
-                    const double yvv = (r3 == 0) ? yv[2 * k3]
-                                     : ((r3 == 1) ? (g >= 4 ? yv[2 * k3 + 1] : yv[2 * k3]) : yv[2 * k3 + 1]);
-                    const double bb = yvv * zv[r3];
-                    dmma884(acc[j][0], acc[j][1], a0, bb);
-#pragma unroll
-                    for (int r = 0; r < 4; ++r) acc2[r][j] = fma(xr[r], bb, acc2[r][j]);
-                }
-            }
-            const bool flush_cell = (sg + 1 >= it.seg_end) || (segs[sg + 1].cell != seg.cell);
-            if (flush_cell) {
-                const bool hi2 = (q & 2) != 0, hi1 = (q & 1) != 0;
-                double* rx = REGm + (ox + g) * S * S + oy * S + oz;
-#pragma unroll
-                for (int j = 0; j < NTH; ++j)
-#pragma unroll
-                    for (int e = 0; e < 2; ++e) {
-                        const int col = 8 * (NTH * half + j) + 2 * q + e;
-                        rx[(col / W) * S + (col % W)] += acc[j][e];
-                    }
-                double* r8 = REGm + (ox + 8 + q) * S * S + oy * S + oz;
-#pragma unroll
-                for (int j = 0; j < NTH; ++j) {
-                    double keep[2];
-#pragma unroll
-                    for (int rr = 0; rr < 2; ++rr) {
-                        const double send = hi2 ? acc2[rr][j] : acc2[2 + rr][j];
-                        const double mine = hi2 ? acc2[2 + rr][j] : acc2[rr][j];
-                        keep[rr] = mine + __shfl_xor_sync(0xffffffffu, send, 2);
-                    }
-                    const double send = hi1 ? keep[0] : keep[1];
-                    const double mine = hi1 ? keep[1] : keep[0];
-                    const double fin = mine + __shfl_xor_sync(0xffffffffu, send, 1);
-                    const int col = 8 * (NTH * half + j) + g;
-                    r8[(col / W) * S + (col % W)] += fin;
-                }
-                fresh = true;
-            }
-        }
-        pair_barrier(pair);
-        const int gx0 = 2 * sx - (m - 1), gy0 = 2 * sy - (m - 1), gz0 = 2 * sz - (m - 1);
-        for (int i = plane; i < C::REG; i += 64) {
-            const double v = REGm[i];
-            if (v != 0.0) {
-                const int rz = i % S, rest = i / S, ry = rest % S, rxx = rest / S;
-                atomicAdd(&grid[((long long)(gx0 + rxx) * n + (gy0 + ry)) * n + (gz0 + rz)], v);
-            }
-        }
-        pair_barrier(pair);
-    }
 }
 
 // ------------------------------------------------------------------------------ spread (TMA, padded)
@@ -854,8 +416,7 @@ using SpreadTPCfgDense = SpreadTPCfg<kSegTmaPDense, 2>;
 template <int SEG, int NPAIR_, bool XP>
 __global__ void __launch_bounds__(64 * NPAIR_, 2)
 spread3_tmapad_kernel(const SpreadItem* __restrict__ items, int nitems, const CellBatch* __restrict__ segs,
-                      const double* __restrict__ taps, const double* __restrict__ w,
-                      double* __restrict__ grid, int n) {
+                      const double* __restrict__ taps, const double* __restrict__ w, const GridAcc ga) {
     using C = SpreadTPCfg<SEG, NPAIR_>;
     // k-step unroll (measured): 4 for the dense shape (c5 spread 15.17 -> 14.71 ms with 2),
     // 8 for the 32-node shape (c3 0.248 -> 0.243 ms)
@@ -871,7 +432,8 @@ spread3_tmapad_kernel(const SpreadItem* __restrict__ items, int nitems, const Ce
     double* REGm = base + 2;
     double* TB0 = base + 2 + C::REGP;
     double* WB0 = TB0 + 2 * C::TBUF;
-    const int ns = n / 2;
+    const int n = ga.n, ns = n / 2;
+    const double gscale = grid_scale(ga);
     const int gp = blockIdx.x * C::NPAIR + pair, np = gridDim.x * C::NPAIR;
     const int z1 = (8 + g) % W;
     const bool producer = half == 0 && lane == 0;
@@ -990,7 +552,7 @@ spread3_tmapad_kernel(const SpreadItem* __restrict__ items, int nitems, const Ce
             const double v = REGm[i];
             if (v != 0.0) {
                 const int rz = i % S, rest = i / S, ry = rest % S, rxx = rest / S;
-                atomicAdd(&grid[((long long)(gx0 + rxx) * n + (gy0 + ry)) * n + (gz0 + rz)], v);
+                grid_add<3>(ga, gscale, gx0 + rxx, gy0 + ry, gz0 + rz, v);
             }
         }
         pair_barrier(pair);

@@ -330,11 +330,12 @@ int launch_scale_const(double* p, long long count, double c, cudaStream_t s) {
 }
 
 // ------------------------------------------------------------------ a8: reductions
-// op 0: sum p_i log x_i;  op 1: sum x_i;  op 2: sum p_i x_i;  op 3: sum log x_i;  op 4: max x_i
+// op 0: sum p_i log x_i;  op 1: sum x_i;  op 2: sum p_i x_i;  op 3: sum log x_i;  op 4: max x_i;
+// op 5: min x_i
 __global__ void reduce_kernel(const double* __restrict__ p, const double* __restrict__ x,
                               long long count, int op, double* __restrict__ partial) {
     __shared__ double sh[kRedBlock / 32];
-    double acc = (op == 4) ? -INFINITY : 0.0;
+    double acc = (op == 4) ? -INFINITY : (op == 5 ? INFINITY : 0.0);
     for (long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x; k < count;
          k += (long long)gridDim.x * blockDim.x) {
         double xv = x[k];
@@ -343,10 +344,12 @@ __global__ void reduce_kernel(const double* __restrict__ p, const double* __rest
             case 1: acc += xv; break;
             case 2: acc += p[k] * xv; break;
             case 3: acc += log(xv); break;
-            default: acc = fmax(acc, xv); break;
+            case 4: acc = fmax(acc, xv); break;
+            default: acc = fmin(acc, xv); break;   // NaN-free inputs; a NaN weight fails the sum check
         }
     }
-    double r = (op == 4) ? block_max<kRedBlock>(acc, sh) : block_sum<kRedBlock>(acc, sh);
+    double r = (op == 4) ? block_max<kRedBlock>(acc, sh)
+                         : (op == 5 ? block_min<kRedBlock>(acc, sh) : block_sum<kRedBlock>(acc, sh));
     if (threadIdx.x == 0) partial[blockIdx.x] = r;
 }
 
@@ -377,11 +380,12 @@ int launch_reduce_sum_log(const double* p, const double* x, long long count, dou
     if (count <= 0) {
         SK_CUDA(cudaMemsetAsync(out_dev, 0, sizeof(double), s));
         if (op == 4) launch_fill(out_dev, 1, -INFINITY, s);
+        if (op == 5) launch_fill(out_dev, 1, INFINITY, s);
         return SK_OK;
     }
     reduce_kernel<<<kRedGrid, kRedBlock, 0, s>>>(p, x, count, op, part);
     SK_LAUNCH_CHECK();
-    finalize_kernel<<<1, kRedBlock, 0, s>>>(part, kRedGrid, 1, 0u, op == 4 ? 1u : 0u, out_dev);
+    finalize_kernel<<<1, kRedBlock, 0, s>>>(part, kRedGrid, 1, op == 5 ? 1u : 0u, op == 4 ? 1u : 0u, out_dev);
     SK_LAUNCH_CHECK();
     return SK_OK;
 }
@@ -409,8 +413,8 @@ int launch_finalize_partials(const double* red, int nparts, int nvals, double* o
 // x_old) (the Lemma at), [3] sum p log x_new (f = 1 - [3]_u - [3]_v after a step).
 __global__ void update_kernel(const double* __restrict__ t, const double* __restrict__ p,
                               double* __restrict__ x, long long count, int want_resid, int iter,
-                              const int* __restrict__ iter_dev, int* __restrict__ bad,
-                              double* __restrict__ partial) {
+                              const int* __restrict__ iter_dev, unsigned long long* __restrict__ bad,
+                              int rank, double* __restrict__ partial) {
     __shared__ double sh[kRedBlock / 32];
     double res = 0.0, tmin = INFINITY, kl = 0.0, slog = 0.0;
     if (iter_dev) iter = *iter_dev;   // graph replay: iteration number from the device counter
@@ -424,10 +428,7 @@ __global__ void update_kernel(const double* __restrict__ t, const double* __rest
             slog += pk * log(xn);
         }
         tmin = fmin(tmin, tk);
-        if (!(tk > 1e-300) || !isfinite(tk)) {  // SK_ENONPOS (tau_pos = 1e-300)
-            atomicMin(bad, (int)k);
-            atomicMin(bad + 1, iter);
-        }
+        if (!(tk > 1e-300) || !isfinite(tk)) record_bad(bad, iter, rank, k);   // SK_ENONPOS (tau_pos = 1e-300)
         x[k] = xn;
     }
     const double r0 = block_sum<kRedBlock>(res, sh);
@@ -446,7 +447,7 @@ int launch_update(Plan& P, int side, const double* t_sorted, const double* p_sor
                   double* x_sorted, int want_resid, int iter, const int* iter_dev, cudaStream_t s) {
     long long count = P.side[side].count;  // count == 0 still writes neutral partials
     update_kernel<<<kRedGrid, kRedBlock, 0, s>>>(t_sorted, p_sorted, x_sorted, count, want_resid,
-                                                 iter, iter_dev, P.flag + 2 * side, P.red);
+                                                 iter, iter_dev, P.bad64 + side, P.ctx->rank, P.red);
     SK_LAUNCH_CHECK();
     return SK_OK;
 }
@@ -607,6 +608,59 @@ int launch_band_coeffs(Plan& P, int kernel, int M, const cufftDoubleComplex* B, 
     return SK_OK;
 }
 
+// Plan-time accuracy estimate: the part of K~'s Fourier series that the N-band drops, measured
+// on the (2N)^d sampling grid: sum |b_k| over the k of that grid with max_a |k_a| > N/2 (the
+// +-N/2 modes count half, reading Q8), both Hermitian halves. |K~(x) - K~_N(x)| <= this sum.
+__global__ void band_tail_kernel(BandParams bp, const cufftDoubleComplex* __restrict__ B,
+                                 double* __restrict__ partial) {
+    __shared__ double sh[kRedBlock / 32];
+    const int M = bp.M, h = bp.N / 2, Mh = M / 2 + 1;
+    long long total = Mh;
+    for (int a = 0; a < bp.d - 1; ++a) total *= M;
+    double acc = 0.0;
+    for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
+         e += (long long)gridDim.x * blockDim.x) {
+        long long rest = e;
+        const int kl = (int)(rest % Mh);
+        rest /= Mh;
+        int kmax = kl;
+        double wgt = (kl == h) ? 0.5 : 1.0;
+        for (int a = 0; a < bp.d - 1; ++a) {
+            int ka = (int)(rest % M);
+            rest /= M;
+            ka = ka >= M / 2 ? M - ka : ka;   // |k_a|
+            kmax = max(kmax, ka);
+            if (ka == h) wgt *= 0.5;
+        }
+        // the band keeps weight wgt of the entries on its faces and all of its interior
+        const double drop = kmax > h ? 1.0 : (kmax == h ? 1.0 - wgt : 0.0);
+        const double herm = (kl == 0 || kl == M / 2) ? 1.0 : 2.0;
+        const cufftDoubleComplex b = B[e];
+        acc += drop * herm * sqrt(b.x * b.x + b.y * b.y);
+    }
+    const double r = block_sum<kRedBlock>(acc, sh);
+    if (threadIdx.x == 0) partial[blockIdx.x] = r * bp.inv_Md;
+}
+
+int launch_band_tail(Plan& P, int M, const cufftDoubleComplex* B, double* out_dev, cudaStream_t s) {
+    BandParams bp;
+    bp.d = P.d;
+    bp.N = P.N;
+    bp.M = M;
+    bp.n = P.n;
+    bp.m = P.win.m;
+    bp.beta = P.win.beta;
+    double Md = 1.0;
+    for (int a = 0; a < P.d; ++a) Md *= M;
+    bp.inv_Md = 1.0 / Md;
+    double* part = out_dev + 1;
+    band_tail_kernel<<<kRedGrid, kRedBlock, 0, s>>>(bp, B, part);
+    SK_LAUNCH_CHECK();
+    finalize_kernel<<<1, kRedBlock, 0, s>>>(part, kRedGrid, 1, 0u, 0u, out_dev);
+    SK_LAUNCH_CHECK();
+    return SK_OK;
+}
+
 // ------------------------------------------------------------------ r = 1 near field (NEXT-2)
 // t_i += sum over sources j with |x'_i - y'_j| < a of w_j (K - K_I)(|x'_i - y'_j|): the part
 // of the Laplace kernel that the inner regularisation K_I removed from the Fourier series
@@ -727,10 +781,66 @@ int launch_multiply(Plan& P, int kernel, cudaStream_t s) {
 }
 
 // ------------------------------------------------------------------ a2 / a7: spread, interp
+// Deterministic spread (GridAcc): max |w_j| as the bits of a non-negative double (their integer
+// order is the value order, so atomicMax on the bits is a max on the values; NaN sorts last).
+__global__ void abs_max_bits_kernel(const double* __restrict__ w, long long count, unsigned long long* out) {
+    unsigned long long mx = 0;
+    for (long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x; k < count;
+         k += (long long)gridDim.x * blockDim.x) {
+        const unsigned long long b = (unsigned long long)__double_as_longlong(fabs(w[k]));
+        mx = b > mx ? b : mx;
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+        const unsigned long long t = __shfl_xor_sync(0xffffffffu, mx, o);
+        mx = t > mx ? t : mx;
+    }
+    if ((threadIdx.x & 31) == 0 && mx) atomicMax(out, mx);
+}
+
+// Fixed-point box accumulator -> FP64 grid: X = hi 2^32 + lo exactly (carry of lo folded into
+// hi), value = X 2^-S; cells outside the box keep the caller's zeros.
+__global__ void grid_fix_convert_kernel(const GridAcc ga, int d, long long box_size) {
+    const double wm = __longlong_as_double((long long)*ga.wmax);
+    const double inv = 1.0 / grid_scale(ga);
+    const bool finite = isfinite(wm);
+    for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < box_size;
+         e += (long long)gridDim.x * blockDim.x) {
+        const long long hi = (long long)ga.acc[2 * e];
+        const unsigned long long lo = ga.acc[2 * e + 1];
+        const long long H = hi + (long long)(lo >> 32);
+        const double L = (double)(lo & 0xffffffffULL);
+        const double v = finite ? fma((double)H, 4294967296.0, L) * inv : NAN;
+        long long rest = e, gi = 0, mul = 1;
+        for (int a = d - 1; a >= 0; --a) {
+            const int c = (int)(rest % ga.bn[a]);
+            rest /= ga.bn[a];
+            gi += (long long)(ga.lo[a] + c) * mul;
+            mul *= ga.n;
+        }
+        ga.grid[gi] = v;
+    }
+}
+
 int launch_spread(Plan& P, int side, const double* w_sorted, double* grid, cudaStream_t s) {
     const NodeSet& S = P.side[side];
     if (S.count <= 0) return SK_OK;
-    SK_TRY(spread_dispatch(P, S, w_sorted, grid, s));
+    GridAcc ga;
+    ga.grid = grid;
+    ga.n = P.n;
+    ga.phi0d = P.phi0d;
+    for (int a = 0; a < P.d; ++a) { ga.lo[a] = P.box_lo[a]; ga.bn[a] = P.box_n[a]; }
+    if (P.deterministic) {
+        ga.acc = P.det_acc;
+        ga.wmax = P.det_acc + 2 * P.box_size;
+        SK_CUDA(cudaMemsetAsync(P.det_acc, 0, sizeof(unsigned long long) * (2 * P.box_size + 1), s));
+        abs_max_bits_kernel<<<grid_for(S.count, 256), 256, 0, s>>>(w_sorted, S.count, P.det_acc + 2 * P.box_size);
+        SK_LAUNCH_CHECK();
+    }
+    SK_TRY(spread_dispatch(P, S, w_sorted, ga, s));
+    if (P.deterministic) {
+        grid_fix_convert_kernel<<<grid_for(P.box_size, 256), 256, 0, s>>>(ga, P.d, P.box_size);
+        SK_LAUNCH_CHECK();
+    }
     return SK_OK;
 }
 

@@ -419,7 +419,7 @@ static int build_cell_lists(Plan& P, NodeSet& S, cudaStream_t s) {
         S.seg_dense = P.spread_tmapad && P.d == 3 && !S.xpairs && count >= thr * (long long)nruns;
     }
     const int seg_max = std::min(P.spread_tmapad ? (S.seg_dense ? kSegTmaPDense : kSegTmaPMax)
-                                 : (P.spread_tma ? kSegTmaMax : (P.spread_hybrid ? kSegHybrid : kSegMax)),
+                                 : kSegMax,
                                  item_max);
     g.xpairs = S.xpairs ? 1 : 0;
     SK_CUDA(cub::DeviceScan::ExclusiveSum(tmp, tb, cnts, rstart, nruns, s));
@@ -558,6 +558,8 @@ static int plan_coefficients(Plan& P, cudaStream_t s) {
     cufftDoubleComplex* B = nullptr;
     SK_TRY(alloc((void**)&samp, sizeof(double) * Md));
     SK_TRY(alloc((void**)&B, sizeof(cufftDoubleComplex) * Bsz));
+    double* tail = nullptr;   // [kernel][1 + kUpdBlocks]: band-tail estimate + partial scratch
+    SK_TRY(alloc((void**)&tail, sizeof(double) * 2 * (1 + kUpdBlocks)));
     cufftHandle h = 0;
     SK_TRY(fft_acquire(P.d, M, CUFFT_D2Z, s, &h));
     for (int kernel = 0; kernel < 2; ++kernel) {
@@ -573,8 +575,12 @@ static int plan_coefficients(Plan& P, cudaStream_t s) {
         SK_CUFFT(cufftExecD2Z(h, samp, B));
         count_launch();
         SK_TRY(launch_band_coeffs(P, kernel, M, B, s));
+        SK_TRY(launch_band_tail(P, M, B, tail + kernel * (1 + kUpdBlocks), s));
     }
+    SK_CUDA(cudaMemcpyAsync(&P.acc_tail[0], tail, sizeof(double), cudaMemcpyDeviceToHost, s));
+    SK_CUDA(cudaMemcpyAsync(&P.acc_tail[1], tail + 1 + kUpdBlocks, sizeof(double), cudaMemcpyDeviceToHost, s));
     SK_CUDA(cudaStreamSynchronize(s));
+    sk_free(tail);
     fft_release(P.d, M, CUFFT_D2Z, h);
     sk_free(samp);
     sk_free(B);
@@ -601,6 +607,11 @@ int build_plan(Ctx* ctx, Plan** out, int d, const double* x, long long n, const 
     if (!(sigma >= 1.0) || fabs(nd - ng) > 1e-9 || (ng & 1))
         return set_error(SK_EINVAL, "sigma*N must be an even integer");
     if (ng < 4 * m_w) return set_error(SK_EINVAL, "sigma*N must be >= 4*m_w (no tap wraps the torus)");
+    {   // cell indices and sort keys are int: the grid must have < 2^31 cells
+        long long cells = 1;
+        for (int a = 0; a < d; ++a) cells *= ng;
+        if (cells > 0x7fffffffLL) return set_error(SK_EINVAL, "(sigma N)^d must be < 2^31 grid cells");
+    }
 
     cudaStream_t s = ctx->stream;
     tls_stream = s;
@@ -643,16 +654,16 @@ int build_plan(Ctx* ctx, Plan** out, int d, const double* x, long long n, const 
         P->dmma = ((P->tiled && m_w == 6) || (d == 2 && m_w == 8 && err >= 0.0 && err <= 1e-14)) &&
                   rpow == 2 && getenv("SK_NO_DMMA") == nullptr && getenv("SK_FORCE_V1") == nullptr;
         if (P->dmma && d == 2) P->tiled = false;
-        // hybrid DMMA+DFMA spread (no padded rows): opt-in until it beats the padded kernel
-        // (c5: 20.6 vs 15.5 ms under ncu, issue/latency-bound with 2 passes per segment)
-        P->spread_hybrid = P->dmma && d == 3 && getenv("SK_SPREAD3_HYBRID") != nullptr;
-        P->spread_tma = P->dmma && d == 3 && !P->spread_hybrid && getenv("SK_SPREAD3_TMA") != nullptr;
-        // default d = 3 spread: the padded DMMA spread on TMA-fed warp pairs (c5 17.0 -> 15.5 ms,
-        // c3 0.31 -> 0.26 ms); SK_SPREAD3_PADDED=1 restores the single-warp padded kernel
-        P->spread_tmapad = P->dmma && d == 3 && !P->spread_hybrid && !P->spread_tma &&
-                           getenv("SK_SPREAD3_PADDED") == nullptr;
-        P->spread_xpairs = P->dmma && d == 3 && !P->spread_hybrid && !P->spread_tma &&
-                           getenv("SK_NO_XPAIRS") == nullptr;
+        // d = 3 spread: the padded DMMA spread on TMA-fed warp pairs, x-pair segments for
+        // sparse sets (SK_NO_XPAIRS=1 disables them)
+        P->spread_tmapad = P->dmma && d == 3;
+        P->spread_xpairs = P->dmma && d == 3 && getenv("SK_NO_XPAIRS") == nullptr;
+    }
+    {   // phi(0)^d bounds one node's spread contribution |w| prod_a phi (deterministic mode)
+        const double bm = P->win.beta * m_w;
+        P->phi0d = pow(sinh(bm) / (3.141592653589793238462643 * m_w), d);
+        const char* det = getenv("SK_DETERMINISTIC");
+        P->deterministic = det ? atoi(det) != 0 : kDeterministicDefault;
     }
     P->tile_cells = P->dmma ? (d == 3 ? 2 : kSup2) : choose_tile(d, ng, P->tiled);
     P->tiles_per_axis = ng / P->tile_cells;
@@ -688,7 +699,11 @@ int build_plan(Ctx* ctx, Plan** out, int d, const double* x, long long n, const 
             return fail(set_error(SK_EGEOMETRY, "empty node sets or non-finite coordinates"));
         }
         const double diag = sqrt(diag2);
-        P->rho = diag > 0.0 ? P->L / diag : 1.0;
+        // diag = 0 (every atom at one point, reading Q6b): the limit diag -> 0 of rho = L / diag
+        // sends lambda' to 0, where the kernel is constant and its Fourier series exact; taken
+        // at lambda' = kLampDegenerate
+        P->rho = diag > 0.0 ? P->L / diag
+                            : (rpow == 2 ? sqrt(lambda / kLampDegenerate) : lambda / kLampDegenerate);
         // exp(-lam |x - y|^r) = exp(-lam' |x' - y'|^r) with x' = rho (x - centre)
         P->lambda_p = rpow == 2 ? lambda / (P->rho * P->rho) : lambda / P->rho;
         // touched grid box: cells floor(u) - m + 1 .. floor(u) + m of every node, u = n(rho(x -
@@ -722,7 +737,26 @@ int build_plan(Ctx* ctx, Plan** out, int d, const double* x, long long n, const 
     // ---- a0: scale, bin, sort (both sides)
     int st = plan_side(*P, 0, x, n, s);
     if (!st) st = plan_side(*P, 1, y, m, s);
-    if (st) return fail(st);
+    if (st && st != SK_EGEOMETRY) return fail(st);
+    if (ctx->world > 1 || ctx->nccl_comm) {
+        // a node outside the ball (or NaN) on any rank fails the plan on every rank; a rank
+        // returning alone would leave the others blocked in their next collective
+        const std::string local_msg = st ? sk_last_error() : "";
+        double flag = st ? 1.0 : 0.0;
+        double* df = nullptr;
+        int st2 = alloc((void**)&df, sizeof(double));
+        if (!st2) st2 = cudaMemcpyAsync(df, &flag, sizeof(double), cudaMemcpyHostToDevice, s) ? SK_ECUDA : SK_OK;
+        if (!st2) st2 = allreduce_sum(ctx, df, 1);
+        if (!st2) st2 = cudaMemcpyAsync(&flag, df, sizeof(double), cudaMemcpyDeviceToHost, s) ? SK_ECUDA : SK_OK;
+        if (!st2) st2 = cudaStreamSynchronize(s) ? SK_ECUDA : SK_OK;
+        sk_free(df);
+        if (st2) return fail(st2);
+        if (flag > 0.0)
+            return fail(set_error(SK_EGEOMETRY, st ? local_msg : "a node of another rank is non-finite or outside "
+                                                                  "the ball |x'| <= 1/4 - eps_B/2"));
+    } else if (st) {
+        return fail(st);
+    }
     // ---- a1: coefficients
     if ((st = alloc((void**)&P->D[0], sizeof(double) * P->band_size))) return fail(st);
     if ((st = alloc((void**)&P->D[1], sizeof(double) * P->band_size))) return fail(st);
@@ -752,12 +786,16 @@ int build_plan(Ctx* ctx, Plan** out, int d, const double* x, long long n, const 
     if ((st = alloc((void**)&P->u_s, sizeof(double) * (std::max(n, 1LL) + 2)))) return fail(st);
     if ((st = alloc((void**)&P->b_s, sizeof(double) * std::max(m, 1LL)))) return fail(st);
     if ((st = alloc((void**)&P->v_s, sizeof(double) * (std::max(m, 1LL) + 2)))) return fail(st);
+    if (P->deterministic &&
+        (st = alloc((void**)&P->det_acc, sizeof(unsigned long long) * (2 * std::max(P->box_size, 1LL) + 1))))
+        return fail(st);
     P->box_exchange = ctx->world > 1 || ctx->nccl_comm || getenv("SK_FORCE_BOX_EXCHANGE") != nullptr;
     if (P->box_exchange && (st = alloc((void**)&P->box_buf, sizeof(double) * std::max(P->box_size, 1LL))))
         return fail(st);
     if ((st = alloc((void**)&P->red, sizeof(double) * 4096))) return fail(st);
     if ((st = alloc((void**)&P->red_out, sizeof(double) * 8192))) return fail(st);
-    if ((st = alloc((void**)&P->flag, sizeof(int) * 8))) return fail(st);
+    if ((st = alloc((void**)&P->flag, sizeof(int) * 16))) return fail(st);
+    P->bad64 = reinterpret_cast<unsigned long long*>(P->flag + 8);
     if ((st = pinned_acquire(&P->host_red))) return fail(st);
     plan_trace("scratch", s);
     *out = P;
@@ -785,7 +823,7 @@ int destroy_plan(Plan* P) {
     if (P->cap_stream) cudaStreamDestroy(P->cap_stream);
     sk_free(P->w_sorted); sk_free(P->t_sorted);
     sk_free(P->a_s); sk_free(P->b_s); sk_free(P->u_s); sk_free(P->v_s);
-    sk_free(P->red); sk_free(P->red_out); sk_free(P->flag); sk_free(P->box_buf);
+    sk_free(P->red); sk_free(P->red_out); sk_free(P->flag); sk_free(P->box_buf); sk_free(P->det_acc);
     pinned_release(P->host_red);
     delete (WinPoly*)P->winpoly;
     delete P;

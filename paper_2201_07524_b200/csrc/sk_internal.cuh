@@ -14,6 +14,8 @@ namespace sk {
 constexpr int kMaxD = 3;
 constexpr int kMaxW = 16;            // 2 * m_w taps per axis, m_w <= 8
 constexpr int kXPairMaxDensity = 96; // x-pair spread segments when nodes per cell < this
+constexpr double kLampDegenerate = 1e-16;   // lambda' of a zero-diameter geometry (reading Q6b)
+constexpr bool kDeterministicDefault = true;    // spread mode when SK_DETERMINISTIC is unset
 
 // Thread-local error message + status helpers (api.cu).
 int set_error(int code, const std::string& msg);
@@ -98,6 +100,9 @@ struct Plan {
     int ki_n = 0;
     int p_smooth = 8;
     double centre[kMaxD] = {0, 0, 0};
+    // plan-time accuracy report (fastsum_plan_info): sum of |b_k| that the N-band drops, measured
+    // on the (2N)^d sampling grid, per kernel (bounds |K~ - K~_N| pointwise)
+    double acc_tail[2] = {0.0, 0.0};
     long long grid_size = 0;  // n^d
     long long spec_size = 0;  // n^{d-1} (n/2 + 1)
     long long band_size = 0;  // (N+1)^{d-1} (N/2 + 1)
@@ -120,7 +125,9 @@ struct Plan {
     double* red = nullptr;        // block partials
     double* red_out = nullptr;    // reduced scalars (device)
     double* host_red = nullptr;   // pinned host mirror
-    int* flag = nullptr;          // [0..3] first bad (index, iteration) per side, [4] graph iteration counter
+    int* flag = nullptr;          // [4] graph iteration counter; 8-byte aligned [8..11]: bad64
+    unsigned long long* bad64 = nullptr;   // [side] first non-positive denominator, packed
+                                           // (iteration << 40 | rank << 32 | sorted index), atomicMin
     // Sinkhorn state in sorted order
     double* a_s = nullptr; double* b_s = nullptr; double* u_s = nullptr; double* v_s = nullptr;
     long long max_count = 0;
@@ -135,31 +142,89 @@ struct Plan {
     int tiles_per_axis = 0;
     bool tiled = false;       // v2 tiled spread/interp usable (d = 3, 2 m_w in {12, 16})
     bool dmma = false;        // FP64 tensor-core spread/interp (d = 3, 2 m_w = 12)
-    bool spread_hybrid = false;  // d = 3 spread: DMMA rows 0..7 + DFMA rows 8..11 (no padding)
-    bool spread_tma = false;     // d = 3 spread: the hybrid on a warp pair fed by TMA-staged segments
     bool spread_tmapad = false;  // d = 3 spread: the padded DMMA spread on TMA-fed warp pairs
+    // deterministic spread (GridAcc): fixed-point box accumulator [box_size][2] + 1 word max |w|
+    bool deterministic = false;
+    unsigned long long* det_acc = nullptr;
+    double phi0d = 1.0;          // phi(0)^d: the largest product of d window taps
     bool spread_xpairs = false;  // d = 3 padded spread: x-minor keys; sides with sparse cells group
                                  // x-pairs of cells into one segment (13 of 16 rows)
     void* winpoly = nullptr;  // host WinPoly (window tap polynomials)
 };
 
+// Spread output (a2). Default: FP64 atomics straight into the grid (the order of the adds, hence
+// the last bits, varies from run to run). Deterministic mode (acc != nullptr): every spread
+// contribution v is rounded once to an integer multiple of 2^-S, X = rint(v 2^S), and added as
+// two 64-bit integer words X = hi 2^32 + lo (hi signed, lo in [0, 2^32)) into a fixed-point
+// accumulator over the touched box; integer addition is associative, so the sum does not depend
+// on the order and the grid is bit-identical from run to run. S = 61 - ilogb(max|w| phi(0)^d):
+// one node contributes < 2^62 and a cell sum of <= 2^31 nodes stays < 2^93 (hi < 2^61, the lo
+// sum of <= 2^31 contributions < 2^63); the rounding is <= 2^-63 of the largest single-node
+// contribution. grid_fix_convert writes the box back as FP64.
+struct GridAcc {
+    double* grid = nullptr;                     // [n^d] FP64 (atomic mode; conversion target)
+    unsigned long long* acc = nullptr;          // deterministic: [box cells][2] (hi, lo)
+    const unsigned long long* wmax = nullptr;   // deterministic: bits of max_j |w_j| (device)
+    double phi0d = 1.0;                         // phi(0)^d, the largest product of d taps
+    int n = 0;                                  // grid edge
+    int lo[3] = {0, 0, 0};                      // box origin and extent per axis
+    int bn[3] = {1, 1, 1};
+};
+#ifdef __CUDACC__
+// 2^S of the deterministic mode (1 in atomic mode)
+__device__ __forceinline__ double grid_scale(const GridAcc& g) {
+    if (!g.acc) return 1.0;
+    const double c = __longlong_as_double((long long)*g.wmax) * g.phi0d;
+    return c > 0.0 ? ldexp(1.0, 61 - ilogb(c)) : 1.0;
+}
+template <int D>
+__device__ __forceinline__ void grid_add(const GridAcc& g, double scale, int x, int y, int z, double v) {
+    if (!g.acc) {
+        long long i = x;
+        if (D >= 2) i = i * g.n + y;
+        if (D >= 3) i = i * g.n + z;
+        atomicAdd(&g.grid[i], v);
+        return;
+    }
+    long long i = x - g.lo[0];
+    if (D >= 2) i = i * g.bn[1] + (y - g.lo[1]);
+    if (D >= 3) i = i * g.bn[2] + (z - g.lo[2]);
+    const double X = v * scale;                              // exact (power of 2)
+    const double h = floor(X * 2.3283064365386963e-10);      // X / 2^32, exact
+    const double l = rint(X - h * 4294967296.0);             // low part in [0, 2^32], exact before rint
+    atomicAdd(&g.acc[2 * i], (unsigned long long)(long long)h);
+    atomicAdd(&g.acc[2 * i + 1], (unsigned long long)l);
+}
+#endif
+
+// SK_ENONPOS event record: one 64-bit word per side, the minimum over events of
+// (iteration << 40 | rank << 32 | sorted index), so the reported (iteration, rank, index) is one
+// event -- the earliest iteration, then the lowest rank and index -- and a min all-reduce over
+// ranks keeps that property.
+constexpr unsigned long long kNoBad = ~0ULL;
+#ifdef __CUDACC__
+__device__ __forceinline__ void record_bad(unsigned long long* bad, int iter, int rank, long long idx) {
+    const unsigned long long v = ((unsigned long long)(unsigned)iter << 40) |
+                                 ((unsigned long long)(rank & 0xff) << 32) | (unsigned long long)(idx & 0xffffffffLL);
+    atomicMin(bad, v);
+}
+#endif
+
 // Optional u/v update fused into the interpolation epilogue (a7): with x != nullptr the
 // interpolation writes x[i] = p[i] / t_i instead of t_i and flags t_i <= 1e-300 (SK_ENONPOS,
-// first index / iteration via atomicMin). Used when no residual or trace is wanted.
+// record_bad). Used when no residual or trace is wanted.
 struct FusedUpd {
     const double* p = nullptr;
     double* x = nullptr;
-    int* bad = nullptr;            // [index, iteration] of the first non-positive t
-    const int* iter_dev = nullptr; // graph replay: iteration number on the device
+    unsigned long long* bad = nullptr;   // packed first non-positive t (record_bad)
+    const int* iter_dev = nullptr;       // graph replay: iteration number on the device
     int iter = 0;
+    int rank = 0;
 };
 #ifdef __CUDACC__
 __device__ __forceinline__ void emit_t(double* __restrict__ t_out, const FusedUpd& fu, long long idx, double t) {
     if (fu.x) {
-        if (!(t > 1e-300) || !isfinite(t)) {
-            atomicMin(fu.bad, (int)idx);
-            atomicMin(fu.bad + 1, fu.iter_dev ? *fu.iter_dev : fu.iter);
-        }
+        if (!(t > 1e-300) || !isfinite(t)) record_bad(fu.bad, fu.iter_dev ? *fu.iter_dev : fu.iter, fu.rank, idx);
         fu.x[idx] = fu.p[idx] / t;
     } else {
         t_out[idx] = t;
@@ -186,6 +251,8 @@ int launch_permute_out(const double* src, const int* perm, long long count, doub
 int launch_sample_kernel(Plan& P, int kernel, int M, const double* kb_coef, int kb_deg,
                          double* out, cudaStream_t s);
 int launch_band_coeffs(Plan& P, int kernel, int M, const cufftDoubleComplex* B, cudaStream_t s);
+// out_dev[0] = sum of the |b_k| outside the N-band (out_dev[1..kUpdBlocks] scratch)
+int launch_band_tail(Plan& P, int M, const cufftDoubleComplex* B, double* out_dev, cudaStream_t s);
 // Sinkhorn fused update: x_s <- p_s / t (t = interpolated), partial sums into red
 int launch_update(Plan& P, int side, const double* t_sorted, const double* p_sorted,
                   double* x_sorted, int want_resid, int iter, const int* iter_dev, cudaStream_t s);

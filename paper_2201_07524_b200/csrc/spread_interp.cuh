@@ -28,30 +28,24 @@ inline bool first_on_device(std::atomic<unsigned long long>& mask) {
 
 template <int D>
 __global__ void spread_v1_kernel(const double* __restrict__ u, long long count,
-                                 const double* __restrict__ w, Window win, int n,
-                                 double* __restrict__ grid) {
+                                 const double* __restrict__ w, Window win, const GridAcc ga) {
     const int W = 2 * win.m;
+    const double gscale = grid_scale(ga);
     for (long long j = blockIdx.x * (long long)blockDim.x + threadIdx.x; j < count;
          j += (long long)gridDim.x * blockDim.x) {
         double phi[D][kMaxW];
         int base[D];
         for (int a = 0; a < D; ++a) base[a] = kb_taps(u[a * count + j], win, phi[a]) - win.m + 1;
         const double wj = w[j];
-        if (D == 1) {
-            for (int t0 = 0; t0 < W; ++t0) atomicAdd(&grid[base[0] + t0], wj * phi[0][t0]);
-        } else if (D == 2) {
-            for (int t0 = 0; t0 < W; ++t0) {
-                const double w0 = wj * phi[0][t0];
-                double* row = grid + (long long)(base[0] + t0) * n + base[1];
-                for (int t1 = 0; t1 < W; ++t1) atomicAdd(&row[t1], w0 * phi[D - 1][t1]);
-            }
-        } else {
-            for (int t0 = 0; t0 < W; ++t0) {
-                const double w0 = wj * phi[0][t0];
+        for (int t0 = 0; t0 < W; ++t0) {
+            const double w0 = wj * phi[0][t0];
+            if (D == 2) {
+                for (int t1 = 0; t1 < W; ++t1) grid_add<2>(ga, gscale, base[0] + t0, base[1] + t1, 0, w0 * phi[D - 1][t1]);
+            } else {
                 for (int t1 = 0; t1 < W; ++t1) {
                     const double w1 = w0 * phi[1][t1];
-                    double* row = grid + ((long long)(base[0] + t0) * n + (base[1] + t1)) * n + base[D - 1];
-                    for (int t2 = 0; t2 < W; ++t2) atomicAdd(&row[t2], w1 * phi[D - 1][t2]);
+                    for (int t2 = 0; t2 < W; ++t2)
+                        grid_add<3>(ga, gscale, base[0] + t0, base[1] + t1, base[D - 1] + t2, w1 * phi[D - 1][t2]);
                 }
             }
         }
@@ -97,8 +91,9 @@ __global__ void interp_v1_kernel(const double* __restrict__ u, long long count, 
 // so the 2m window evaluations (sqrt + sinh each) of a node run in parallel instead of in one
 // thread's dependent sequence (the d = 1 problems are small and latency-bound).
 __global__ void spread_d1_kernel(const double* __restrict__ u, long long count, const double* __restrict__ w,
-                                 Window win, double* __restrict__ grid) {
+                                 Window win, const GridAcc ga) {
     const int W = 2 * win.m;
+    const double gscale = grid_scale(ga);
     const long long total = count * W;
     for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
          i += (long long)gridDim.x * blockDim.x) {
@@ -106,7 +101,7 @@ __global__ void spread_d1_kernel(const double* __restrict__ u, long long count, 
         const int t = (int)(i - j * W);
         const double uj = u[j], c = floor(uj);
         const double phi = kb_phi(uj - c + (double)(win.m - 1 - t), win);
-        atomicAdd(&grid[(long long)c - win.m + 1 + t], w[j] * phi);
+        grid_add<1>(ga, gscale, (int)c - win.m + 1 + t, 0, 0, w[j] * phi);
     }
 }
 
@@ -142,7 +137,7 @@ inline int persistent_grid(K kernel, int threads, size_t smem, int nitems) {
 }
 
 template <int W>
-inline int spread3_launch(Plan& P, const NodeSet& S, const double* w, double* grid, cudaStream_t s) {
+inline int spread3_launch(Plan& P, const NodeSet& S, const double* w, const GridAcc& ga, cudaStream_t s) {
     using C = Spread3Cfg<W>;
     static std::atomic<unsigned long long> attr{0};
     if (first_on_device(attr)) {
@@ -150,7 +145,7 @@ inline int spread3_launch(Plan& P, const NodeSet& S, const double* w, double* gr
     }
     const int g = persistent_grid(spread3_v2_kernel<W>, C::NT, C::SMEM_BYTES, S.nitems);
     spread3_v2_kernel<W><<<g, C::NT, C::SMEM_BYTES, s>>>((const TileItem*)S.items, S.nitems, S.u, w, S.count,
-                                                         grid, P.n, P.tiles_per_axis, *(const WinPoly*)P.winpoly);
+                                                         ga, P.tiles_per_axis, *(const WinPoly*)P.winpoly);
     return SK_OK;
 }
 
@@ -181,7 +176,7 @@ inline int taps_dispatch(Plan& P, NodeSet& S, cudaStream_t s) {
     return SK_OK;
 }
 
-inline int spread_dispatch(Plan& P, const NodeSet& S, const double* w, double* grid, cudaStream_t s) {
+inline int spread_dispatch(Plan& P, const NodeSet& S, const double* w, const GridAcc& ga, cudaStream_t s) {
     if (P.dmma && P.d == 2) {
         using C = Spread2Cfg;
         static std::atomic<unsigned long long> attr{0};
@@ -191,14 +186,14 @@ inline int spread_dispatch(Plan& P, const NodeSet& S, const double* w, double* g
         if (S.nsitems > 0) {
             const int g = persistent_grid(spread2_dmma_kernel, C::NT, C::SMEM_BYTES, (S.nsitems + C::NWARP - 1) / C::NWARP);
             spread2_dmma_kernel<<<g, C::NT, C::SMEM_BYTES, s>>>((const SpreadItem*)S.sitems, S.nsitems,
-                                                                (const CellBatch*)S.segs, S.taps, w, grid, P.n);
+                                                                (const CellBatch*)S.segs, S.taps, w, ga);
             count_launch();
         }
         cudaError_t e = cudaGetLastError();
         if (e != cudaSuccess) return set_error(SK_ECUDA, std::string("spread2_dmma: ") + cudaGetErrorString(e));
         return SK_OK;
     }
-    if (P.dmma && P.spread_tmapad) {
+    if (P.dmma) {   // d = 3, 2 m_w = 12: the padded DMMA spread on TMA-fed warp pairs
         static std::atomic<unsigned long long> attr{0};
         if (first_on_device(attr)) {
             cudaFuncSetAttribute(spread3_tmapad_kernel<kSegTmaPMax, kSparsePairs, false>,
@@ -216,68 +211,17 @@ inline int spread_dispatch(Plan& P, const NodeSet& S, const double* w, double* g
             const int nt = S.seg_dense ? SpreadTPCfgDense::NT : SpreadTPCfgSparse::NT;
             const size_t sm = S.seg_dense ? SpreadTPCfgDense::SMEM_BYTES : SpreadTPCfgSparse::SMEM_BYTES;
             const int g = persistent_grid(kern, nt, sm, (S.nsitems + np - 1) / np);
-            kern<<<g, nt, sm, s>>>((const SpreadItem*)S.sitems, S.nsitems, (const CellBatch*)S.segs, S.taps, w, grid,
-                                   P.n);
+            kern<<<g, nt, sm, s>>>((const SpreadItem*)S.sitems, S.nsitems, (const CellBatch*)S.segs, S.taps, w, ga);
             count_launch();
         }
         cudaError_t e = cudaGetLastError();
         if (e != cudaSuccess) return set_error(SK_ECUDA, std::string("spread3_tmapad: ") + cudaGetErrorString(e));
         return SK_OK;
     }
-    if (P.dmma && P.spread_tma) {
-        using C = SpreadTCfg;
-        static std::atomic<unsigned long long> attr{0};
-        if (first_on_device(attr)) {
-            cudaFuncSetAttribute(spread3_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM_BYTES);
-        }
-        if (S.nsitems > 0) {
-            const int g = persistent_grid(spread3_tma_kernel, C::NT, C::SMEM_BYTES, (S.nsitems + C::NPAIR - 1) / C::NPAIR);
-            spread3_tma_kernel<<<g, C::NT, C::SMEM_BYTES, s>>>((const SpreadItem*)S.sitems, S.nsitems,
-                                                               (const CellBatch*)S.segs, S.taps, w, grid, P.n);
-            count_launch();
-        }
-        cudaError_t e = cudaGetLastError();
-        if (e != cudaSuccess) return set_error(SK_ECUDA, std::string("spread3_tma: ") + cudaGetErrorString(e));
-        return SK_OK;
-    }
-    if (P.dmma && P.spread_hybrid) {
-        using C = SpreadHCfg;
-        static std::atomic<unsigned long long> attr{0};
-        if (first_on_device(attr)) {
-            cudaFuncSetAttribute(spread3_hybrid_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM_BYTES);
-        }
-        if (S.nsitems > 0) {
-            const int g = persistent_grid(spread3_hybrid_kernel, C::NT, C::SMEM_BYTES, (S.nsitems + C::NWARP - 1) / C::NWARP);
-            spread3_hybrid_kernel<<<g, C::NT, C::SMEM_BYTES, s>>>((const SpreadItem*)S.sitems, S.nsitems,
-                                                                  (const CellBatch*)S.segs, S.taps, w, grid, P.n);
-            count_launch();
-        }
-        cudaError_t e = cudaGetLastError();
-        if (e != cudaSuccess) return set_error(SK_ECUDA, std::string("spread3_hybrid: ") + cudaGetErrorString(e));
-        return SK_OK;
-    }
-    if (P.dmma) {
-        using C = SpreadDCfg;
-        static std::atomic<unsigned long long> attr{0};
-        if (first_on_device(attr)) {
-            cudaFuncSetAttribute(spread3_dmma_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM_BYTES);
-            cudaFuncSetAttribute(spread3_dmma_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM_BYTES);
-        }
-        if (S.nsitems > 0) {
-            const auto kern = S.xpairs ? spread3_dmma_kernel<true> : spread3_dmma_kernel<false>;
-            const int g = persistent_grid(kern, C::NT, C::SMEM_BYTES, (S.nsitems + C::NWARP - 1) / C::NWARP);
-            kern<<<g, C::NT, C::SMEM_BYTES, s>>>((const SpreadItem*)S.sitems, S.nsitems,
-                                                 (const CellBatch*)S.segs, S.taps, w, grid, P.n);
-            count_launch();
-        }
-        cudaError_t e = cudaGetLastError();
-        if (e != cudaSuccess) return set_error(SK_ECUDA, std::string("spread3_dmma: ") + cudaGetErrorString(e));
-        return SK_OK;
-    }
     if (P.tiled && P.d == 3) {
         if (S.nitems > 0) {
-            if (P.win.m == 6) spread3_launch<12>(P, S, w, grid, s);
-            else spread3_launch<16>(P, S, w, grid, s);
+            if (P.win.m == 6) spread3_launch<12>(P, S, w, ga, s);
+            else spread3_launch<16>(P, S, w, ga, s);
             count_launch();
         }
         cudaError_t e = cudaGetLastError();
@@ -285,7 +229,7 @@ inline int spread_dispatch(Plan& P, const NodeSet& S, const double* w, double* g
         return SK_OK;
     }
     if (P.d == 1) {
-        spread_d1_kernel<<<v1_grid(S.count * 2 * P.win.m), 128, 0, s>>>(S.u, S.count, w, P.win, grid);
+        spread_d1_kernel<<<v1_grid(S.count * 2 * P.win.m), 128, 0, s>>>(S.u, S.count, w, P.win, ga);
         count_launch();
         cudaError_t e = cudaGetLastError();
         if (e != cudaSuccess) return set_error(SK_ECUDA, std::string("spread_d1: ") + cudaGetErrorString(e));
@@ -293,9 +237,8 @@ inline int spread_dispatch(Plan& P, const NodeSet& S, const double* w, double* g
     }
     const int g = v1_grid(S.count);
     switch (P.d) {
-        case 1: spread_v1_kernel<1><<<g, 128, 0, s>>>(S.u, S.count, w, P.win, P.n, grid); break;
-        case 2: spread_v1_kernel<2><<<g, 128, 0, s>>>(S.u, S.count, w, P.win, P.n, grid); break;
-        default: spread_v1_kernel<3><<<g, 128, 0, s>>>(S.u, S.count, w, P.win, P.n, grid); break;
+        case 2: spread_v1_kernel<2><<<g, 128, 0, s>>>(S.u, S.count, w, P.win, ga); break;
+        default: spread_v1_kernel<3><<<g, 128, 0, s>>>(S.u, S.count, w, P.win, ga); break;
     }
     count_launch();
     cudaError_t e = cudaGetLastError();

@@ -191,9 +191,11 @@ struct Spread3Cfg {
 template <int W>
 __global__ void __launch_bounds__(Spread3Cfg<W>::NT, 4)
 spread3_v2_kernel(const TileItem* __restrict__ items, int nitems, const double* __restrict__ u,
-                  const double* __restrict__ w, long long count, double* __restrict__ grid, int n,
+                  const double* __restrict__ w, long long count, const GridAcc ga,
                   int tpa, const __grid_constant__ WinPoly wp) {
     using C = Spread3Cfg<W>;
+    const int n = ga.n;
+    const double gscale = grid_scale(ga);
     constexpr int T = C::T, R = C::R, RZ = C::RZ, m = W / 2, CP = C::CP, NCOL = C::NCOL;
     extern __shared__ __align__(16) double smem[];
     double* TX = smem;                     // [CP][TXS]  w * phi_x
@@ -264,7 +266,7 @@ spread3_v2_kernel(const TileItem* __restrict__ items, int nitems, const double* 
             const int rz = idx % R, col = idx / R, ry = col % R, rx = col / R;
             const double val = OUT[col * RZ + rz];
             if (val != 0.0)
-                atomicAdd(&grid[((long long)(gx0 + rx) * n + (gy0 + ry)) * n + (gz0 + rz)], val);
+                grid_add<3>(ga, gscale, gx0 + rx, gy0 + ry, gz0 + rz, val);
         }
     }
 }

@@ -395,3 +395,23 @@ def test_degenerate_geometry_limit(d):
     r = nfft_ref.sinkhorn_fastsum(x, y, a, b, 7.0, 16, 1 / 16, 8, 3)
     assert abs(r["s_cost"]) <= 1e-20
     assert abs(r["s_dual"] + (math.log(5) + math.log(4)) / 7.0) <= 1e-15
+
+
+@pytest.mark.parametrize("d,N,m,tol", [(1, 32, 8, 5e-14), (2, 16, 8, 5e-14), (3, 12, 6, 2e-11), (3, 16, 8, 1e-13)])
+def test_nfft_operator_is_ndft_operator_to_window_error(d, N, m, tol):
+    """NfftFastsumOperator (gridding with the window matrix + FFT + phihat deconvolution)
+    equals FastsumOperator (exact NDFTs) to the Kaiser-Bessel window error at sigma = 2 (pins G2/G3),
+    and its window matrix equals the dense gridding definition grid_spread."""
+    rng = np.random.default_rng(30 + d + m)
+    x, y = rng.random((37, d)), rng.random((41, d))
+    w, wx = rng.random(41), rng.random(37)
+    op = nfft_ref.FastsumOperator(x, y, 20.0, N, 1 / 16, 8)
+    opn = nfft_ref.NfftFastsumOperator(x, y, 20.0, N, 1 / 16, 8, m, 2.0)
+    for k in (0, 1):
+        ref, reft = op.apply(w, False, k), op.apply(wx, True, k)
+        assert np.abs(opn.apply(w, False, k) - ref).max() <= tol * np.abs(ref).max()
+        assert np.abs(opn.apply(wx, True, k) - reft).max() <= tol * np.abs(reft).max()
+    c, rho, _ = nfft_ref.geometry(x, y, 1 / 16, 20.0)
+    ys = nfft_ref.scale(y, c, rho)
+    g = nfft_ref.grid_spread(ys, w, 2 * N, m, 2.0).ravel()
+    assert np.abs(nfft_ref.window_matrix(ys, 2 * N, m, 2.0).T @ w - g).max() <= 1e-15 * np.abs(g).max()

@@ -19,7 +19,8 @@ from synthetic import get, make_inputs, subsample  # noqa: E402
 
 OUT = os.path.join(ROOT, "tests", "golden", "divergence_full.json")
 # relative tolerance the GPU must meet (1e-8 = BJ gate; c2 is conditioning-limited)
-TOL = {"c2": 1e-5, "c3": 1e-8, "c5": 1e-8}
+TOL = {"c2": 1e-5, "c3": 1e-8, "c4": 1e-3, "c5": 1e-8}
+TOL_DUAL = {"c2": 1e-7, "c3": 1e-8, "c4": 1e-4, "c5": 1e-8}
 
 
 def main(names):
@@ -36,7 +37,7 @@ def main(names):
         gold[name] = {
             "s_cost": res["s_cost"], "s_dual": res["s_dual"], "row_resid": res["row_resid"],
             "mass": res["mass"], "subsample": sub, "n": int(x.shape[0]), "m": int(y.shape[0]),
-            "iters": cfg.iters, "tol": TOL[name], "oracle_seconds": dt, "oracle_threads": dense.num_threads(),
+            "iters": cfg.iters, "tol": TOL[name], "tol_dual": TOL_DUAL[name], "enonpos_allowed": name == "c4", "oracle_seconds": dt, "oracle_threads": dense.num_threads(),
             "source": "tools/make_golden.py -> oracle.dense.sinkhorn_divergence (log-domain Alg. 1, P:L261-291)",
         }
         with open(OUT, "w") as fh:

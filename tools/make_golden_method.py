@@ -6,10 +6,13 @@ For each case, on the same seeded inputs:
   dense   oracle.dense.sinkhorn_divergence: log-domain Alg. 1 with exact sums (P:L261-291);
           the exact answer up to FP64 rounding, which dense sums keep relative per entry.
   method  oracle.nfft_ref.sinkhorn_fastsum: Alg. 2 with the method's own fast
-          summation (Eq. (fastsum) P:L622-631 with exact NDFTs, i.e. without the window error):
-          what any faithful implementation of the paper's method computes. Its distance to
-          `dense` is the method's error at these inputs (Fourier truncation, and FP64 rounding
-          of an absolute-error summation amplified by kappa = ||v||_1 / min (K v)).
+          summation (Eq. (fastsum) P:L622-631 with exact NDFTs, i.e. without the window error).
+          Its distance to `dense` is the method's error at these inputs (Fourier truncation, and
+          FP64 rounding of an absolute-error summation amplified by kappa = ||v||_1 / min (K v)).
+  nfft    the same with the complete NFFT fast summation (Kaiser-Bessel window, m_w, sigma:
+          NfftFastsumOperator): what a faithful implementation computes. nfft and method differ
+          only by the window error (~5e-15 per matvec at m_w = 8); their distance at the end of
+          Alg. 2 is the spread that FP64-level matvec perturbations cause at these inputs.
   log10_kappa  from the method run: log10(max(||v||_1 / min K v, ||u||_1 / min K^T u)) at the end.
 
 Cases: c1 at BJ's N = 64 and at N = 96; c2 and c4 on their seeded 3000-point subsamples
@@ -51,11 +54,16 @@ def case(name, cfg, x, y, a, b, lam, N):
     t0 = time.time()
     ref, _, _ = dense.sinkhorn_divergence(x, y, a, b, lam, cfg.iters)
     meth, lk = kappa_log10(x, y, a, b, lam, N, cfg, cfg.iters)
+    nf = nfft_ref.sinkhorn_fastsum(x, y, a, b, lam, N, cfg.eps_B, cfg.p, cfg.iters, window=(cfg.m_w, cfg.sigma))
     rec = {"config": cfg.name, "n": int(x.shape[0]), "m": int(y.shape[0]), "lam": lam, "N": N,
            "iters": cfg.iters, "dense_s_cost": ref["s_cost"], "dense_s_dual": ref["s_dual"],
            "method_s_cost": meth["s_cost"], "method_s_dual": meth["s_dual"],
            "method_rel_err_s_cost": abs(meth["s_cost"] - ref["s_cost"]) / abs(ref["s_cost"]),
            "method_rel_err_s_dual": abs(meth["s_dual"] - ref["s_dual"]) / abs(ref["s_dual"]),
+           "nfft_s_cost": nf["s_cost"], "nfft_s_dual": nf["s_dual"],
+           "nfft_rel_err_s_cost": abs(nf["s_cost"] - ref["s_cost"]) / abs(ref["s_cost"]),
+           "nfft_rel_err_s_dual": abs(nf["s_dual"] - ref["s_dual"]) / abs(ref["s_dual"]),
+           "nfft_vs_method_s_cost": abs(nf["s_cost"] - meth["s_cost"]) / abs(ref["s_cost"]),
            "log10_kappa": lk, "seconds": time.time() - t0}
     print(name, json.dumps(rec), flush=True)
     return rec
