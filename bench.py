@@ -218,6 +218,11 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1 or args.nccl_self:
+        # NCCL prints one "comm ... rank r nranks N ... Init COMPLETE" line per communicator on
+        # stderr, so the ranks of both the torch and the library communicator can be checked
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
     torch.cuda.set_device(local)
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
@@ -334,6 +339,7 @@ def main():
     # ---- fast-summation point-evaluations/s: per direction, median over reps of
     # one fast summation each (CUDA events), max over ranks; also NUFFT points/s = (n_s + n_t)/t
     plan = capi.Plan(ctx, dx, dy, cfg.lam, cfg.N, cfg.sigma, cfg.m_w, cfg.eps_B, cfg.p)
+    box_size = plan.info()["box_size"]
     wy = torch.rand(hy.shape[0], dtype=torch.float64, device="cuda")
     wx = torch.rand(hx.shape[0], dtype=torch.float64, device="cuda")
     ox = torch.empty(hx.shape[0], dtype=torch.float64, device="cuda")
@@ -439,6 +445,12 @@ def main():
         # grid; the pruned d = 3 path moves less than this definition charges)
         "stage_hbm_frac": stage_hbm,
         "gpu_launches": int(launches),
+        "comm": {"world": world, "rank0_of": world,
+                 "backend": "nccl" if (world > 1 or args.nccl_self) else "none (one rank)",
+                 "grid_allreduce_bytes_per_apply": (8 * box_size if (world > 1 or args.nccl_self) else 0),
+                 "collective": "ncclAllReduce(sum, f64) of the touched grid box per fast summation "
+                               "+ scalar all-reduces (DESIGN.md §7)"},
+        "spread_mode": "deterministic (fixed-point)" if os.environ.get("SK_DETERMINISTIC", "1") != "0" else "fp64 atomics",
         "clocks": clk,
         "divergence": {"s_dual": results[0], "s_cost": results[1]} if results else None,
         "kappa_log10_est": results[2].kappa_log10_est if results else None,

@@ -203,7 +203,8 @@ __device__ __forceinline__ void grid_add(const GridAcc& g, double scale, int x, 
 // ranks keeps that property.
 constexpr unsigned long long kNoBad = ~0ULL;
 #ifdef __CUDACC__
-__device__ __forceinline__ void record_bad(unsigned long long* bad, int iter, int rank, long long idx) {
+// (out of line: the failure path stays out of the interpolation epilogue's schedule)
+static __device__ __noinline__ void record_bad(unsigned long long* bad, int iter, int rank, long long idx) {
     const unsigned long long v = ((unsigned long long)(unsigned)iter << 40) |
                                  ((unsigned long long)(rank & 0xff) << 32) | (unsigned long long)(idx & 0xffffffffLL);
     atomicMin(bad, v);
