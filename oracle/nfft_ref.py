@@ -327,7 +327,7 @@ class FastsumOperator:
         return self._trafo(dst, self.coef[kernel] * self._adjoint(src, w))
 
 
-def sinkhorn_fastsum(x, y, a, b, lam, N, eps_B, p, iters):
+def sinkhorn_fastsum(x, y, a, b, lam, N, eps_B, p, iters, window=None):
     """Alg. 2 with the method's own fast summation (FastsumOperator: Eq. (fastsum)
     with exact NDFTs, i.e. the NFFT fast summation without the window error), in the plain
     (scaling) domain exactly as Alg. 2 states it: alpha~ = 1, then per iteration
@@ -340,8 +340,11 @@ def sinkhorn_fastsum(x, y, a, b, lam, N, eps_B, p, iters):
                fast summation).
     This is the statement of the method whose only error against the dense Alg. 1 is the
     regularised kernel's Fourier truncation and FP64 rounding of the sums: it isolates the
-    method's error from an implementation's (SURVEY.md §8(c) consequence (1))."""
-    op = FastsumOperator(x, y, lam, N, eps_B, p)
+    method's error from an implementation's (SURVEY.md §8(c) consequence (1)).
+    window=(m_w, sigma): use NfftFastsumOperator instead -- the complete method with the NFFT's
+    window error, i.e. what a faithful implementation computes up to FP64 rounding."""
+    op = FastsumOperator(x, y, lam, N, eps_B, p) if window is None else \
+        NfftFastsumOperator(x, y, lam, N, eps_B, p, window[0], window[1])
     a = np.asarray(a, dtype=np.float64)
     b = np.asarray(b, dtype=np.float64)
     al, at = np.ones(a.shape[0]), np.ones(b.shape[0])
@@ -357,3 +360,59 @@ def sinkhorn_fastsum(x, y, a, b, lam, N, eps_B, p, iters):
     s_dual = (1.0 + float(a @ np.log(al)) + float(b @ np.log(at)) - S3) / lam
     s_cost = float(al @ op.apply(at, False, 1))
     return dict(s_dual=s_dual, s_cost=s_cost, alpha=al, alpha_t=at, min_t=min_t)
+
+
+def window_matrix(pts_scaled, n, m, sigma):
+    """Sparse Phi[j, l] = prod_a phi(n (x_ja + 1/2) - l_a) over the 2m taps per axis
+    l_a = floor(u_a) - m + 1 .. floor(u_a) + m (u = n (x + 1/2)); row-major flat grid index.
+    The gridding definition of grid_spread / grid_interp as a matrix: g = Phi^T w, t = Phi G
+    (P:L475-477)."""
+    from scipy import sparse
+    pts = np.asarray(pts_scaled, dtype=np.float64)
+    cnt, d = pts.shape
+    u = n * (pts + 0.5)
+    base = np.floor(u).astype(np.int64) - m + 1
+    taps = np.arange(2 * m)
+    vals = np.ones((cnt, 1))
+    flat = np.zeros((cnt, 1), dtype=np.int64)
+    for a in range(d):
+        la = base[:, a:a + 1] + taps[None, :]                    # [cnt, 2m]
+        pa = kb_phi(u[:, a:a + 1] - la, m, sigma)
+        vals = (vals[:, :, None] * pa[:, None, :]).reshape(cnt, -1)
+        flat = (flat[:, :, None] * n + (la % n)[:, None, :]).reshape(cnt, -1)
+    rows = np.repeat(np.arange(cnt), vals.shape[1])
+    return sparse.csr_matrix((vals.ravel(), (rows, flat.ravel())), shape=(cnt, n ** d))
+
+
+class NfftFastsumOperator:
+    """The fast summation exactly as the paper builds it (P:L473-477 + Eq. (fastsum)):
+    adjoint NFFT of the sources (gridding with the Kaiser-Bessel window on the sigma N grid,
+    FFT, division by phihat on the N-band), multiplication by kw_k b_k, NFFT to the targets
+    (division by phihat, inverse FFT, window interpolation). The window error is included, so
+    an implementation of the method matches this up to FP64 rounding."""
+
+    def __init__(self, x, y, lam, N, eps_B, p, m, sigma):
+        x = np.asarray(x, dtype=np.float64).reshape(len(x), -1)
+        y = np.asarray(y, dtype=np.float64).reshape(len(y), -1)
+        self.d = d = x.shape[1]
+        centre, rho, L = geometry(x, y, eps_B, lam)
+        lamp = lam / rho ** 2
+        self.n = n = int(round(sigma * N))
+        self.Phx = window_matrix(scale(x, centre, rho), n, m, sigma)
+        self.Phy = window_matrix(scale(y, centre, rho), n, m, sigma)
+        ks, kw = band(N, d)
+        self.idx = tuple(ks[:, a].astype(int) % n for a in range(d))
+        shift = (-1.0) ** ks.sum(1)          # grid index l <-> position l/n - 1/2
+        ph = np.prod([kb_phihat(ks[:, a], n, m, sigma) for a in range(d)], axis=0)
+        self.deconv = shift / ph
+        self.coef = [kw * bk_sampled(d, N, lamp, rho, kern, L, p).real.reshape(-1) for kern in (0, 1)]
+
+    def apply(self, w, transpose=False, kernel=0):
+        src, dst = (self.Phx, self.Phy) if transpose else (self.Phy, self.Phx)
+        shape = (self.n,) * self.d
+        g = (src.T @ np.asarray(w, dtype=np.float64)).reshape(shape)
+        ahat = np.fft.fftn(g)[self.idx] * self.deconv                 # adjoint NFFT on the band
+        H = np.zeros(shape, dtype=complex)
+        H[self.idx] = self.coef[kernel] * ahat * self.deconv
+        G = (np.fft.ifftn(H) * self.n ** self.d).real                 # NFFT: grid values
+        return dst @ G.ravel()
