@@ -22,6 +22,7 @@ def main():
     ap.add_argument("--reps", type=int, default=3)
     ap.add_argument("--n", type=int, default=0)
     ap.add_argument("--m", type=int, default=0)
+    ap.add_argument("--per-dir", action="store_true", help="also time K v and K^T u separately")
     args = ap.parse_args()
     from paper_2201_07524_b200 import capi
     cfg = get(args.config)
@@ -52,6 +53,13 @@ def main():
     for s, (c, ms) in prof.items():
         if c:
             print(f"{s:10s} launches {c:4d}  avg {ms / c:9.4f} ms")
+    if args.per_dir:   # spread y + interp x (K v), then spread x + interp y (K^T u)
+        for tr, w_ in ((0, w_y), (1, w_x)):
+            for _ in range(args.reps):
+                capi.fastsum_apply(P, w_, tr, 0)
+            torch.cuda.synchronize()
+            prof = capi.sk_profile_read()
+            print(f"  dir {tr}: " + "  ".join(f"{s} {ms / c:.4f}" for s, (c, ms) in prof.items() if c and s in ("spread", "interp")))
     P.close()
     ctx.close()
 
