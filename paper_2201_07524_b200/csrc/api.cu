@@ -363,8 +363,7 @@ int nfft_spread(sk_plan_t plan, int side, const double* w, double* grid) {
     cudaStream_t s = P.ctx->stream;
     const NodeSet& S = P.side[side];
     SK_TRY(launch_permute_in(w, S.perm, S.count, P.w_sorted, s));
-    SK_CUDA(cudaMemsetAsync(grid, 0, sizeof(double) * P.grid_size, s));
-    SK_TRY(launch_spread(P, side, P.w_sorted, grid, s));
+    SK_TRY(launch_spread(P, side, P.w_sorted, grid, s));   // writes every grid cell
     return SK_OK;
 }
 

@@ -781,12 +781,16 @@ int launch_multiply(Plan& P, int kernel, cudaStream_t s) {
 }
 
 // ------------------------------------------------------------------ a2 / a7: spread, interp
-// Deterministic spread (GridAcc): max |w_j| as the bits of a non-negative double (their integer
-// order is the value order, so atomicMax on the bits is a max on the values; NaN sorts last).
-__global__ void abs_max_bits_kernel(const double* __restrict__ w, long long count, unsigned long long* out) {
+// Deterministic spread (GridAcc), before the spread: zero the fixed-point box accumulator and
+// take max |w_j| as the bits of a non-negative double (their integer order is the value order, so
+// atomicMax on the bits is a max on the values; NaN sorts last). out[0] must be 0 on entry
+// (grid_fix_convert_kernel leaves it so).
+__global__ void det_prepare_kernel(const double* __restrict__ w, long long count, unsigned long long* __restrict__ acc,
+                                   long long acc_words, unsigned long long* __restrict__ wmax) {
+    const long long tid = blockIdx.x * (long long)blockDim.x + threadIdx.x, stride = (long long)gridDim.x * blockDim.x;
+    for (long long k = tid; k < acc_words; k += stride) acc[k] = 0ULL;
     unsigned long long mx = 0;
-    for (long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x; k < count;
-         k += (long long)gridDim.x * blockDim.x) {
+    for (long long k = tid; k < count; k += stride) {
         const unsigned long long b = (unsigned long long)__double_as_longlong(fabs(w[k]));
         mx = b > mx ? b : mx;
     }
@@ -794,51 +798,70 @@ __global__ void abs_max_bits_kernel(const double* __restrict__ w, long long coun
         const unsigned long long t = __shfl_xor_sync(0xffffffffu, mx, o);
         mx = t > mx ? t : mx;
     }
-    if ((threadIdx.x & 31) == 0 && mx) atomicMax(out, mx);
+    if ((threadIdx.x & 31) == 0 && mx) atomicMax(wmax, mx);
 }
 
-// Fixed-point box accumulator -> FP64 grid: X = hi 2^32 + lo exactly (carry of lo folded into
-// hi), value = X 2^-S; cells outside the box keep the caller's zeros.
-__global__ void grid_fix_convert_kernel(const GridAcc ga, int d, long long box_size) {
+// Fixed-point box accumulator -> FP64 grid over the WHOLE grid (zeros outside the box, so no
+// separate memset): X = hi 2^32 + lo exactly (carry of lo folded into hi), value = X 2^-S. The
+// last block to finish resets max |w| for the next spread.
+__global__ void grid_fix_convert_kernel(const GridAcc ga, int d, long long grid_size, unsigned int* __restrict__ done,
+                                        unsigned long long* __restrict__ wmax_reset) {
     const double wm = __longlong_as_double((long long)*ga.wmax);
     const double inv = 1.0 / grid_scale(ga);
     const bool finite = isfinite(wm);
-    for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < box_size;
-         e += (long long)gridDim.x * blockDim.x) {
-        const long long hi = (long long)ga.acc[2 * e];
-        const unsigned long long lo = ga.acc[2 * e + 1];
-        const long long H = hi + (long long)(lo >> 32);
-        const double L = (double)(lo & 0xffffffffULL);
-        const double v = finite ? fma((double)H, 4294967296.0, L) * inv : NAN;
-        long long rest = e, gi = 0, mul = 1;
+    for (long long gi = blockIdx.x * (long long)blockDim.x + threadIdx.x; gi < grid_size;
+         gi += (long long)gridDim.x * blockDim.x) {
+        long long rest = gi, bi = 0, mul = 1;
+        bool in = true;
         for (int a = d - 1; a >= 0; --a) {
-            const int c = (int)(rest % ga.bn[a]);
-            rest /= ga.bn[a];
-            gi += (long long)(ga.lo[a] + c) * mul;
-            mul *= ga.n;
+            const int c = (int)(rest % ga.n) - ga.lo[a];
+            rest /= ga.n;
+            in = in && c >= 0 && c < ga.bn[a];
+            bi += (long long)c * mul;
+            mul *= ga.bn[a];
+        }
+        double v = 0.0;
+        if (in) {
+            const long long hi = (long long)ga.acc[2 * bi];
+            const unsigned long long lo = ga.acc[2 * bi + 1];
+            const long long H = hi + (long long)(lo >> 32);
+            const double L = (double)(lo & 0xffffffffULL);
+            v = finite ? fma((double)H, 4294967296.0, L) * inv : NAN;
         }
         ga.grid[gi] = v;
+    }
+    // every block has read *wmax above; the last one to arrive clears it for the next apply
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        if (atomicAdd(done, 1u) == gridDim.x - 1) {
+            *wmax_reset = 0ULL;
+            *done = 0u;
+        }
     }
 }
 
 int launch_spread(Plan& P, int side, const double* w_sorted, double* grid, cudaStream_t s) {
     const NodeSet& S = P.side[side];
+    if (S.count <= 0 || !P.deterministic) SK_CUDA(cudaMemsetAsync(grid, 0, sizeof(double) * P.grid_size, s));
     if (S.count <= 0) return SK_OK;
     GridAcc ga;
     ga.grid = grid;
     ga.n = P.n;
     ga.phi0d = P.phi0d;
     for (int a = 0; a < P.d; ++a) { ga.lo[a] = P.box_lo[a]; ga.bn[a] = P.box_n[a]; }
+    unsigned long long* wmax = P.det_acc + 2 * P.box_size;
     if (P.deterministic) {
         ga.acc = P.det_acc;
-        ga.wmax = P.det_acc + 2 * P.box_size;
-        SK_CUDA(cudaMemsetAsync(P.det_acc, 0, sizeof(unsigned long long) * (2 * P.box_size + 1), s));
-        abs_max_bits_kernel<<<grid_for(S.count, 256), 256, 0, s>>>(w_sorted, S.count, P.det_acc + 2 * P.box_size);
+        ga.wmax = wmax;
+        const long long words = 2 * P.box_size;
+        det_prepare_kernel<<<grid_for(std::max(words, S.count), 256), 256, 0, s>>>(w_sorted, S.count, P.det_acc, words, wmax);
         SK_LAUNCH_CHECK();
     }
     SK_TRY(spread_dispatch(P, S, w_sorted, ga, s));
     if (P.deterministic) {
-        grid_fix_convert_kernel<<<grid_for(P.box_size, 256), 256, 0, s>>>(ga, P.d, P.box_size);
+        grid_fix_convert_kernel<<<grid_for(P.grid_size, 256), 256, 0, s>>>(
+            ga, P.d, P.grid_size, reinterpret_cast<unsigned int*>(wmax + 1), wmax);
         SK_LAUNCH_CHECK();
     }
     return SK_OK;

@@ -786,9 +786,12 @@ int build_plan(Ctx* ctx, Plan** out, int d, const double* x, long long n, const 
     if ((st = alloc((void**)&P->u_s, sizeof(double) * (std::max(n, 1LL) + 2)))) return fail(st);
     if ((st = alloc((void**)&P->b_s, sizeof(double) * std::max(m, 1LL)))) return fail(st);
     if ((st = alloc((void**)&P->v_s, sizeof(double) * (std::max(m, 1LL) + 2)))) return fail(st);
-    if (P->deterministic &&
-        (st = alloc((void**)&P->det_acc, sizeof(unsigned long long) * (2 * std::max(P->box_size, 1LL) + 1))))
-        return fail(st);
+    if (P->deterministic) {   // [2 box][max |w| bits][block counter of the conversion], all zero
+        const size_t words = 2 * std::max(P->box_size, 1LL) + 2;
+        if ((st = alloc((void**)&P->det_acc, sizeof(unsigned long long) * words))) return fail(st);
+        if (cudaMemsetAsync(P->det_acc, 0, sizeof(unsigned long long) * words, s) != cudaSuccess)
+            return fail(set_error(SK_ECUDA, "memset det_acc"));
+    }
     P->box_exchange = ctx->world > 1 || ctx->nccl_comm || getenv("SK_FORCE_BOX_EXCHANGE") != nullptr;
     if (P->box_exchange && (st = alloc((void**)&P->box_buf, sizeof(double) * std::max(P->box_size, 1LL))))
         return fail(st);
@@ -836,8 +839,7 @@ int apply_sorted(Plan& P, int transpose, int kernel, const double* w_sorted, dou
     cudaStream_t s = P.ctx->stream;
     const int src = transpose ? 0 : 1, dst = transpose ? 1 : 0;
     prof_begin(ST_SPREAD, s);
-    SK_CUDA(cudaMemsetAsync(P.grid, 0, sizeof(double) * P.grid_size, s));
-    SK_TRY(launch_spread(P, src, w_sorted, P.grid, s));
+    SK_TRY(launch_spread(P, src, w_sorted, P.grid, s));   // writes every grid cell
     prof_end(ST_SPREAD, s);
     if (P.box_exchange) {
         // a3: sum the partial grids of all ranks over the touched box only (pack, NCCL
