@@ -351,7 +351,7 @@ int fastsum_apply(sk_plan_t plan, int transpose, int kernel, const double* w, do
     const NodeSet& src = P.side[transpose ? 0 : 1];
     const NodeSet& dst = P.side[transpose ? 1 : 0];
     if ((src.count > 0 && !w) || (dst.count > 0 && !t)) return set_error(SK_EINVAL, "NULL w/t");
-    SK_TRY(launch_permute_in(w, src.perm, src.count, P.w_sorted, s));
+    SK_TRY(launch_permute_in(w, src.perm, src.count, P.w_sorted, s, wslot(P, WSLOT_W)));
     SK_TRY(apply_sorted(P, transpose, kernel, P.w_sorted, P.t_sorted));
     SK_TRY(launch_permute_out(P.t_sorted, dst.perm, dst.count, t, s));
     return SK_OK;
@@ -362,7 +362,7 @@ int nfft_spread(sk_plan_t plan, int side, const double* w, double* grid) {
     Plan& P = *plan->p;
     cudaStream_t s = P.ctx->stream;
     const NodeSet& S = P.side[side];
-    SK_TRY(launch_permute_in(w, S.perm, S.count, P.w_sorted, s));
+    SK_TRY(launch_permute_in(w, S.perm, S.count, P.w_sorted, s, wslot(P, WSLOT_W)));
     SK_TRY(launch_spread(P, side, P.w_sorted, grid, s));   // writes every grid cell
     return SK_OK;
 }
@@ -476,8 +476,10 @@ static int run_impl(sk_plan_t plan, const double* a, const double* b, int iters,
     SK_TRY(launch_permute_in(a, X.perm, X.count, P.a_s, s));
     SK_TRY(launch_permute_in(b, Y.perm, Y.count, P.b_s, s));
     SK_TRY(check_weights(P));
+    // u is rewritten (and its bound recorded) before it is first spread; v is spread first
     SK_TRY(launch_permute_in(u, X.perm, X.count, P.u_s, s));
-    SK_TRY(launch_permute_in(v, Y.perm, Y.count, P.v_s, s));
+    if (wslot(P, WSLOT_U)) SK_CUDA(cudaMemsetAsync(wslot(P, WSLOT_U), 0, sizeof(unsigned), s));
+    SK_TRY(launch_permute_in(v, Y.perm, Y.count, P.v_s, s, wslot(P, WSLOT_V)));
     const unsigned long long nobad[2] = {kNoBad, kNoBad};
     SK_CUDA(cudaMemcpyAsync(P.bad64, nobad, sizeof(nobad), cudaMemcpyHostToDevice, s));
     // resources released on every exit path
@@ -520,7 +522,7 @@ static int run_impl(sk_plan_t plan, const double* a, const double* b, int iters,
             if (rescale_policy == 1) SK_TRY(allreduce_sum(C, r, 1));
             else SK_TRY(allreduce_minmax(C, r + 600, r, 1));
             SK_TRY(launch_rescale_factor(r, rescale_policy, (double)Y.total, s));
-            SK_TRY(launch_scale_vec(P.v_s, Y.count, r, s));
+            SK_TRY(launch_scale_vec(P.v_s, Y.count, r, s, wslot(P, WSLOT_V)));
         }
         if (last) SK_TRY(launch_reduce_sum_log(nullptr, P.v_s, Y.count, slot(P, SL_D), 1, s));
         // odd Delta: t = K v, u = a / t   (Eq. (even_F_sink)). Without a residual or
@@ -530,6 +532,7 @@ static int run_impl(sk_plan_t plan, const double* a, const double* b, int iters,
         FusedUpd fu_u;
         fu_u.p = P.a_s; fu_u.x = P.u_s; fu_u.bad = P.bad64; fu_u.iter_dev = iter_dev; fu_u.iter = it;
         fu_u.rank = C->rank;
+        fu_u.xmax = wslot(P, WSLOT_U);
         SK_TRY(apply_sorted(P, 0, 0, P.v_s, P.t_sorted, want_u ? nullptr : &fu_u));
         if (want_u) {
             prof_begin(ST_UPDATE, s);
@@ -545,6 +548,7 @@ static int run_impl(sk_plan_t plan, const double* a, const double* b, int iters,
         FusedUpd fu_v;
         fu_v.p = P.b_s; fu_v.x = P.v_s; fu_v.bad = P.bad64 + 1; fu_v.iter_dev = iter_dev; fu_v.iter = it;
         fu_v.rank = C->rank;
+        fu_v.xmax = wslot(P, WSLOT_V);
         SK_TRY(apply_sorted(P, 1, 0, P.u_s, P.t_sorted, want_v ? nullptr : &fu_v));
         if (want_v) {
             prof_begin(ST_UPDATE, s);
@@ -695,8 +699,8 @@ int sinkhorn_divergence(sk_plan_t plan, const double* a, const double* b, const 
     if ((X.count > 0 && (!a || !u)) || (Y.count > 0 && (!b || !v))) return set_error(SK_EINVAL, "NULL a/b/u/v");
     SK_TRY(launch_permute_in(a, X.perm, X.count, P.a_s, s));
     SK_TRY(launch_permute_in(b, Y.perm, Y.count, P.b_s, s));
-    SK_TRY(launch_permute_in(u, X.perm, X.count, P.u_s, s));
-    SK_TRY(launch_permute_in(v, Y.perm, Y.count, P.v_s, s));
+    SK_TRY(launch_permute_in(u, X.perm, X.count, P.u_s, s, wslot(P, WSLOT_U)));
+    SK_TRY(launch_permute_in(v, Y.perm, Y.count, P.v_s, s, wslot(P, WSLOT_V)));
     double* sc = slot(P, SL_SCALARS);
     // S1 = sum a log u, S2 = sum b log v
     SK_TRY(launch_reduce_sum_log(P.a_s, P.u_s, X.count, slot(P, SL_A), 0, s));

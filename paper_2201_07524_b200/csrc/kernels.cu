@@ -231,10 +231,15 @@ int launch_tile_offsets(const int* sorted_keys, long long count, int ntiles, int
 
 // ------------------------------------------------------------------ permutations / vectors
 __global__ void permute_in_kernel(const double* __restrict__ src, const int* __restrict__ perm,
-                                  long long count, double* __restrict__ dst) {
+                                  long long count, double* __restrict__ dst, unsigned* __restrict__ slot) {
+    unsigned mx = 0;
     for (long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x; k < count;
-         k += (long long)gridDim.x * blockDim.x)
-        dst[k] = src[perm[k]];
+         k += (long long)gridDim.x * blockDim.x) {
+        const double v = src[perm[k]];
+        dst[k] = v;
+        mx = max(mx, absmax_hi(v));
+    }
+    if (slot) note_absmax(slot, mx);
 }
 __global__ void permute_out_kernel(const double* __restrict__ src, const int* __restrict__ perm,
                                    long long count, double* __restrict__ dst) {
@@ -242,9 +247,13 @@ __global__ void permute_out_kernel(const double* __restrict__ src, const int* __
          k += (long long)gridDim.x * blockDim.x)
         dst[perm[k]] = src[k];
 }
-int launch_permute_in(const double* src, const int* perm, long long count, double* dst, cudaStream_t s) {
+unsigned* wslot(Plan& P, int k) { return P.det_wmax ? P.det_wmax + k : nullptr; }
+
+int launch_permute_in(const double* src, const int* perm, long long count, double* dst, cudaStream_t s,
+                      unsigned* slot) {
+    if (slot) SK_CUDA(cudaMemsetAsync(slot, 0, sizeof(unsigned), s));
     if (count <= 0) return SK_OK;
-    permute_in_kernel<<<grid_for(count, 256), 256, 0, s>>>(src, perm, count, dst);
+    permute_in_kernel<<<grid_for(count, 256), 256, 0, s>>>(src, perm, count, dst, slot);
     SK_LAUNCH_CHECK();
     return SK_OK;
 }
@@ -304,15 +313,23 @@ int launch_fill(double* p, long long count, double v, cudaStream_t s) {
     return SK_OK;
 }
 
-__global__ void scale_vec_kernel(double* p, long long count, const double* __restrict__ sc) {
+__global__ void scale_vec_kernel(double* p, long long count, const double* __restrict__ sc,
+                                 unsigned* __restrict__ slot) {
     const double c = *sc;
+    unsigned mx = 0;
     for (long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x; k < count;
-         k += (long long)gridDim.x * blockDim.x)
-        p[k] *= c;
+         k += (long long)gridDim.x * blockDim.x) {
+        const double v = p[k] * c;
+        p[k] = v;
+        mx = max(mx, absmax_hi(v));
+    }
+    if (slot) note_absmax(slot, mx);
 }
-int launch_scale_vec(double* p, long long count, const double* scale_dev, cudaStream_t s) {
+// slot (deterministic spread): the bound slot of p, re-measured for the scaled vector
+int launch_scale_vec(double* p, long long count, const double* scale_dev, cudaStream_t s, unsigned* slot) {
+    if (slot) SK_CUDA(cudaMemsetAsync(slot, 0, sizeof(unsigned), s));
     if (count <= 0) return SK_OK;
-    scale_vec_kernel<<<grid_for(count, 256), 256, 0, s>>>(p, count, scale_dev);
+    scale_vec_kernel<<<grid_for(count, 256), 256, 0, s>>>(p, count, scale_dev, slot);
     SK_LAUNCH_CHECK();
     return SK_OK;
 }
@@ -414,9 +431,10 @@ int launch_finalize_partials(const double* red, int nparts, int nvals, double* o
 __global__ void update_kernel(const double* __restrict__ t, const double* __restrict__ p,
                               double* __restrict__ x, long long count, int want_resid, int iter,
                               const int* __restrict__ iter_dev, unsigned long long* __restrict__ bad,
-                              int rank, double* __restrict__ partial) {
+                              int rank, unsigned* __restrict__ xmax, double* __restrict__ partial) {
     __shared__ double sh[kRedBlock / 32];
     double res = 0.0, tmin = INFINITY, kl = 0.0, slog = 0.0;
+    unsigned mx = 0;
     if (iter_dev) iter = *iter_dev;   // graph replay: iteration number from the device counter
     for (long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x; k < count;
          k += (long long)gridDim.x * blockDim.x) {
@@ -430,7 +448,9 @@ __global__ void update_kernel(const double* __restrict__ t, const double* __rest
         tmin = fmin(tmin, tk);
         if (!(tk > 1e-300) || !isfinite(tk)) record_bad(bad, iter, rank, k);   // SK_ENONPOS (tau_pos = 1e-300)
         x[k] = xn;
+        mx = max(mx, absmax_hi(xn));
     }
+    if (xmax) note_absmax(xmax, mx);
     const double r0 = block_sum<kRedBlock>(res, sh);
     const double r1 = block_min<kRedBlock>(tmin, sh);
     const double r2 = want_resid == 2 ? block_sum<kRedBlock>(kl, sh) : 0.0;
@@ -447,7 +467,8 @@ int launch_update(Plan& P, int side, const double* t_sorted, const double* p_sor
                   double* x_sorted, int want_resid, int iter, const int* iter_dev, cudaStream_t s) {
     long long count = P.side[side].count;  // count == 0 still writes neutral partials
     update_kernel<<<kRedGrid, kRedBlock, 0, s>>>(t_sorted, p_sorted, x_sorted, count, want_resid,
-                                                 iter, iter_dev, P.bad64 + side, P.ctx->rank, P.red);
+                                                 iter, iter_dev, P.bad64 + side, P.ctx->rank,
+                                                 wslot(P, side == 0 ? WSLOT_U : WSLOT_V), P.red);
     SK_LAUNCH_CHECK();
     return SK_OK;
 }
@@ -781,34 +802,25 @@ int launch_multiply(Plan& P, int kernel, cudaStream_t s) {
 }
 
 // ------------------------------------------------------------------ a2 / a7: spread, interp
-// Deterministic spread (GridAcc), before the spread: zero the fixed-point box accumulator and
-// take max |w_j| as the bits of a non-negative double (their integer order is the value order, so
-// atomicMax on the bits is a max on the values; NaN sorts last). out[0] must be 0 on entry
-// (grid_fix_convert_kernel leaves it so).
-__global__ void det_prepare_kernel(const double* __restrict__ w, long long count, unsigned long long* __restrict__ acc,
-                                   long long acc_words, unsigned long long* __restrict__ wmax) {
-    const long long tid = blockIdx.x * (long long)blockDim.x + threadIdx.x, stride = (long long)gridDim.x * blockDim.x;
-    for (long long k = tid; k < acc_words; k += stride) acc[k] = 0ULL;
-    unsigned long long mx = 0;
-    for (long long k = tid; k < count; k += stride) {
-        const unsigned long long b = (unsigned long long)__double_as_longlong(fabs(w[k]));
-        mx = b > mx ? b : mx;
-    }
-    for (int o = 16; o > 0; o >>= 1) {
-        const unsigned long long t = __shfl_xor_sync(0xffffffffu, mx, o);
-        mx = t > mx ? t : mx;
-    }
-    if ((threadIdx.x & 31) == 0 && mx) atomicMax(wmax, mx);
+// Deterministic spread (GridAcc): max |w_j| bound of a source vector that no producer recorded
+// (fastsum_apply / nfft_spread record theirs in permute_in): the slot must be zero on entry.
+__global__ void absmax_kernel(const double* __restrict__ w, long long count, unsigned* __restrict__ slot) {
+    unsigned mx = 0;
+    for (long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x; k < count;
+         k += (long long)gridDim.x * blockDim.x)
+        mx = max(mx, absmax_hi(w[k]));
+    note_absmax(slot, mx);
 }
 
 // Fixed-point box accumulator -> FP64 grid over the WHOLE grid (zeros outside the box, so no
-// separate memset): X = hi 2^32 + lo exactly (carry of lo folded into hi), value = X 2^-S. The
-// last block to finish resets max |w| for the next spread.
-__global__ void grid_fix_convert_kernel(const GridAcc ga, int d, long long grid_size, unsigned int* __restrict__ done,
-                                        unsigned long long* __restrict__ wmax_reset) {
-    const double wm = __longlong_as_double((long long)*ga.wmax);
+// separate memset): X = hi 2^32 + lo exactly (carry of lo folded into hi), value = X 2^-S. Each
+// accumulator word is cleared after it is read, and the last block to finish clears the source
+// vector's bound slot, so the next spread starts from zero without another launch.
+__global__ void grid_fix_convert_kernel(const GridAcc ga, int d, long long grid_size, unsigned* __restrict__ done,
+                                        unsigned* __restrict__ slot) {
+    const unsigned hi = *ga.wmax;
     const double inv = 1.0 / grid_scale(ga);
-    const bool finite = isfinite(wm);
+    const bool finite = isfinite(__longlong_as_double((long long)(((unsigned long long)hi << 32) | 0xffffffffULL)));
     for (long long gi = blockIdx.x * (long long)blockDim.x + threadIdx.x; gi < grid_size;
          gi += (long long)gridDim.x * blockDim.x) {
         long long rest = gi, bi = 0, mul = 1;
@@ -822,20 +834,22 @@ __global__ void grid_fix_convert_kernel(const GridAcc ga, int d, long long grid_
         }
         double v = 0.0;
         if (in) {
-            const long long hi = (long long)ga.acc[2 * bi];
-            const unsigned long long lo = ga.acc[2 * bi + 1];
-            const long long H = hi + (long long)(lo >> 32);
-            const double L = (double)(lo & 0xffffffffULL);
+            const long long hw = (long long)ga.acc[2 * bi];
+            const unsigned long long lw = ga.acc[2 * bi + 1];
+            ga.acc[2 * bi] = 0ULL;
+            ga.acc[2 * bi + 1] = 0ULL;
+            const long long H = hw + (long long)(lw >> 32);
+            const double L = (double)(lw & 0xffffffffULL);
             v = finite ? fma((double)H, 4294967296.0, L) * inv : NAN;
         }
         ga.grid[gi] = v;
     }
-    // every block has read *wmax above; the last one to arrive clears it for the next apply
+    // every block has read the slot above; the last one to arrive clears it for the next producer
     __syncthreads();
     if (threadIdx.x == 0) {
         __threadfence();
         if (atomicAdd(done, 1u) == gridDim.x - 1) {
-            *wmax_reset = 0ULL;
+            *slot = 0u;
             *done = 0u;
         }
     }
@@ -850,18 +864,24 @@ int launch_spread(Plan& P, int side, const double* w_sorted, double* grid, cudaS
     ga.n = P.n;
     ga.phi0d = P.phi0d;
     for (int a = 0; a < P.d; ++a) { ga.lo[a] = P.box_lo[a]; ga.bn[a] = P.box_n[a]; }
-    unsigned long long* wmax = P.det_acc + 2 * P.box_size;
+    unsigned* slot = nullptr;
     if (P.deterministic) {
+        // the bound recorded by the vector's producer; otherwise measure it now
+        slot = w_sorted == P.w_sorted ? wslot(P, WSLOT_W)
+             : (w_sorted == P.u_s ? wslot(P, WSLOT_U) : (w_sorted == P.v_s ? wslot(P, WSLOT_V) : nullptr));
+        if (!slot) {
+            slot = wslot(P, WSLOT_TMP);
+            SK_CUDA(cudaMemsetAsync(slot, 0, sizeof(unsigned), s));
+            absmax_kernel<<<grid_for(S.count, 256), 256, 0, s>>>(w_sorted, S.count, slot);
+            SK_LAUNCH_CHECK();
+        }
         ga.acc = P.det_acc;
-        ga.wmax = wmax;
-        const long long words = 2 * P.box_size;
-        det_prepare_kernel<<<grid_for(std::max(words, S.count), 256), 256, 0, s>>>(w_sorted, S.count, P.det_acc, words, wmax);
-        SK_LAUNCH_CHECK();
+        ga.wmax = slot;
     }
     SK_TRY(spread_dispatch(P, S, w_sorted, ga, s));
     if (P.deterministic) {
-        grid_fix_convert_kernel<<<grid_for(P.grid_size, 256), 256, 0, s>>>(
-            ga, P.d, P.grid_size, reinterpret_cast<unsigned int*>(wmax + 1), wmax);
+        grid_fix_convert_kernel<<<grid_for(P.grid_size, 256), 256, 0, s>>>(ga, P.d, P.grid_size, P.det_wmax + kWSlots,
+                                                                           slot);
         SK_LAUNCH_CHECK();
     }
     return SK_OK;

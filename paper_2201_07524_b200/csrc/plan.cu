@@ -391,7 +391,13 @@ static int build_cell_lists(Plan& P, NodeSet& S, cudaStream_t s) {
     CellGeom g{d, n, tpa, T, Td, P.spread_xpairs ? 1 : 0, 0};
     // spread work-unit size: enough items to keep ~4 per resident warp busy (148 SMs x 8
     // warps), at most kSpreadItemMax nodes (one region flush per item)
-    const int item_max = (int)std::max((long long)SK_SPREAD_ITEM_MIN, std::min((long long)kSpreadItemMax, count / 4736));
+    // (the floor is a runtime knob for measurements: SK_SPREAD_ITEM_MIN overrides the default)
+    static const long long item_min_env = getenv("SK_SPREAD_ITEM_MIN") ? atoll(getenv("SK_SPREAD_ITEM_MIN")) : 0;
+    // deterministic flushes cost twice the atomics: a larger floor for small sets (measured, DESIGN.md
+    // §6: img512 spread 44 -> 34 us at 128 nodes, c2 26.9 -> 27.6 us; c3 / c4 / c5 items are larger)
+    const long long item_min = item_min_env > 0 ? item_min_env
+                                                : (P.deterministic ? 2LL * SK_SPREAD_ITEM_MIN : (long long)SK_SPREAD_ITEM_MIN);
+    const int item_max = (int)std::max(item_min, std::min((long long)kSpreadItemMax, count / 4736));
 
     // run-length encode the sorted keys; 7 int arrays of nruns (<= count) entries
     int* buf = nullptr;
@@ -786,11 +792,12 @@ int build_plan(Ctx* ctx, Plan** out, int d, const double* x, long long n, const 
     if ((st = alloc((void**)&P->u_s, sizeof(double) * (std::max(n, 1LL) + 2)))) return fail(st);
     if ((st = alloc((void**)&P->b_s, sizeof(double) * std::max(m, 1LL)))) return fail(st);
     if ((st = alloc((void**)&P->v_s, sizeof(double) * (std::max(m, 1LL) + 2)))) return fail(st);
-    if (P->deterministic) {   // [2 box][max |w| bits][block counter of the conversion], all zero
-        const size_t words = 2 * std::max(P->box_size, 1LL) + 2;
+    if (P->deterministic) {   // [2 box] accumulator, then 4 bound slots + the conversion's counter, all zero
+        const size_t words = 2 * std::max(P->box_size, 1LL) + 4;
         if ((st = alloc((void**)&P->det_acc, sizeof(unsigned long long) * words))) return fail(st);
         if (cudaMemsetAsync(P->det_acc, 0, sizeof(unsigned long long) * words, s) != cudaSuccess)
             return fail(set_error(SK_ECUDA, "memset det_acc"));
+        P->det_wmax = reinterpret_cast<unsigned*>(P->det_acc + 2 * std::max(P->box_size, 1LL));
     }
     P->box_exchange = ctx->world > 1 || ctx->nccl_comm || getenv("SK_FORCE_BOX_EXCHANGE") != nullptr;
     if (P->box_exchange && (st = alloc((void**)&P->box_buf, sizeof(double) * std::max(P->box_size, 1LL))))

@@ -145,7 +145,8 @@ struct Plan {
     bool spread_tmapad = false;  // d = 3 spread: the padded DMMA spread on TMA-fed warp pairs
     // deterministic spread (GridAcc): fixed-point box accumulator [box_size][2] + 1 word max |w|
     bool deterministic = false;
-    unsigned long long* det_acc = nullptr;
+    unsigned long long* det_acc = nullptr;   // [2 box_size] accumulator, then 8 uint: 4 bound slots,
+    unsigned* det_wmax = nullptr;            // the conversion's block counter (zeroed at plan time)
     double phi0d = 1.0;          // phi(0)^d: the largest product of d window taps
     bool spread_xpairs = false;  // d = 3 padded spread: x-minor keys; sides with sparse cells group
                                  // x-pairs of cells into one segment (13 of 16 rows)
@@ -157,25 +158,41 @@ struct Plan {
 // contribution v is rounded once to an integer multiple of 2^-S, X = rint(v 2^S), and added as
 // two 64-bit integer words X = hi 2^32 + lo (hi signed, lo in [0, 2^32)) into a fixed-point
 // accumulator over the touched box; integer addition is associative, so the sum does not depend
-// on the order and the grid is bit-identical from run to run. S = 61 - ilogb(max|w| phi(0)^d):
-// one node contributes < 2^62 and a cell sum of <= 2^31 nodes stays < 2^93 (hi < 2^61, the lo
-// sum of <= 2^31 contributions < 2^63); the rounding is <= 2^-63 of the largest single-node
-// contribution. grid_fix_convert writes the box back as FP64.
+// on the order and the grid is bit-identical from run to run. S = 61 - ilogb(B phi(0)^d) with
+// B >= max_j |w_j| (B from the high 32 bits of max |w|, at most 2x above it): one node contributes
+// < 2^62 and a cell sum of <= 2^31 nodes stays < 2^93 (hi < 2^61, the lo sum of <= 2^31
+// contributions < 2^63); the rounding is <= 2^-62 of the largest single-node contribution.
+// The kernel that produces a spread's source vector (the permutation into sorted order, the
+// fused Sinkhorn update) records B (note_absmax) in the vector's bound slot; grid_fix_convert
+// writes the grid back as FP64, clears the accumulator and the slot.
 struct GridAcc {
-    double* grid = nullptr;                     // [n^d] FP64 (atomic mode; conversion target)
-    unsigned long long* acc = nullptr;          // deterministic: [box cells][2] (hi, lo)
-    const unsigned long long* wmax = nullptr;   // deterministic: bits of max_j |w_j| (device)
-    double phi0d = 1.0;                         // phi(0)^d, the largest product of d taps
-    int n = 0;                                  // grid edge
-    int lo[3] = {0, 0, 0};                      // box origin and extent per axis
+    double* grid = nullptr;                 // [n^d] FP64 (atomic mode; conversion target)
+    unsigned long long* acc = nullptr;      // deterministic: [box cells][2] (hi, lo)
+    const unsigned int* wmax = nullptr;     // deterministic: high 32 bits of max_j |w_j| (device)
+    double phi0d = 1.0;                     // phi(0)^d, the largest product of d taps
+    int n = 0;                              // grid edge
+    int lo[3] = {0, 0, 0};                  // box origin and extent per axis
     int bn[3] = {1, 1, 1};
 };
+// bound slots of the deterministic spread's source vectors (Plan::det_wmax[k])
+enum { WSLOT_W = 0, WSLOT_U = 1, WSLOT_V = 2, WSLOT_TMP = 3, kWSlots = 4 };
 #ifdef __CUDACC__
-// 2^S of the deterministic mode (1 in atomic mode)
+// high 32 bits of |x| (monotone in |x| for doubles; NaN sorts above every number)
+__device__ __forceinline__ unsigned absmax_hi(double x) {
+    return (unsigned)((unsigned long long)__double_as_longlong(fabs(x)) >> 32);
+}
+// max of the converged lanes' values into a bound slot (one atomic per warp)
+__device__ __forceinline__ void note_absmax(unsigned* slot, unsigned hi) {
+    const unsigned mask = __activemask();
+    const unsigned mx = __reduce_max_sync(mask, hi);
+    if ((int)(threadIdx.x & 31) == __ffs(mask) - 1 && mx) atomicMax(slot, mx);
+}
+// 2^S of the deterministic mode (1 in atomic mode, for all-zero or non-finite weights)
 __device__ __forceinline__ double grid_scale(const GridAcc& g) {
     if (!g.acc) return 1.0;
-    const double c = __longlong_as_double((long long)*g.wmax) * g.phi0d;
-    return c > 0.0 ? ldexp(1.0, 61 - ilogb(c)) : 1.0;
+    const unsigned hi = *g.wmax;
+    const double c = __longlong_as_double((long long)(((unsigned long long)hi << 32) | 0xffffffffULL)) * g.phi0d;
+    return (hi != 0 && isfinite(c)) ? ldexp(1.0, 61 - ilogb(c)) : 1.0;
 }
 template <int D>
 __device__ __forceinline__ void grid_add(const GridAcc& g, double scale, int x, int y, int z, double v) {
@@ -219,6 +236,7 @@ struct FusedUpd {
     double* x = nullptr;
     unsigned long long* bad = nullptr;   // packed first non-positive t (record_bad)
     const int* iter_dev = nullptr;       // graph replay: iteration number on the device
+    unsigned* xmax = nullptr;            // deterministic spread: bound slot of x (note_absmax)
     int iter = 0;
     int rank = 0;
 };
@@ -226,7 +244,9 @@ struct FusedUpd {
 __device__ __forceinline__ void emit_t(double* __restrict__ t_out, const FusedUpd& fu, long long idx, double t) {
     if (fu.x) {
         if (!(t > 1e-300) || !isfinite(t)) record_bad(fu.bad, fu.iter_dev ? *fu.iter_dev : fu.iter, fu.rank, idx);
-        fu.x[idx] = fu.p[idx] / t;
+        const double x = fu.p[idx] / t;
+        fu.x[idx] = x;
+        if (fu.xmax) note_absmax(fu.xmax, absmax_hi(x));
     } else {
         t_out[idx] = t;
     }
@@ -247,7 +267,10 @@ int launch_taps(Plan& P, int side, cudaStream_t s);
 int launch_interp(Plan& P, int side, const double* grid, double* t_sorted, cudaStream_t s,
                   const FusedUpd& fu = FusedUpd());   // fu.x only on the DMMA interps (P.dmma)
 int launch_multiply(Plan& P, int kernel, cudaStream_t s);
-int launch_permute_in(const double* src, const int* perm, long long count, double* dst, cudaStream_t s);
+// slot (deterministic spread): cleared, then max |dst| recorded in it (note_absmax)
+int launch_permute_in(const double* src, const int* perm, long long count, double* dst, cudaStream_t s,
+                      unsigned* slot = nullptr);
+unsigned* wslot(Plan& P, int k);   // Plan::det_wmax + k, nullptr in atomic mode
 int launch_permute_out(const double* src, const int* perm, long long count, double* dst, cudaStream_t s);
 int launch_sample_kernel(Plan& P, int kernel, int M, const double* kb_coef, int kb_deg,
                          double* out, cudaStream_t s);
@@ -263,7 +286,8 @@ constexpr int kUpdVals = 4;     // update_kernel partials per block (residual, m
 constexpr int kUpdBlocks = 592; // update / reduction grid (4 x 148 SMs)
 // a3: grid box <-> packed buffer (dir 0: pack grid -> buf, 1: unpack buf -> grid)
 int launch_box_copy(const Plan& P, double* grid, double* buf, int dir, cudaStream_t s);
-int launch_scale_vec(double* p, long long count, const double* scale_dev, cudaStream_t s);
+int launch_scale_vec(double* p, long long count, const double* scale_dev, cudaStream_t s,
+                     unsigned* slot = nullptr);
 int launch_scale_const(double* p, long long count, double c, cudaStream_t s);
 int launch_reduce_sum_log(const double* p, const double* x, long long count, double* out_dev,
                           int op, cudaStream_t s);
