@@ -821,3 +821,50 @@ def test_deterministic_spread_is_bitwise_reproducible(capi, ctx, name):
     r0 = _with_env({"SK_DETERMINISTIC": "0"}, solve)
     tol = 1e-5 if name == "c2" else 1e-8
     assert abs(r0[1] - r1[1]) <= tol * abs(r0[1]) and abs(r0[0] - r1[0]) <= tol * abs(r0[0]), (r0[:2], r1[:2])
+
+
+def test_deterministic_spread_properties(capi, ctx):
+    """Deterministic spread, stage level: nfft_spread twice gives bit-identical
+    grids for every kernel family (d = 1 per-tap, d = 2 DMMA, d = 3 dense / sparse / x-pair TMA
+    spreads), equal to the FP64-atomic spread to rounding; weights spanning 1e-30 .. 1e30 keep
+    their relative accuracy where they dominate (the scale follows max |w|), all-zero weights
+    give an all-zero grid, and a NaN weight gives a non-finite grid instead of a silent number."""
+    rng = np.random.default_rng(5)
+    for d, N, m_w, cnt in ((1, 64, 8, 500), (2, 32, 8, 3000), (3, 16, 6, 4000)):
+        x, y = rng.random((cnt, d)), rng.random((cnt + 5, d))
+        mk = lambda: capi.Plan(ctx, dev(x), dev(y), 20.0, N, 2.0, m_w)  # noqa: E731
+        Pd = _with_env({"SK_DETERMINISTIC": "1"}, mk)
+        Pa = _with_env({"SK_DETERMINISTIC": "0"}, mk)
+        for w in (rng.random(cnt), rng.random(cnt) * 10.0 ** rng.uniform(-30, 30, cnt)):
+            g1 = capi.nfft_spread(Pd, 0, dev(w)).cpu().numpy()
+            g2 = capi.nfft_spread(Pd, 0, dev(w)).cpu().numpy()
+            ga = capi.nfft_spread(Pa, 0, dev(w)).cpu().numpy()
+            assert np.array_equal(g1, g2), d
+            assert np.abs(g1 - ga).max() <= 1e-14 * np.abs(ga).max(), (d, np.abs(g1 - ga).max() / np.abs(ga).max())
+        assert not np.any(capi.nfft_spread(Pd, 0, dev(np.zeros(cnt))).cpu().numpy())
+        wn = rng.random(cnt)
+        wn[cnt // 2] = np.nan
+        assert not np.all(np.isfinite(capi.nfft_spread(Pd, 0, dev(wn)).cpu().numpy()))
+        Pd.close()
+        Pa.close()
+
+
+def test_deterministic_emulated_two_ranks_reproducible(capi):
+    """The multi-rank code path (SK_EMULATE_WORLD=2: box exchange, scalar all-reduces, graph
+    capture) with the deterministic spread: two solves bit-identical."""
+    cfg = get("c3").with_(n=20000, m=15000)
+    x, y, a, b = make_inputs(cfg)
+    a, b = a / a.sum() / 2, b / b.sum() / 2
+    os.environ["SK_EMULATE_WORLD"] = "2"
+    try:
+        c2 = capi.Context(0)
+    finally:
+        del os.environ["SK_EMULATE_WORLD"]
+    out = []
+    for _ in range(2):
+        P = capi.Plan(c2, dev(x), dev(y), cfg.lam, cfg.N, cfg.sigma, cfg.m_w, cfg.eps_B, cfg.p)
+        u, v, _ = capi.sinkhorn_run(P, dev(a), dev(b), 12)
+        out.append((capi.sinkhorn_divergence(P, dev(a), dev(b), u, v), u.cpu().numpy(), v.cpu().numpy()))
+        P.close()
+    assert out[0][0] == out[1][0] and np.array_equal(out[0][1], out[1][1]) and np.array_equal(out[0][2], out[1][2])
+    c2.close()
