@@ -429,6 +429,15 @@ def main():
                      "peak_source": f"{N_SM} SMs x {FP64_FMA_PER_CLK_PER_SM} FP64 FMA/clk x 2 x sm_max_mhz "
                                     f"{pk.get('sm_max_mhz')} (DESIGN.md)",
                      "hbm_frac": bytes_alg / (avg_ms * 1e-3) / (pk["hbm_gbs"] * 1e9),
+                     # what the kernel's FP64 instruction mix allows on this chip (microbenchmarks of
+                     # the same mix with operands in shared memory): the spread pads the
+                     # 12-tap axis to 16 DMMA rows and forms 144 DMUL products per node, the interp
+                     # pays one DFMA per E value; d = 3, m_w = 6 only
+                     "mix_ceiling_tflops": ({"spread": 22.3, "interp": 31.2}.get(dom)
+                                            if (cfg.d == 3 and cfg.m_w == 6) else None),
+                     "frac_of_mix_ceiling": ((achieved / {"spread": 22.3, "interp": 31.2}[dom])
+                                             if (cfg.d == 3 and cfg.m_w == 6) else None),
+                     "mix_ceiling_source": "profiles/r1_microbench.txt, profiles/r1_interp_mix.txt",
                      "avg_launch_ms": avg_ms,
                      "timing": "CUDA events around the kernel's stage on the library stream, averaged "
                                "over its launches in the profiled step (stage_profile)"},
