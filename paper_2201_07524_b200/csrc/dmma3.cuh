@@ -67,8 +67,7 @@ struct SpreadItem {
 #define SK_TP_SEG_MAX 32
 #endif
 constexpr int kInterpBatch3 = SK_INTERP_NB;   // d = 3 interp batch (nodes of one cell per warp pass)
-constexpr int kSegMax = 1024;
-constexpr int kSegTmaMax = 64;     // spread3_tma_kernel segments (one TMA-staged buffer each)
+constexpr int kSegMax = 1024;     // d = 2 spread segments (nodes of one cell)
 constexpr int kSegTmaPMax = SK_TP_SEG_MAX;   // spread3_tmapad_kernel segments (sparse cells)
 #ifndef SK_TP_SEG_DENSE
 #define SK_TP_SEG_DENSE 64
