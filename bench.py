@@ -242,8 +242,21 @@ def main():
         ctx = capi.Context(local, 0, 1, capi.sk_nccl_unique_id(), stream)
     else:
         ctx = capi.Context(local, stream=stream)
-    solve = lambda: capi.sinkhorn_solve(ctx, dx, dy, da, db, cfg.lam, cfg.N, cfg.sigma, cfg.m_w,  # noqa: E731
-                                        cfg.eps_B, cfg.p, cfg.iters)
+    def solve_r1(x_, y_, a_, b_):
+        """r = 1 workloads (NEXT-2): the same step through the C-ABI calls sinkhorn_solve wraps
+        for r = 2 (fastsum_plan_ex with the Laplace kernel + near field, Alg. 2, divergences)."""
+        P = capi.Plan(ctx, x_, y_, cfg.lam, cfg.N, cfg.sigma, cfg.m_w, cfg.eps_B, cfg.p, r=1,
+                      near_cells=cfg.near_cells)
+        u, v, info = capi.sinkhorn_run(P, a_, b_, cfg.iters)
+        sd, sc = capi.sinkhorn_divergence(P, a_, b_, u, v)
+        P.close()
+        return sd, sc, info
+
+    if cfg.r == 1:
+        solve = lambda: solve_r1(dx, dy, da, db)  # noqa: E731
+    else:
+        solve = lambda: capi.sinkhorn_solve(ctx, dx, dy, da, db, cfg.lam, cfg.N, cfg.sigma, cfg.m_w,  # noqa: E731
+                                            cfg.eps_B, cfg.p, cfg.iters)
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")   # 256 MB > L2
 
     def barrier():
@@ -314,8 +327,12 @@ def main():
     if not args.no_e2e:
         pin = lambda z: torch.from_numpy(z).pin_memory()  # noqa: E731
         px, py, pa, pb = pin(hx), pin(hy), pin(ha), pin(hb)
-        solve_h = lambda: capi.sinkhorn_solve(ctx, px, py, pa, pb, cfg.lam, cfg.N, cfg.sigma, cfg.m_w,  # noqa
-                                              cfg.eps_B, cfg.p, cfg.iters, inputs_on_host=True)
+        if cfg.r == 1:   # host buffers: the copies to the device are part of the step
+            solve_h = lambda: solve_r1(px.cuda(non_blocking=True), py.cuda(non_blocking=True),  # noqa: E731
+                                       pa.cuda(non_blocking=True), pb.cuda(non_blocking=True))
+        else:
+            solve_h = lambda: capi.sinkhorn_solve(ctx, px, py, pa, pb, cfg.lam, cfg.N, cfg.sigma, cfg.m_w,  # noqa
+                                                  cfg.eps_B, cfg.p, cfg.iters, inputs_on_host=True)
         solve_h()
         tot = 0.0
         for _ in range(args.steps):
@@ -338,7 +355,8 @@ def main():
 
     # ---- fast-summation point-evaluations/s: per direction, median over reps of
     # one fast summation each (CUDA events), max over ranks; also NUFFT points/s = (n_s + n_t)/t
-    plan = capi.Plan(ctx, dx, dy, cfg.lam, cfg.N, cfg.sigma, cfg.m_w, cfg.eps_B, cfg.p)
+    plan = capi.Plan(ctx, dx, dy, cfg.lam, cfg.N, cfg.sigma, cfg.m_w, cfg.eps_B, cfg.p, r=cfg.r,
+                     near_cells=cfg.near_cells)
     box_size = plan.info()["box_size"]
     wy = torch.rand(hy.shape[0], dtype=torch.float64, device="cuda")
     wx = torch.rand(hx.shape[0], dtype=torch.float64, device="cuda")
@@ -370,13 +388,28 @@ def main():
     # ---- roofline of the dominant kernel (from the live CUDA-event stage profile)
     pk = peaks()
     stage_ms = {s: (c, ms) for s, (c, ms) in prof.items() if c > 0}
-    dom = max(("spread", "interp"), key=lambda s: stage_ms.get(s, (0, 0.0))[1])
+    dom = max(("spread", "interp", "nearfield"), key=lambda s: stage_ms.get(s, (0, 0.0))[1])
     cnt, ms = stage_ms.get(dom, (1, float("nan")))
     avg_ms = ms / max(cnt, 1)
     W = 2 * cfg.m_w
     # per launch: spread/interp alternate between the x (n) and y (m) node sets -> mean (n+m)/2
     pts_per_launch = (cfg.n + cfg.m) / 2 / world
     flops = 2.0 * W ** cfg.d * pts_per_launch                 # one multiply-add per grid tap
+    near_pairs, near_rad = None, None
+    if cfg.r == 1 and cfg.d == 1 and world == 1:
+        # NEXT-2 near field: exact pairs within the radius a = near_cells / (sigma N) torus units
+        # (a / rho in the caller's units), counted on the host; the same count both directions
+        Pq = capi.Plan(ctx, dx, dy, cfg.lam, cfg.N, cfg.sigma, cfg.m_w, cfg.eps_B, cfg.p, r=1,
+                       near_cells=cfg.near_cells)
+        near_rad = cfg.near_cells / (cfg.N * cfg.sigma) / Pq.info()["rho"]
+        Pq.close()
+        ys = np.sort(hy[:, 0])
+        near_pairs = int((np.searchsorted(ys, hx[:, 0] + near_rad, side="left")
+                          - np.searchsorted(ys, hx[:, 0] - near_rad, side="right")).sum())
+    if dom == "nearfield":
+        # per pair within the radius: |x - y|, r^2, (r/a)^2 (3), K_I Horner (p - 1 FMA), the
+        # factored exp product (1), w (K - K_I) (1 FMA) and the accumulate (1): 2p + 5 flops
+        flops = (2.0 * cfg.p + 5.0) * near_pairs
     sm_mhz = clk.get("sm_mhz") or pk.get("sm_max_mhz", 1965.0)
     fp64_peak = N_SM * FP64_FMA_PER_CLK_PER_SM * 2 * pk.get("sm_max_mhz", 1965.0) * 1e6 / 1e12
     achieved = flops / (avg_ms * 1e-3) / 1e12
@@ -425,7 +458,9 @@ def main():
                      # measured DRAM bytes (ncu) over the live launch time: how close the kernel's real
                      # traffic runs to the HBM roof
                      "traffic_hbm_frac": (traffic / (avg_ms * 1e-3) / (pk["hbm_gbs"] * 1e9)) if traffic else None,
-                     "algorithmic": f"2*(2m_w)^d flops per node per launch, {pts_per_launch:.3g} nodes/launch",
+                     "algorithmic": (f"2p + 5 = {2 * cfg.p + 5} flops per pair within the radius, {near_pairs} pairs/launch"
+                                     if dom == "nearfield" else
+                                     f"2*(2m_w)^d flops per node per launch, {pts_per_launch:.3g} nodes/launch"),
                      "peak_source": f"{N_SM} SMs x {FP64_FMA_PER_CLK_PER_SM} FP64 FMA/clk x 2 x sm_max_mhz "
                                     f"{pk.get('sm_max_mhz')} (DESIGN.md)",
                      "hbm_frac": bytes_alg / (avg_ms * 1e-3) / (pk["hbm_gbs"] * 1e9),
@@ -467,6 +502,15 @@ def main():
         # (no plan, no divergence), from the run's own CUDA events, last timed step, rank 0
         "sinkhorn_run_iterations_per_s": (cfg.iters / results[2].seconds) if results and results[2].seconds > 0 else None,
     }
+    if near_pairs is not None:
+        c_n, ms_n = stage_ms.get("nearfield", (0, 0.0))
+        nf_ms = ms_n / max(c_n, 1)
+        line["nearfield"] = {"radius_caller_units": near_rad, "pairs_per_apply": near_pairs,
+                             "avg_launch_ms": nf_ms,
+                             "pair_evals_per_s": near_pairs / (nf_ms * 1e-3) if ms_n else None,
+                             "flops_per_pair": 2 * cfg.p + 5,
+                             "note": "position-sorted nodes, 32 targets x 8 warps per CTA over the contiguous "
+                                     "source range in the radius, factored exp (DESIGN.md §9b)"}
     if e2e:
         line["e2e"] = e2e
     if rank == 0 and not args.no_cpu_baseline:

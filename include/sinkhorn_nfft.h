@@ -213,8 +213,8 @@ long long sk_launch_count(void);
  * starts recording an event pair around every stage of every fast summation; sk_profile_read
  * writes out[2k] = number of timed launches and out[2k+1] = their total device milliseconds
  * for stage k = 0 spread, 1 grid all-reduce, 2 forward FFT, 3 multiply, 4 inverse FFT,
- * 5 interp, 6 update, 7 plan (sinkhorn_solve's fastsum_plan; nstages <= 8 entries are
- * written); reset != 0 clears the totals. While profiling, sinkhorn_run launches every kernel
+ * 5 interp, 6 update, 7 plan (sinkhorn_solve's fastsum_plan), 8 near field (r = 1;
+ * nstages <= 9 entries are written); reset != 0 clears the totals. While profiling, sinkhorn_run launches every kernel
  * eagerly (no CUDA-graph replay of iterations). */
 void sk_profile(int on);
 int sk_profile_read(double* out, int nstages, int reset);

@@ -121,7 +121,7 @@ def sk_launch_count() -> int:
     return int(_lib.sk_launch_count())
 
 
-STAGES = ("spread", "allreduce", "fft_fwd", "multiply", "fft_inv", "interp", "update", "plan")
+STAGES = ("spread", "allreduce", "fft_fwd", "multiply", "fft_inv", "interp", "update", "plan", "nearfield")
 
 
 def sk_profile(on: bool) -> None:

@@ -126,7 +126,16 @@ struct ScaleParams {
     int cell_minor;   // 1: key = tile * T^d + cell-within-tile index: nodes sorted by cell
     int xminor;       // cell-within-tile digits with x least significant (d = 3 spread x-pairs)
     int Td;           // T^d
+    int fine_shift;   // d = 1 near field: key = floor(u 2^fine_shift) (position order), 0 = off
+    int fine_max;     // largest fine key: tiles_per_axis * T * 2^fine_shift - 1
 };
+
+// position key of a d = 1 node (the sort key and the near-field range search use this one
+// definition, so the binary search below sees exactly the sorted order)
+__device__ __forceinline__ int fine_key(double u, int shift, int kmax) {
+    const double f = floor(ldexp(u, shift));
+    return f < 0.0 ? 0 : (f > (double)kmax ? kmax : (int)f);
+}
 
 // x' = rho (x - centre), u = n (x' + 1/2): the one definition both the key and the gather use
 // (bit-identical u in both kernels)
@@ -160,7 +169,8 @@ __global__ void scale_key_kernel(const double* __restrict__ pts, long long count
             }
         }
         if (!ok || !(r2 <= sp.r2max)) atomicMin(bad, (int)i);
-        key[i] = sp.cell_minor ? k * sp.Td + sub : k;
+        key[i] = sp.fine_shift ? fine_key(grid_u(sp, scaled_x(sp, pts[i], 0)), sp.fine_shift, sp.fine_max)
+                               : (sp.cell_minor ? k * sp.Td + sub : k);
         idx[i] = (int)i;
     }
 }
@@ -179,7 +189,24 @@ static ScaleParams scale_params(const Plan& P) {
     sp.xminor = P.spread_xpairs ? 1 : 0;
     sp.Td = 1;
     for (int a = 0; a < P.d; ++a) sp.Td *= P.tile_cells;
+    sp.fine_shift = P.fine_shift;
+    sp.fine_max = (int)(((long long)P.tiles_per_axis * P.tile_cells << P.fine_shift) - 1);
     return sp;
+}
+
+// fine (position) keys -> tile index, in place, for tile_offsets
+__global__ void fine_to_tile_kernel(int* __restrict__ key, long long count, int shift, int T, int tpa) {
+    for (long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x; k < count;
+         k += (long long)gridDim.x * blockDim.x)
+        key[k] = min(tpa - 1, (key[k] >> shift) / T);
+}
+
+int launch_fine_to_tile(Plan& P, int* key, long long count, cudaStream_t s) {
+    if (count <= 0) return SK_OK;
+    fine_to_tile_kernel<<<grid_for(count, 256), 256, 0, s>>>(key, count, P.fine_shift, P.tile_cells,
+                                                             P.tiles_per_axis);
+    SK_LAUNCH_CHECK();
+    return SK_OK;
 }
 
 int launch_scale_key(Plan& P, const double* pts, long long count, int* key, int* idx, int* bad,
@@ -733,6 +760,128 @@ __global__ void nearfield_kernel(NearParams np, const double* __restrict__ ut, l
     }
 }
 
+// d = 1 near field on position-sorted nodes (Plan::fine_shift), n-body style: a CTA takes 32
+// consecutive targets (one per lane; they span a tiny interval) and the one contiguous source
+// range within the radius of them, found by binary search on the same fine keys the sort used.
+// Sources are staged in shared memory in blocks of kNearBlk; each of the 8 warps sums its 32
+// targets against every 8th source of a block (latency hidden across warps even where the
+// source density is high), and the 8 partial sums are added in warp order at the end (the
+// result does not depend on scheduling).
+// On the line |x - y| = +-(x - y), so exp(-lam' |x - y|) = g_i f_j (x >= y) or 1 / (g_i f_j)
+// with g_i = exp(-lam' (x_i - c)), f_j = exp(lam' (y_j - c)) about the chunk's lowest target c:
+// one exp per staged source and per target instead of one per pair. The exponents stay below
+// lam' x (chunk span + radius), checked against kNearExpMax (else the per-pair exp).
+// Per pair: a difference, a compare, a product and the K_I Horner polynomial.
+constexpr int kNearBlk = 256, kNearWarps = 8, kNearKI = 8;
+constexpr double kNearExpMax = 600.0;
+
+// one warp's share of a staged block: its 32 targets against sources warp, warp + 8, ...
+// (branch-free: out-of-radius pairs are masked). K_I has kNearKI coefficients, zero-padded at
+// the top (exact in Horner: fma(0, t2, c) = c).
+template <int KERNEL, bool SEP>
+__device__ __forceinline__ double near_block(const double2* __restrict__ syw, const double2* __restrict__ sff,
+                                             int cnt, int warp, double xi, double gi, double igi, double a2,
+                                             double inv_a2, double lam_p, double rho_inv, const double* ki,
+                                             double acc) {
+#pragma unroll 4
+    for (int k = warp; k < cnt; k += kNearWarps) {
+        const double2 yw = syw[k];
+        const double dx = xi - yw.x;   // torus units
+        const double r2 = dx * dx;
+        const double r = fabs(dx);
+        double wk;   // w_j K(r)
+        if (SEP) {
+            const double2 ff = sff[k];
+            wk = dx >= 0.0 ? gi * ff.x : igi * ff.y;
+        } else {
+            wk = yw.y * exp(-lam_p * r);
+        }
+        if (KERNEL == 1) wk *= r * rho_inv;
+        const double t2 = r2 * inv_a2;
+        double q = ki[kNearKI - 1];
+#pragma unroll
+        for (int c = kNearKI - 2; c >= 0; --c) q = fma(q, t2, ki[c]);
+        const double v = fma(-yw.y, q, wk);
+        acc += r2 < a2 ? v : 0.0;
+    }
+    return acc;
+}
+
+template <int KERNEL>
+__global__ void __launch_bounds__(kNearWarps * 32, 2) nearfield_d1_kernel(
+    NearParams np, const double* __restrict__ ut, long long nt, const double* __restrict__ us, long long ns,
+    int shift, int kmax, const double* __restrict__ w, double* __restrict__ t) {
+    __shared__ double2 syw[kNearBlk], sff[kNearBlk];   // (y_j, w_j), (w_j f_j, w_j / f_j)
+    __shared__ double part[kNearWarps][32];
+    __shared__ long long range[2];
+    __shared__ double chunk_lo;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const long long i0 = (long long)blockIdx.x * 32, i = i0 + lane;
+    const bool active = i < nt;
+    const double ag = np.a * (double)np.n;   // radius in grid units
+    if (warp == 0) {
+        const double ui = active ? ut[i] : ut[i0];
+        double lo = ui, hi = ui;
+        for (int o = 16; o; o >>= 1) {
+            lo = fmin(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+            hi = fmax(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+        }
+        if (lane < 2) {
+            // lane 0: first source with key >= key(lo - a); lane 1: first with key > key(hi + a)
+            const int kb = lane == 0 ? fine_key(lo - ag, shift, kmax) : fine_key(hi + ag, shift, kmax);
+            long long L = 0, R = ns;
+            while (L < R) {
+                const long long M = (L + R) >> 1;
+                const int km = fine_key(us[M], shift, kmax);
+                if (lane == 0 ? km < kb : km <= kb) L = M + 1; else R = M;
+            }
+            range[lane] = L;
+        }
+        if (lane == 0) chunk_lo = lo;
+    }
+    __syncthreads();
+    const long long j0 = range[0], j1 = range[1];
+    const double c = chunk_lo;
+    const double lam_n = np.lam_p * np.inv_n;   // lam' per grid unit
+    // every exponent lam' |u - c| of this CTA below kNearExpMax (sources sorted: the ends bound it)
+    const bool sep = j1 > j0 && lam_n * fmax(fabs(us[j1 - 1] - c), fabs(us[j0] - c)) < kNearExpMax &&
+                     lam_n * (active ? ut[i] - c : 0.0) < kNearExpMax;
+    const bool sep_all = __syncthreads_and(sep);
+    const double ui = active ? ut[i] : c;
+    const double xi = ui * np.inv_n;
+    const double gi = sep_all ? exp(-lam_n * (ui - c)) : 1.0, igi = 1.0 / gi;
+    const double a2 = np.a * np.a, inv_a2 = 1.0 / a2;
+    double ki[kNearKI];
+#pragma unroll
+    for (int q = 0; q < kNearKI; ++q) ki[q] = q < np.ki_n ? np.ki[q] : 0.0;
+    double acc = 0.0;
+    for (long long jb = j0; jb < j1; jb += kNearBlk) {
+        const int cnt = (int)min((long long)kNearBlk, j1 - jb);
+        __syncthreads();
+        for (int k = threadIdx.x; k < cnt; k += blockDim.x) {
+            const double uj = us[jb + k], wj = w[jb + k];
+            syw[k] = make_double2(uj * np.inv_n, wj);
+            if (sep_all) {
+                const double f = exp(lam_n * (uj - c));
+                sff[k] = make_double2(wj * f, wj / f);
+            }
+        }
+        __syncthreads();
+        if (!active) continue;
+        acc = sep_all ? near_block<KERNEL, true>(syw, sff, cnt, warp, xi, gi, igi, a2, inv_a2, np.lam_p,
+                                                 np.rho_inv, ki, acc)
+                      : near_block<KERNEL, false>(syw, sff, cnt, warp, xi, gi, igi, a2, inv_a2, np.lam_p,
+                                                  np.rho_inv, ki, acc);
+    }
+    part[warp][lane] = acc;
+    __syncthreads();
+    if (warp == 0 && active) {
+        double sum = part[0][lane];
+        for (int q = 1; q < kNearWarps; ++q) sum += part[q][lane];
+        t[i] += sum;
+    }
+}
+
 int launch_nearfield(Plan& P, int src, int dst, int kernel, const double* w_sorted, double* t_sorted,
                      cudaStream_t s) {
     const NodeSet& S = P.side[src];
@@ -751,8 +900,17 @@ int launch_nearfield(Plan& P, int src, int dst, int kernel, const double* w_sort
     np.rho_inv = 1.0 / P.rho;
     np.inv_n = 1.0 / P.n;
     for (int i = 0; i < 16; ++i) np.ki[i] = P.ki[kernel][i];
-    nearfield_kernel<<<grid_for(D.count, 128), 128, 0, s>>>(np, D.u, D.count, S.u, S.count, S.tile_start,
-                                                            w_sorted, t_sorted);
+    if (P.d == 1 && P.fine_shift) {
+        const long long blocks = (D.count + 31) / 32;
+        const int kmax = (int)(((long long)P.tiles_per_axis * P.tile_cells << P.fine_shift) - 1);
+        if (P.ki_n > kNearKI) return set_error(SK_EINVAL, "near field: more than 8 K_I coefficients");
+        const auto kern = kernel == 0 ? nearfield_d1_kernel<0> : nearfield_d1_kernel<1>;
+        kern<<<(unsigned)blocks, kNearWarps * 32, 0, s>>>(np, D.u, D.count, S.u, S.count, P.fine_shift, kmax,
+                                                          w_sorted, t_sorted);
+    } else {
+        nearfield_kernel<<<grid_for(D.count, 128), 128, 0, s>>>(np, D.u, D.count, S.u, S.count, S.tile_start,
+                                                                w_sorted, t_sorted);
+    }
     SK_LAUNCH_CHECK();
     return SK_OK;
 }

@@ -522,7 +522,8 @@ static int plan_side(Plan& P, int sidx, const double* pts, long long count, cuda
     }
     long long Td = 1;
     for (int a = 0; a < P.d; ++a) Td *= P.tile_cells;
-    const long long nkeys = P.dmma ? (long long)S.ntiles * Td : S.ntiles;
+    const long long nkeys = P.fine_shift ? ((long long)S.ntiles * P.tile_cells << P.fine_shift)
+                                         : (P.dmma ? (long long)S.ntiles * Td : S.ntiles);
     int end_bit = 1;
     while ((1LL << end_bit) < nkeys) ++end_bit;
     size_t tmp_bytes = 0;
@@ -543,6 +544,7 @@ static int plan_side(Plan& P, int sidx, const double* pts, long long count, cuda
         SK_TRY(launch_taps(P, sidx, s));
         plan_trace("side: taps", s);
     } else {
+        if (P.fine_shift) SK_TRY(launch_fine_to_tile(P, S.cell_key, count, s));
         SK_TRY(launch_tile_offsets(S.cell_key, count, S.ntiles, S.tile_start, s));
         SK_CUDA(cudaStreamSynchronize(s));
         if (P.tiled) SK_TRY(build_items(P, S, s));
@@ -673,6 +675,12 @@ int build_plan(Ctx* ctx, Plan** out, int d, const double* x, long long n, const 
     }
     P->tile_cells = P->dmma ? (d == 3 ? 2 : kSup2) : choose_tile(d, ng, P->tiled);
     P->tiles_per_axis = ng / P->tile_cells;
+    if (d == 1 && rpow == 1 && !P->dmma && getenv("SK_NEARFIELD_V1") == nullptr) {
+        // position sort for the d = 1 near field: fine keys below 2^30
+        int shift = 0;
+        while (((long long)ng << (shift + 1)) <= (1LL << 30)) ++shift;
+        P->fine_shift = shift;
+    }
 
     auto fail = [&](int code) { destroy_plan(P); return code; };
 
@@ -874,21 +882,29 @@ int apply_sorted(Plan& P, int transpose, int kernel, const double* w_sorted, dou
         count_launch();
         prof_end(ST_FFT_INV, s);
     }
+    auto nearfield = [&]() -> int {   // r = 1: the near-field correction, its own profiled stage
+        prof_begin(ST_NEARFIELD, s);
+        SK_TRY(launch_nearfield(P, src, dst, kernel, w_sorted, t_sorted, s));
+        prof_end(ST_NEARFIELD, s);
+        return SK_OK;
+    };
     prof_begin(ST_INTERP, s);
     if (fu && fu->x) {
         // the caller wants x = p / t: fused into the DMMA (or d = 1) interpolation when it can be
         if ((P.dmma || P.d == 1) && P.rpow == 2) {
             SK_TRY(launch_interp(P, dst, P.grid, t_sorted, s, *fu));
+            prof_end(ST_INTERP, s);
         } else {
             SK_TRY(launch_interp(P, dst, P.grid, t_sorted, s));
-            if (P.rpow == 1) SK_TRY(launch_nearfield(P, src, dst, kernel, w_sorted, t_sorted, s));
+            prof_end(ST_INTERP, s);
+            if (P.rpow == 1) SK_TRY(nearfield());
             SK_TRY(launch_update(P, dst, t_sorted, fu->p, fu->x, 0, fu->iter, fu->iter_dev, s));
         }
     } else {
         SK_TRY(launch_interp(P, dst, P.grid, t_sorted, s));
-        if (P.rpow == 1) SK_TRY(launch_nearfield(P, src, dst, kernel, w_sorted, t_sorted, s));
+        prof_end(ST_INTERP, s);
+        if (P.rpow == 1) SK_TRY(nearfield());
     }
-    prof_end(ST_INTERP, s);
     return SK_OK;
 }
 

@@ -97,6 +97,9 @@ struct Plan {
     int near_cells = 0;
     double near_a = 0.0;
     double ki[2][16] = {};    // K_I coefficients in (r / near_a)^2, kernels 0 and 1
+    // d = 1 with a near field: nodes sorted by position (key = floor(u 2^fine_shift)), not only by
+    // tile, so a chunk of consecutive targets has one contiguous source range (0 = tile sort)
+    int fine_shift = 0;
     int ki_n = 0;
     int p_smooth = 8;
     double centre[kMaxD] = {0, 0, 0};
@@ -298,6 +301,7 @@ int launch_finalize_partials(const double* red, int nparts, int nvals, double* o
 int build_plan(Ctx* ctx, Plan** out, int d, const double* x, long long n, const double* y,
                long long m, double lambda, int N, double sigma, int m_w, double eps_B, int p,
                int rpow, int near_cells);
+int launch_fine_to_tile(Plan& P, int* key, long long count, cudaStream_t s);
 int launch_nearfield(Plan& P, int src, int dst, int kernel, const double* w_sorted, double* t_sorted,
                      cudaStream_t s);
 int destroy_plan(Plan* P);
@@ -313,7 +317,7 @@ int apply_sorted(Plan& P, int transpose, int kernel, const double* w_sorted, dou
                  const FusedUpd* fu = nullptr);   // fu: update fused into a7 where supported
 
 // ---- stage profiling (api.cu): CUDA-event pairs around each stage when enabled ----
-enum Stage { ST_SPREAD = 0, ST_ALLREDUCE, ST_FFT_FWD, ST_MULTIPLY, ST_FFT_INV, ST_INTERP, ST_UPDATE, ST_PLAN, ST_COUNT };
+enum Stage { ST_SPREAD = 0, ST_ALLREDUCE, ST_FFT_FWD, ST_MULTIPLY, ST_FFT_INV, ST_INTERP, ST_UPDATE, ST_PLAN, ST_NEARFIELD, ST_COUNT };
 // host wall-clock trace of the plan phases (SK_PLAN_TRACE=1), printed to stderr
 void plan_trace(const char* phase, cudaStream_t s);
 void prof_begin(int stage, cudaStream_t s);

@@ -32,6 +32,8 @@ class Config:
     grid_y: int = 0
     sub_n: int = 0    # divergence-parity subsample sizes (0 = full size)
     sub_m: int = 0
+    r: int = 2            # cost |x - y|^r (NEXT-2: r = 1, Laplace kernel + near field)
+    near_cells: int = 0   # r = 1: near-field radius in oversampled-grid cells
 
     def with_(self, **kw) -> "Config":
         return replace(self, **kw)
@@ -70,8 +72,14 @@ for _K in (32, 64, 128, 256, 512):
     CONFIGS[f"img{_K}"] = Config(f"img{_K}", 2, _K * _K, _K * _K, 20.0, 64, 2.0, 8, 1 / 16, 8, 100,
                                  "pixel_grid", "pixel_grid", "bumps", grid_x=_K, grid_y=_K)
 
+# r = 1 on the paper's d = 1 experiment shape (Table 1, "the results for
+# r = 1 are similar"): x ~ U[0,1], y ~ N(0.5, 0.1^2) clipped (the c1 recipe), uniform weights,
+# lambda = 20, N = 256, m_w = 8, 16 near-field cells (DESIGN.md §9b readings R1-R6), 50 iterations.
+CONFIGS["c1r1"] = Config("c1r1", 1, 100_000, 100_000, 20.0, 256, 2.0, 8, 1 / 16, 8, 50,
+                         "uniform", "normal_clip", "uniform", r=1, near_cells=16)
+
 CONFIG_INDEX = {"c1": 1, "c2": 2, "c3": 3, "c4": 4, "c5": 5,
-                "img32": 6, "img64": 7, "img128": 8, "img256": 9, "img512": 10}
+                "img32": 6, "img64": 7, "img128": 8, "img256": 9, "img512": 10, "c1r1": 11}
 
 
 def get(name: str) -> Config:

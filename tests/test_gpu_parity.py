@@ -761,6 +761,26 @@ def test_random_configs_match_method_statement(capi, ctx, d, seed):
             (d, n, m, N, m_w, kernel, rel_linf(t, ref), rel_linf(tt, reft))
 
 
+@pytest.mark.parametrize("lam,kernel", [(20.0, 0), (20.0, 1), (3000.0, 0), (3000.0, 1)])
+def test_r1_d1_nearfield_tiles(capi, ctx, lam, kernel):
+    """d = 1 near field at a size spanning many 128-target CTAs, several 256-source blocks per CTA
+    (clustered targets: ~400 sources within the radius) and a ragged tail: GPU = the oracle's
+    statement of the method. lam = 20 takes the factored exp(-lam'|x - y|) = g_i f_j path,
+    lam = 3000 (lam' x span > 600) the per-pair exp."""
+    from oracle import laplace_ref as LR
+    rng = np.random.default_rng(77)
+    n, m = 8000 + 37, 8000 + 13
+    x = np.clip(rng.normal(0.5, 0.05, (n, 1)), 0.0, 1.0)
+    y = rng.random((m, 1))
+    wy, wx = rng.random(m), rng.random(n)
+    P = capi.Plan(ctx, dev(x), dev(y), lam, 256, 2.0, 8, 1 / 16, 8, r=1, near_cells=16)
+    t = capi.fastsum_apply(P, dev(wy), 0, kernel).cpu().numpy()
+    tt = capi.fastsum_apply(P, dev(wx), 1, kernel).cpu().numpy()
+    ref = LR.fastsum_ndft(x, y, wy, lam, 256, 1 / 16, 8, 16, kernel=kernel)
+    reft = LR.fastsum_ndft(y, x, wx, lam, 256, 1 / 16, 8, 16, kernel=kernel)
+    assert rel_linf(t, ref) <= 1e-12 and rel_linf(tt, reft) <= 1e-12, (rel_linf(t, ref), rel_linf(tt, reft))
+
+
 @pytest.mark.parametrize("d,seed", [(1, 0), (1, 1), (2, 0), (2, 1), (3, 0)])
 def test_random_r1_configs_match_method_statement(capi, ctx, d, seed):
     """r = 1 plans with seeded random sizes, lambda, N and near-field radius: GPU = the oracle's
