@@ -197,6 +197,14 @@ __device__ __forceinline__ double grid_scale(const GridAcc& g) {
     const double c = __longlong_as_double((long long)(((unsigned long long)hi << 32) | 0xffffffffULL)) * g.phi0d;
     return (hi != 0 && isfinite(c)) ? ldexp(1.0, 61 - ilogb(c)) : 1.0;
 }
+// v 2^S as the two words (hi, lo) of the fixed-point accumulator: X = hi 2^32 + lo
+__device__ __forceinline__ void fixed_words(double v, double scale, unsigned long long& hi, unsigned long long& lo) {
+    const double X = v * scale;                              // exact (power of 2)
+    const double h = floor(X * 2.3283064365386963e-10);      // X / 2^32, exact
+    const double l = rint(X - h * 4294967296.0);             // low part in [0, 2^32], exact before rint
+    hi = (unsigned long long)(long long)h;
+    lo = (unsigned long long)l;
+}
 template <int D>
 __device__ __forceinline__ void grid_add(const GridAcc& g, double scale, int x, int y, int z, double v) {
     if (!g.acc) {
@@ -209,11 +217,10 @@ __device__ __forceinline__ void grid_add(const GridAcc& g, double scale, int x, 
     long long i = x - g.lo[0];
     if (D >= 2) i = i * g.bn[1] + (y - g.lo[1]);
     if (D >= 3) i = i * g.bn[2] + (z - g.lo[2]);
-    const double X = v * scale;                              // exact (power of 2)
-    const double h = floor(X * 2.3283064365386963e-10);      // X / 2^32, exact
-    const double l = rint(X - h * 4294967296.0);             // low part in [0, 2^32], exact before rint
-    atomicAdd(&g.acc[2 * i], (unsigned long long)(long long)h);
-    atomicAdd(&g.acc[2 * i + 1], (unsigned long long)l);
+    unsigned long long h, l;
+    fixed_words(v, scale, h, l);
+    atomicAdd(&g.acc[2 * i], h);
+    atomicAdd(&g.acc[2 * i + 1], l);
 }
 #endif
 

@@ -105,6 +105,69 @@ __global__ void spread_d1_kernel(const double* __restrict__ u, long long count, 
     }
 }
 
+// d = 1 spread privatised per CTA: 256 consecutive sorted nodes (position- or tile-sorted, so
+// they cover a short interval) accumulate their 2m taps into a shared-memory window of the grid,
+// then the window's nonzero cells are added to the grid once. Deterministic mode keeps the
+// fixed-point words in shared memory (integer adds: the totals do not depend on order); a CTA
+// whose window exceeds kD1Win cells adds straight to the grid.
+constexpr int kD1Nodes = 256, kD1Win = 1024;
+__global__ void __launch_bounds__(kD1Nodes) spread_d1_win_kernel(const double* __restrict__ u, long long count,
+                                                                 const double* __restrict__ w, Window win,
+                                                                 const GridAcc ga, int chunk) {
+    __shared__ unsigned long long sacc[2 * kD1Win];   // (hi, lo) per cell, or the FP64 sum in word 0
+    __shared__ int wlo_s, whi_s;
+    const int W = 2 * win.m;
+    const long long j0 = (long long)blockIdx.x * chunk;
+    const int cnt = (int)min((long long)chunk, count - j0);
+    const double gscale = grid_scale(ga);
+    // window [min floor(u) - m + 1, max floor(u) + m] over the chunk
+    int c = INT_MAX, cmax = INT_MIN;
+    if ((int)threadIdx.x < cnt) { c = (int)floor(u[j0 + threadIdx.x]); cmax = c; }
+    const int lo = __reduce_min_sync(0xffffffffu, c), hi = __reduce_max_sync(0xffffffffu, cmax);
+    if (threadIdx.x == 0) { wlo_s = INT_MAX; whi_s = INT_MIN; }
+    __syncthreads();
+    if ((threadIdx.x & 31) == 0) { atomicMin(&wlo_s, lo); atomicMax(&whi_s, hi); }
+    __syncthreads();
+    const int wlo = wlo_s - win.m + 1, wn = whi_s + win.m - wlo + 1;
+    const bool priv = wn <= kD1Win;
+    if (priv) {
+        for (int k = threadIdx.x; k < 2 * wn; k += blockDim.x) sacc[k] = 0ULL;
+        __syncthreads();
+    }
+    double* sdbl = reinterpret_cast<double*>(sacc);
+    for (int p = threadIdx.x; p < cnt * W; p += blockDim.x) {
+        const int jj = p / W, t = p - jj * W;
+        const double uj = u[j0 + jj], cj = floor(uj);
+        const double v = w[j0 + jj] * kb_phi(uj - cj + (double)(win.m - 1 - t), win);
+        const int x = (int)cj - win.m + 1 + t;
+        if (!priv) {
+            grid_add<1>(ga, gscale, x, 0, 0, v);
+        } else if (ga.acc) {
+            unsigned long long h, l;
+            fixed_words(v, gscale, h, l);
+            atomicAdd(&sacc[2 * (x - wlo)], h);
+            atomicAdd(&sacc[2 * (x - wlo) + 1], l);
+        } else {
+            atomicAdd(&sdbl[2 * (x - wlo)], v);
+        }
+    }
+    if (!priv) return;
+    __syncthreads();
+    for (int k = threadIdx.x; k < wn; k += blockDim.x) {
+        const int x = wlo + k;
+        if (ga.acc) {
+            const unsigned long long h = sacc[2 * k], l = sacc[2 * k + 1];
+            if (h | l) {
+                const long long i = x - ga.lo[0];
+                atomicAdd(&ga.acc[2 * i], h);
+                atomicAdd(&ga.acc[2 * i + 1], l);
+            }
+        } else if (sdbl[2 * k] != 0.0) {
+            atomicAdd(&ga.grid[x], sdbl[2 * k]);
+        }
+    }
+}
+
 __global__ void interp_d1_kernel(const double* __restrict__ u, long long count, Window win,
                                  const double* __restrict__ grid, double* __restrict__ t_out, const FusedUpd fu) {
     const int W = 2 * win.m, lane = threadIdx.x & 31;
@@ -229,7 +292,16 @@ inline int spread_dispatch(Plan& P, const NodeSet& S, const double* w, const Gri
         return SK_OK;
     }
     if (P.d == 1) {
-        spread_d1_kernel<<<v1_grid(S.count * 2 * P.win.m), 128, 0, s>>>(S.u, S.count, w, P.win, ga);
+        static const bool d1_flat = getenv("SK_SPREAD_D1_FLAT") != nullptr;
+        if (d1_flat || P.win.m * 2 > kD1Win / 4)
+            spread_d1_kernel<<<v1_grid(S.count * 2 * P.win.m), 128, 0, s>>>(S.u, S.count, w, P.win, ga);
+        else
+        {
+            // nodes per CTA: at least ~2 CTAs per SM for small sets, at most kD1Nodes
+            const long long chunk = std::max(16LL, std::min((long long)kD1Nodes, S.count / (2 * 148)));
+            spread_d1_win_kernel<<<(unsigned)((S.count + chunk - 1) / chunk), kD1Nodes, 0, s>>>(
+                S.u, S.count, w, P.win, ga, (int)chunk);
+        }
         count_launch();
         cudaError_t e = cudaGetLastError();
         if (e != cudaSuccess) return set_error(SK_ECUDA, std::string("spread_d1: ") + cudaGetErrorString(e));
