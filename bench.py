@@ -150,7 +150,7 @@ def cpu_oracle_rate(cfg, budget_s: float):
     # calibrate: one iteration on a small subsample, then size the sample to the budget
     k = min(2000, x.shape[0], y.shape[0])
     t0 = time.perf_counter()
-    dense.sinkhorn_log(x[:k], y[:k], a[:k] / a[:k].sum(), b[:k] / b[:k].sum(), cfg.lam, 1)
+    dense.sinkhorn_log(x[:k], y[:k], a[:k] / a[:k].sum(), b[:k] / b[:k].sum(), cfg.lam, 1, r=cfg.r)
     per_pair = (time.perf_counter() - t0) / (k * k)
     iters = 5
     ks = int(min(x.shape[0], y.shape[0], (budget_s / (iters * per_pair)) ** 0.5))
@@ -158,14 +158,14 @@ def cpu_oracle_rate(cfg, budget_s: float):
     xs, ys = x[:ks], y[:ks]
     as_, bs = a[:ks] / a[:ks].sum(), b[:ks] / b[:ks].sum()
     t0 = time.perf_counter()
-    dense.sinkhorn_log(xs, ys, as_, bs, cfg.lam, iters)
+    dense.sinkhorn_log(xs, ys, as_, bs, cfg.lam, iters, r=cfg.r)
     dt = time.perf_counter() - t0
     rate_sample = iters / dt
     rate_full = rate_sample * (ks * ks) / (cfg.n * cfg.m)
     # oracle direct-sum throughput (pair evaluations/s of the matvec checks)
     kr = min(512, xs.shape[0])
     t0 = time.perf_counter()
-    dense.direct_sum(xs[:kr], ys, bs, cfg.lam, 0)
+    dense.direct_sum(xs[:kr], ys, bs, cfg.lam, 0, r=cfg.r)
     global ORACLE_PAIRS_PER_S
     ORACLE_PAIRS_PER_S = kr * ys.shape[0] / (time.perf_counter() - t0)
     desc = (f"{iters} log-domain Alg. 1 iterations on the first {ks}+{ks} points of {cfg.name} "

@@ -775,110 +775,129 @@ __global__ void nearfield_kernel(NearParams np, const double* __restrict__ ut, l
 constexpr int kNearBlk = 256, kNearWarps = 8, kNearKI = 8;
 constexpr double kNearExpMax = 600.0;
 
-// one warp's share of a staged block: its 32 targets against sources warp, warp + 8, ...
-// (branch-free: out-of-radius pairs are masked). K_I has kNearKI coefficients, zero-padded at
-// the top (exact in Horner: fma(0, t2, c) = c).
+// one warp's share of a staged block: its 32 x kNearTPL targets against sources warp,
+// warp + 8, ... (each staged source read once per kNearTPL pairs: shared-memory loads were the
+// co-bottleneck with one target per lane). Coordinates are in units of the radius a, so
+// t2 = dx^2 = (r / a)^2 feeds the K_I Horner directly; the radius test (t2 < 1) and the side
+// test (dx >= 0) read the high words as integers, off the FP64 pipe (t2 >= 0: hi < 0x3ff00000
+// <=> t2 < 1). Out-of-radius pairs are masked, not branched. K_I has kNearKI coefficients,
+// zero-padded at the top (exact in Horner: fma(0, t2, c) = c). Per pair: 12 FP64 instructions
+// (14 for the c K kernel).
+constexpr int kNearTPL = 2;
+#ifndef SK_NEAR_MINB
+#define SK_NEAR_MINB 2
+#endif
 template <int KERNEL, bool SEP>
-__device__ __forceinline__ double near_block(const double2* __restrict__ syw, const double2* __restrict__ sff,
-                                             int cnt, int warp, double xi, double gi, double igi, double a2,
-                                             double inv_a2, double lam_p, double rho_inv, const double* ki,
-                                             double acc) {
-#pragma unroll 4
+__device__ __forceinline__ void near_block(const double2* __restrict__ syw, const double2* __restrict__ sff,
+                                           int cnt, int warp, const double* xi, const double* gi,
+                                           const double* igi, double lam_a, double r_scale, const double* ki,
+                                           double* acc) {
+#pragma unroll 2
     for (int k = warp; k < cnt; k += kNearWarps) {
         const double2 yw = syw[k];
-        const double dx = xi - yw.x;   // torus units
-        const double r2 = dx * dx;
-        const double r = fabs(dx);
-        double wk;   // w_j K(r)
-        if (SEP) {
-            const double2 ff = sff[k];
-            wk = dx >= 0.0 ? gi * ff.x : igi * ff.y;
-        } else {
-            wk = yw.y * exp(-lam_p * r);
-        }
-        if (KERNEL == 1) wk *= r * rho_inv;
-        const double t2 = r2 * inv_a2;
-        double q = ki[kNearKI - 1];
+        double2 ff;
+        if (SEP) ff = sff[k];
 #pragma unroll
-        for (int c = kNearKI - 2; c >= 0; --c) q = fma(q, t2, ki[c]);
-        const double v = fma(-yw.y, q, wk);
-        acc += r2 < a2 ? v : 0.0;
+        for (int e = 0; e < kNearTPL; ++e) {
+            const double dx = xi[e] - yw.x;   // (x - y) / a
+            const double t2 = dx * dx;
+            const int dxh = __double2hiint(dx), t2h = __double2hiint(t2);
+            double wk;   // w_j K(r)
+            if (SEP) {
+                const bool right = dxh >= 0;   // select the factors, then one product
+                wk = (right ? gi[e] : igi[e]) * (right ? ff.x : ff.y);
+            } else {
+                wk = yw.y * exp(-lam_a * fabs(dx));
+            }
+            if (KERNEL == 1) wk *= fabs(dx) * r_scale;
+            double q = ki[kNearKI - 1];
+#pragma unroll
+            for (int c = kNearKI - 2; c >= 0; --c) q = fma(q, t2, ki[c]);
+            const double v = fma(-yw.y, q, wk);
+            acc[e] += t2h < 0x3ff00000 ? v : 0.0;
+        }
     }
-    return acc;
 }
 
 template <int KERNEL>
-__global__ void __launch_bounds__(kNearWarps * 32, 2) nearfield_d1_kernel(
+__global__ void __launch_bounds__(kNearWarps * 32, SK_NEAR_MINB) nearfield_d1_kernel(
     NearParams np, const double* __restrict__ ut, long long nt, const double* __restrict__ us, long long ns,
     int shift, int kmax, const double* __restrict__ w, double* __restrict__ t) {
+    constexpr int CH = 32 * kNearTPL;   // targets per CTA
     __shared__ double2 syw[kNearBlk], sff[kNearBlk];   // (y_j, w_j), (w_j f_j, w_j / f_j)
-    __shared__ double part[kNearWarps][32];
+    __shared__ double part[kNearWarps][CH];
     __shared__ long long range[2];
     __shared__ double chunk_lo;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const long long i0 = (long long)blockIdx.x * 32, i = i0 + lane;
-    const bool active = i < nt;
+    const long long i0 = (long long)blockIdx.x * CH;
+    const long long ilast = min(nt, i0 + CH) - 1;
     const double ag = np.a * (double)np.n;   // radius in grid units
-    if (warp == 0) {
-        const double ui = active ? ut[i] : ut[i0];
-        double lo = ui, hi = ui;
-        for (int o = 16; o; o >>= 1) {
-            lo = fmin(lo, __shfl_xor_sync(0xffffffffu, lo, o));
-            hi = fmax(hi, __shfl_xor_sync(0xffffffffu, hi, o));
-        }
-        if (lane < 2) {
-            // lane 0: first source with key >= key(lo - a); lane 1: first with key > key(hi + a)
-            const int kb = lane == 0 ? fine_key(lo - ag, shift, kmax) : fine_key(hi + ag, shift, kmax);
+    if (threadIdx.x == 0) {
+        // targets sorted by fine key: the chunk's interval is [u(i0), u(ilast)] to within a key bin
+        const double lo = fmin(ut[i0], ut[ilast]) - ldexp(1.0, -shift);
+        const double hi = fmax(ut[i0], ut[ilast]) + ldexp(1.0, -shift);
+        chunk_lo = lo;
+        for (int side = 0; side < 2; ++side) {
+            // side 0: first source with key >= key(lo - a); side 1: first with key > key(hi + a)
+            const int kb = side == 0 ? fine_key(lo - ag, shift, kmax) : fine_key(hi + ag, shift, kmax);
             long long L = 0, R = ns;
             while (L < R) {
                 const long long M = (L + R) >> 1;
                 const int km = fine_key(us[M], shift, kmax);
-                if (lane == 0 ? km < kb : km <= kb) L = M + 1; else R = M;
+                if (side == 0 ? km < kb : km <= kb) L = M + 1; else R = M;
             }
-            range[lane] = L;
+            range[side] = L;
         }
-        if (lane == 0) chunk_lo = lo;
     }
     __syncthreads();
     const long long j0 = range[0], j1 = range[1];
     const double c = chunk_lo;
     const double lam_n = np.lam_p * np.inv_n;   // lam' per grid unit
-    // every exponent lam' |u - c| of this CTA below kNearExpMax (sources sorted: the ends bound it)
-    const bool sep = j1 > j0 && lam_n * fmax(fabs(us[j1 - 1] - c), fabs(us[j0] - c)) < kNearExpMax &&
-                     lam_n * (active ? ut[i] - c : 0.0) < kNearExpMax;
-    const bool sep_all = __syncthreads_and(sep);
-    const double ui = active ? ut[i] : c;
-    const double xi = ui * np.inv_n;
-    const double gi = sep_all ? exp(-lam_n * (ui - c)) : 1.0, igi = 1.0 / gi;
-    const double a2 = np.a * np.a, inv_a2 = 1.0 / a2;
-    double ki[kNearKI];
+    const double to_a = np.inv_n / np.a;        // grid units -> units of the radius
+    double xi[kNearTPL], gi[kNearTPL], igi[kNearTPL], acc[kNearTPL];
+    bool sep = j1 > j0 && lam_n * fmax(fabs(us[j1 - 1] - c), fabs(us[j0] - c)) < kNearExpMax;
 #pragma unroll
-    for (int q = 0; q < kNearKI; ++q) ki[q] = q < np.ki_n ? np.ki[q] : 0.0;
-    double acc = 0.0;
+    for (int e = 0; e < kNearTPL; ++e) {
+        const long long i = i0 + e * 32 + lane;
+        const double ui = i < nt ? ut[i] : c;
+        sep = sep && lam_n * (ui - c) < kNearExpMax;
+        xi[e] = ui * to_a;
+        gi[e] = ui;
+        acc[e] = 0.0;
+    }
+    // every exponent lam' |u - c| of this CTA below kNearExpMax (sources sorted: the ends bound it)
+    const bool sep_all = __syncthreads_and(sep);
+#pragma unroll
+    for (int e = 0; e < kNearTPL; ++e) {
+        gi[e] = sep_all ? exp(-lam_n * (gi[e] - c)) : 1.0;
+        igi[e] = 1.0 / gi[e];
+    }
+    // K_I coefficients straight from the kernel parameters (constant-bank operands of the DFMAs;
+    // Plan::ki is zero beyond ki_n)
+    const double* ki = np.ki;
     for (long long jb = j0; jb < j1; jb += kNearBlk) {
         const int cnt = (int)min((long long)kNearBlk, j1 - jb);
         __syncthreads();
         for (int k = threadIdx.x; k < cnt; k += blockDim.x) {
             const double uj = us[jb + k], wj = w[jb + k];
-            syw[k] = make_double2(uj * np.inv_n, wj);
+            syw[k] = make_double2(uj * to_a, wj);
             if (sep_all) {
                 const double f = exp(lam_n * (uj - c));
                 sff[k] = make_double2(wj * f, wj / f);
             }
         }
         __syncthreads();
-        if (!active) continue;
-        acc = sep_all ? near_block<KERNEL, true>(syw, sff, cnt, warp, xi, gi, igi, a2, inv_a2, np.lam_p,
-                                                 np.rho_inv, ki, acc)
-                      : near_block<KERNEL, false>(syw, sff, cnt, warp, xi, gi, igi, a2, inv_a2, np.lam_p,
-                                                  np.rho_inv, ki, acc);
+        // r = a |dx| torus units, r / rho the caller's units (c K kernel)
+        if (sep_all) near_block<KERNEL, true>(syw, sff, cnt, warp, xi, gi, igi, np.lam_p * np.a, np.a * np.rho_inv, ki, acc);
+        else near_block<KERNEL, false>(syw, sff, cnt, warp, xi, gi, igi, np.lam_p * np.a, np.a * np.rho_inv, ki, acc);
     }
-    part[warp][lane] = acc;
+#pragma unroll
+    for (int e = 0; e < kNearTPL; ++e) part[warp][e * 32 + lane] = acc[e];
     __syncthreads();
-    if (warp == 0 && active) {
-        double sum = part[0][lane];
-        for (int q = 1; q < kNearWarps; ++q) sum += part[q][lane];
-        t[i] += sum;
+    if (threadIdx.x < CH && i0 + threadIdx.x < nt) {
+        double sum = part[0][threadIdx.x];
+        for (int q = 1; q < kNearWarps; ++q) sum += part[q][threadIdx.x];
+        t[i0 + threadIdx.x] += sum;
     }
 }
 
@@ -901,7 +920,7 @@ int launch_nearfield(Plan& P, int src, int dst, int kernel, const double* w_sort
     np.inv_n = 1.0 / P.n;
     for (int i = 0; i < 16; ++i) np.ki[i] = P.ki[kernel][i];
     if (P.d == 1 && P.fine_shift) {
-        const long long blocks = (D.count + 31) / 32;
+        const long long blocks = (D.count + 32 * kNearTPL - 1) / (32 * kNearTPL);
         const int kmax = (int)(((long long)P.tiles_per_axis * P.tile_cells << P.fine_shift) - 1);
         if (P.ki_n > kNearKI) return set_error(SK_EINVAL, "near field: more than 8 K_I coefficients");
         const auto kern = kernel == 0 ? nearfield_d1_kernel<0> : nearfield_d1_kernel<1>;
