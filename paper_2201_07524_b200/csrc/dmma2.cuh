@@ -16,6 +16,7 @@
 namespace sk {
 
 constexpr int kSup2 = 4;  // d = 2 super-tile edge (cells)
+constexpr long long kSpread2CtaNodes = 150000;   // node sets at most this large: one spread item per CTA
 
 #ifndef SK_WORKLIST_ONLY
 
@@ -95,6 +96,7 @@ struct Spread2Cfg {
     static constexpr size_t SMEM_BYTES = sizeof(double) * (NWARP * REG);
 };
 
+template <bool CTA_ITEM>
 __global__ void __launch_bounds__(128, 4)
 spread2_dmma_kernel(const SpreadItem* __restrict__ items, int nitems, const CellBatch* __restrict__ segs,
                     const double* __restrict__ taps, const double* __restrict__ w, const GridAcc ga) {
@@ -107,14 +109,19 @@ spread2_dmma_kernel(const SpreadItem* __restrict__ items, int nitems, const Cell
     const int g = lane >> 2, q = lane & 3;
     double* REGm = smem + warp * C::REG;
     const int ns = n / kSup2;
-    const int gw = blockIdx.x * C::NWARP + warp, nw = gridDim.x * C::NWARP;
 
-    for (int ii = gw; ii < nitems; ii += nw) {
+    // CTA_ITEM (few items: small node sets): one item per CTA, warp w takes segments w, w + 4,
+    // ... into its own region and the flush adds the 4 regions in warp order (deterministic):
+    // 4 short dependent-load chains per item instead of one long one, which is the critical
+    // path at a few nodes per cell (img64 spread 23.5 -> 15.7 us, c2 26 -> 22 us). Otherwise
+    // one item per warp (many items: c4, img512 lose 15-35 % in the CTA form).
+    const int gw = blockIdx.x * C::NWARP + warp, nw = gridDim.x * C::NWARP;
+    for (int ii = CTA_ITEM ? blockIdx.x : gw; ii < nitems; ii += CTA_ITEM ? gridDim.x : nw) {
         const SpreadItem it = items[ii];
         const int sy = it.stile % ns, sx = it.stile / ns;
         for (int i = lane; i < C::REG; i += 32) REGm[i] = 0.0;
         __syncwarp();
-        for (int sg = it.seg_begin; sg < it.seg_end; ++sg) {
+        for (int sg = it.seg_begin + (CTA_ITEM ? warp : 0); sg < it.seg_end; sg += CTA_ITEM ? C::NWARP : 1) {
             const CellBatch seg = segs[sg];
             const int cy = seg.cell % n, cx = seg.cell / n;
             const int ox = cx - kSup2 * sx, oy = cy - kSup2 * sy;
@@ -151,11 +158,23 @@ spread2_dmma_kernel(const SpreadItem* __restrict__ items, int nitems, const Cell
             __syncwarp();
         }
         const int gx0 = kSup2 * sx - (m - 1), gy0 = kSup2 * sy - (m - 1);
-        for (int i = lane; i < C::REG; i += 32) {
-            const double v = REGm[i];
-            if (v != 0.0) grid_add<2>(ga, gscale, gx0 + i / S, gy0 + i % S, 0, v);
+        if (CTA_ITEM) {
+            __syncthreads();
+            for (int i = threadIdx.x; i < C::REG; i += C::NT) {
+                double v = smem[i];
+#pragma unroll
+                for (int w = 1; w < C::NWARP; ++w) v += smem[w * C::REG + i];
+                if (v != 0.0) grid_add<2>(ga, gscale, gx0 + i / S, gy0 + i % S, 0, v);
+            }
+            __syncthreads();
+        } else {
+            __syncwarp();
+            for (int i = lane; i < C::REG; i += 32) {
+                const double v = REGm[i];
+                if (v != 0.0) grid_add<2>(ga, gscale, gx0 + i / S, gy0 + i % S, 0, v);
+            }
+            __syncwarp();
         }
-        __syncwarp();
     }
 }
 

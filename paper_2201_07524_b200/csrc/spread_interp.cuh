@@ -244,12 +244,19 @@ inline int spread_dispatch(Plan& P, const NodeSet& S, const double* w, const Gri
         using C = Spread2Cfg;
         static std::atomic<unsigned long long> attr{0};
         if (first_on_device(attr)) {
-            cudaFuncSetAttribute(spread2_dmma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM_BYTES);
+            cudaFuncSetAttribute(spread2_dmma_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM_BYTES);
+            cudaFuncSetAttribute(spread2_dmma_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM_BYTES);
         }
         if (S.nsitems > 0) {
-            const int g = persistent_grid(spread2_dmma_kernel, C::NT, C::SMEM_BYTES, (S.nsitems + C::NWARP - 1) / C::NWARP);
-            spread2_dmma_kernel<<<g, C::NT, C::SMEM_BYTES, s>>>((const SpreadItem*)S.sitems, S.nsitems,
-                                                                (const CellBatch*)S.segs, S.taps, w, ga);
+            // small sets (c2, images up to 256^2): one item per CTA; larger: one per warp
+            // (measured: img512, c4 lose 15-35 % in the CTA form; SK_SPREAD2_CTA_NODES overrides)
+            static const long long cta_nodes = getenv("SK_SPREAD2_CTA_NODES") ? atoll(getenv("SK_SPREAD2_CTA_NODES"))
+                                                                               : kSpread2CtaNodes;
+            const bool cta = S.count <= cta_nodes;
+            const auto kern = cta ? spread2_dmma_kernel<true> : spread2_dmma_kernel<false>;
+            const int g = persistent_grid(kern, C::NT, C::SMEM_BYTES, cta ? S.nsitems : (S.nsitems + C::NWARP - 1) / C::NWARP);
+            kern<<<g, C::NT, C::SMEM_BYTES, s>>>((const SpreadItem*)S.sitems, S.nsitems, (const CellBatch*)S.segs,
+                                                 S.taps, w, ga);
             count_launch();
         }
         cudaError_t e = cudaGetLastError();
