@@ -26,66 +26,77 @@ struct Interp2Cfg {
     static constexpr size_t SMEM_BYTES = 0;
 };
 
+// One batch (<= 32 nodes of one cell) with NT_ n-tiles of 8 nodes: sparse cells (c2, the
+// images: a few nodes per cell) run ceil(count / 8) n-tiles instead of 4.
+template <int NT_>
+__device__ __forceinline__ void interp2_batch(const CellBatch& B, const double* __restrict__ taps,
+                                              const double* __restrict__ grid, int n, int g, int q,
+                                              double* __restrict__ t_out, const FusedUpd& fu) {
+    using C = Interp2Cfg;
+    constexpr int W = C::W, KS = C::KS, m = W / 2, TS = C::TS;
+    const int cy = B.cell % n, cx = B.cell / n;
+    const double* T0 = taps + (long long)B.start * TS;
+    const int last = B.count - 1;
+    const double* Hb = grid + (long long)(cx - m + 1) * n + (cy - m + 1) + q;
+    double a[2][KS];
+#pragma unroll
+    for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+        for (int s = 0; s < KS; ++s) a[mt][s] = __ldg(Hb + (long long)(8 * mt + g) * n + 4 * s);
+    double d[2][NT_][2];
+#pragma unroll
+    for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+        for (int nt = 0; nt < NT_; ++nt) d[mt][nt][0] = d[mt][nt][1] = 0.0;
+#pragma unroll
+    for (int nt = 0; nt < NT_; ++nt) {
+        const double* ty = T0 + min(8 * nt + g, last) * TS + W;
+#pragma unroll
+        for (int s = 0; s < KS; ++s) {
+            const double bf = __ldg(ty + 4 * s + q);
+            dmma884(d[0][nt][0], d[0][nt][1], a[0][s], bf);
+            dmma884(d[1][nt][0], d[1][nt][1], a[1][s], bf);
+        }
+    }
+    double acc[NT_][2];
+#pragma unroll
+    for (int nt = 0; nt < NT_; ++nt)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+            const double* tx = T0 + min(8 * nt + 2 * q + e, last) * TS;
+            double v = __ldg(tx + g) * d[0][nt][e];
+            v = fma(__ldg(tx + 8 + g), d[1][nt][e], v);
+            v += __shfl_xor_sync(0xffffffffu, v, 4);
+            v += __shfl_xor_sync(0xffffffffu, v, 8);
+            v += __shfl_xor_sync(0xffffffffu, v, 16);
+            acc[nt][e] = v;
+        }
+    // every lane now holds the sums of its q; lane (g, q) emits node 8 (g/2) + 2 q + g%2, so the
+    // results (and the fused division) take one full-warp pass
+    double v = acc[0][0];
+#pragma unroll
+    for (int nt = 0; nt < NT_; ++nt)
+#pragma unroll
+        for (int e = 0; e < 2; ++e)
+            if (g == 2 * nt + e) v = acc[nt][e];
+    const int p = 8 * (g >> 1) + 2 * q + (g & 1);
+    if ((g >> 1) < NT_ && p < B.count) emit_t(t_out, fu, B.start + p, v);
+}
+
 __global__ void __launch_bounds__(128, 4)
 interp2_dmma_kernel(const CellBatch* __restrict__ batches, int nbatches, const double* __restrict__ taps,
                     const double* __restrict__ grid, int n, double* __restrict__ t_out, const FusedUpd fu) {
     using C = Interp2Cfg;
-    constexpr int W = C::W, KS = C::KS, m = W / 2, TS = C::TS;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int g = lane >> 2, q = lane & 3;
     const int gw = blockIdx.x * C::NWARP + warp, nw = gridDim.x * C::NWARP;
-
     for (int bi = gw; bi < nbatches; bi += nw) {
         const CellBatch B = batches[bi];
-        const int cy = B.cell % n, cx = B.cell / n;
-        const double* T0 = taps + (long long)B.start * TS;
-        const int last = B.count - 1;
-        const double* Hb = grid + (long long)(cx - m + 1) * n + (cy - m + 1) + q;
-        double a[2][KS];
-#pragma unroll
-        for (int mt = 0; mt < 2; ++mt)
-#pragma unroll
-            for (int s = 0; s < KS; ++s) a[mt][s] = __ldg(Hb + (long long)(8 * mt + g) * n + 4 * s);
-        double d[2][4][2];
-#pragma unroll
-        for (int mt = 0; mt < 2; ++mt)
-#pragma unroll
-            for (int nt = 0; nt < 4; ++nt) d[mt][nt][0] = d[mt][nt][1] = 0.0;
-#pragma unroll
-        for (int nt = 0; nt < 4; ++nt) {
-            const double* ty = T0 + min(8 * nt + g, last) * TS + W;
-#pragma unroll
-            for (int s = 0; s < KS; ++s) {
-                const double bf = __ldg(ty + 4 * s + q);
-                dmma884(d[0][nt][0], d[0][nt][1], a[0][s], bf);
-                dmma884(d[1][nt][0], d[1][nt][1], a[1][s], bf);
-            }
-        }
-        double acc[4][2];
-#pragma unroll
-        for (int nt = 0; nt < 4; ++nt)
-#pragma unroll
-            for (int e = 0; e < 2; ++e) {
-                const double* tx = T0 + min(8 * nt + 2 * q + e, last) * TS;
-                double v = __ldg(tx + g) * d[0][nt][e];
-                v = fma(__ldg(tx + 8 + g), d[1][nt][e], v);
-                v += __shfl_xor_sync(0xffffffffu, v, 4);
-                v += __shfl_xor_sync(0xffffffffu, v, 8);
-                v += __shfl_xor_sync(0xffffffffu, v, 16);
-                acc[nt][e] = v;
-            }
-        // every lane now holds the 8 sums of its q; lane (g, q) emits node 8 (g/2) + 2 q + g%2,
-        // so the 32 results (and the fused division) take one full-warp pass
-        {
-            double v = acc[0][0];
-#pragma unroll
-            for (int nt = 0; nt < 4; ++nt)
-#pragma unroll
-                for (int e = 0; e < 2; ++e)
-                    if (g == 2 * nt + e) v = acc[nt][e];
-            const int p = 8 * (g >> 1) + 2 * q + (g & 1);
-            if (p < B.count) emit_t(t_out, fu, B.start + p, v);
-        }
+        const int ntn = (B.count + 7) >> 3;   // warp-uniform
+        if (ntn >= 4) interp2_batch<4>(B, taps, grid, n, g, q, t_out, fu);
+        else if (ntn == 3) interp2_batch<3>(B, taps, grid, n, g, q, t_out, fu);
+        else if (ntn == 2) interp2_batch<2>(B, taps, grid, n, g, q, t_out, fu);
+        else interp2_batch<1>(B, taps, grid, n, g, q, t_out, fu);
     }
 }
 

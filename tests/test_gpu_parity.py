@@ -70,6 +70,57 @@ def test_spread_interp_match_gridding_definition(capi, ctx, d, N, m_w, cnt):
     assert (np.abs(t - t_ref) <= 1e-14 * scale).all()
 
 
+@pytest.mark.parametrize("N,cnt,r", [(4096, 40, 2), (256, 200000, 2), (256, 50000, 1)])
+def test_d1_spread_windows_match_gridding_definition(capi, ctx, N, cnt, r):
+    """d = 1 spread (shared-memory window per CTA): sparse nodes on a large grid (windows wider
+    than the shared buffer take the direct path), 2e5 nodes (full 256-node CTAs, ragged tail),
+    and an r = 1 plan (position-sorted nodes) against the gridding definition. The grid
+    geometry (rho, centre) is the plan's own, pinned by the test above."""
+    rng = np.random.default_rng(N + cnt + r)
+    x = np.sort(rng.random((cnt, 1)), axis=0)[::-1].copy() if r == 1 else rng.random((cnt, 1))
+    y = rng.random((cnt + 5, 1))
+    w = rng.random(cnt)
+    kw = {"r": 1, "near_cells": 16} if r == 1 else {}
+    P = capi.Plan(ctx, dev(x), dev(y), 20.0, N, 2.0, 8, **kw)
+    info = P.info()
+    xs = nfft_ref.scale(x, np.asarray(info["centre"][:1]), info["rho"])
+    n = int(info["n_grid"])
+    g_ref = nfft_ref.grid_spread(xs, w, n, 8, 2.0)
+    g = capi.nfft_spread(P, 0, dev(w)).cpu().numpy()
+    # u = n (x' + 1/2) carries |u| ulp ~ n 2^-53 of rounding on either side; the window's slope
+    # turns it into ~1e-13 (n / 512) of phi(0) at n = 8192 (measured 3.6e-13)
+    assert np.abs(g - g_ref).max() <= 1e-13 * max(1.0, n / 512) * np.abs(g_ref).max()
+
+
+@pytest.mark.parametrize("case", ["single", "disjoint", "duplicates"])
+def test_r1_d1_nearfield_edges(capi, ctx, case):
+    """d = 1 near field edge cases against the oracle's statement of the method: one node per
+    side, supports farther apart than the radius (no near pairs), and heavy duplication
+    (runs of identical coordinates, equal fine keys)."""
+    from oracle import laplace_ref as LR
+    rng = np.random.default_rng(5)
+    if case == "single":
+        x, y = np.array([[0.3]]), np.array([[0.31]])
+    elif case == "disjoint":
+        x, y = 0.1 * rng.random((500, 1)), 0.9 + 0.1 * rng.random((400, 1))
+    else:
+        x = np.repeat(rng.random((40, 1)), 25, axis=0)
+        y = np.repeat(rng.random((30, 1)), 33, axis=0)
+    wy, wx = rng.random(y.shape[0]), rng.random(x.shape[0])
+    P = capi.Plan(ctx, dev(x), dev(y), 20.0, 128, 2.0, 8, 1 / 16, 8, r=1, near_cells=16)
+    for kernel in (0, 1):
+        t = capi.fastsum_apply(P, dev(wy), 0, kernel).cpu().numpy()
+        tt = capi.fastsum_apply(P, dev(wx), 1, kernel).cpu().numpy()
+        ref = LR.fastsum_ndft(x, y, wy, 20.0, 128, 1 / 16, 8, 16, kernel=kernel)
+        reft = LR.fastsum_ndft(y, x, wx, 20.0, 128, 1 / 16, 8, 16, kernel=kernel)
+        # the window error is absolute, ~1e-15 ||w||_1 (the NFFT bound): on disjoint supports
+        # the sums themselves are ~e^-16 ||w||_1, so the gate is on that scale, not on max |t|
+        assert np.abs(t - ref).max() <= 1e-13 * np.abs(wy).sum(), (case, kernel, np.abs(t - ref).max())
+        assert np.abs(tt - reft).max() <= 1e-13 * np.abs(wx).sum(), (case, kernel, np.abs(tt - reft).max())
+        if case != "disjoint":
+            assert rel_linf(t, ref) <= 1e-12 and rel_linf(tt, reft) <= 1e-12, (case, kernel, rel_linf(t, ref))
+
+
 @pytest.mark.parametrize("d,m_w", [(3, 6), (2, 8)])
 def test_cell_occupancies_match_gridding_definition(capi, ctx, d, m_w):
     """Clusters of x nodes confined to single grid cells, one cluster per occupancy in
