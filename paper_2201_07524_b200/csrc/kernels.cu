@@ -185,7 +185,7 @@ static ScaleParams scale_params(const Plan& P) {
     sp.d = P.d;
     sp.T = P.tile_cells;
     sp.tiles_per_axis = P.tiles_per_axis;
-    sp.cell_minor = P.dmma ? 1 : 0;
+    sp.cell_minor = (P.dmma || P.near_cell_sort) ? 1 : 0;
     sp.xminor = P.spread_xpairs ? 1 : 0;
     sp.Td = 1;
     for (int a = 0; a < P.d; ++a) sp.Td *= P.tile_cells;
@@ -194,17 +194,19 @@ static ScaleParams scale_params(const Plan& P) {
     return sp;
 }
 
-// fine (position) keys -> tile index, in place, for tile_offsets
-__global__ void fine_to_tile_kernel(int* __restrict__ key, long long count, int shift, int T, int tpa) {
+// fine (position, d = 1) or (tile, cell) keys -> tile index, in place, for tile_offsets
+__global__ void key_to_tile_kernel(int* __restrict__ key, long long count, int shift, int T, int tpa, int Td) {
     for (long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x; k < count;
          k += (long long)gridDim.x * blockDim.x)
-        key[k] = min(tpa - 1, (key[k] >> shift) / T);
+        key[k] = shift ? min(tpa - 1, (key[k] >> shift) / T) : key[k] / Td;
 }
 
-int launch_fine_to_tile(Plan& P, int* key, long long count, cudaStream_t s) {
+int launch_key_to_tile(Plan& P, int* key, long long count, cudaStream_t s) {
     if (count <= 0) return SK_OK;
-    fine_to_tile_kernel<<<grid_for(count, 256), 256, 0, s>>>(key, count, P.fine_shift, P.tile_cells,
-                                                             P.tiles_per_axis);
+    int Td = 1;
+    for (int a = 0; a < P.d; ++a) Td *= P.tile_cells;
+    key_to_tile_kernel<<<grid_for(count, 256), 256, 0, s>>>(key, count, P.fine_shift, P.tile_cells,
+                                                            P.tiles_per_axis, Td);
     SK_LAUNCH_CHECK();
     return SK_OK;
 }
@@ -901,6 +903,131 @@ __global__ void __launch_bounds__(kNearWarps * 32, SK_NEAR_MINB) nearfield_d1_ke
     }
 }
 
+// d >= 2 near field (r = 1), one CTA per NearItem (<= 64 targets of a run of tiles along the last
+// axis, 2 per lane): the source tiles within the radius of the item's tiles form (2 ceil(R / T) + 2)^(d-1) runs that
+// are contiguous in sorted order (consecutive tiles along the last axis); the CTA streams their
+// concatenation through shared memory in blocks of kNearBlk and each of the 8 warps sums its
+// targets against every 8th staged source (partials added in warp order). Per pair in the
+// ball: r = sqrt(t2) in units of the radius, exp(-lam' r) (no factoring off the line), the K_I
+// Horner in t2; pairs outside the ball are skipped (divergent only near the ball's surface).
+constexpr int kNearSegMax = 512;
+template <int D, int KERNEL>
+__global__ void __launch_bounds__(kNearWarps * 32, 2) nearfield_tiled_kernel(
+    NearParams np, const NearItem* __restrict__ items, const double* __restrict__ ut, long long nt,
+    const double* __restrict__ us, long long ns, const int* __restrict__ tile_start, const double* __restrict__ w,
+    double* __restrict__ t) {
+    __shared__ double sy[D][kNearBlk], sw[kNearBlk];
+    __shared__ double part[kNearWarps][kNearChunk];
+    __shared__ int seg_a[kNearSegMax], seg_pre[kNearSegMax + 1];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const NearItem it = items[blockIdx.x];
+    int tc[3] = {0, 0, 0}, te[3] = {0, 0, 0}, lo[3], hi[3];
+    for (int a = D - 1, r = it.tile, r2 = it.tile_last; a >= 0; --a) {
+        tc[a] = r % np.tpa; r /= np.tpa;
+        te[a] = r2 % np.tpa; r2 /= np.tpa;
+    }
+    for (int a = 0; a < D; ++a) {
+        // a target in tiles tc .. te reaches cells [tc T - R, (te + 1) T + R - 1]
+        const int lc = tc[a] * np.T - np.R, hc = (te[a] + 1) * np.T + np.R - 1;
+        lo[a] = lc <= 0 ? 0 : lc / np.T;
+        hi[a] = min(np.tpa - 1, hc / np.T);
+    }
+    const int n0 = hi[0] - lo[0] + 1, n1 = D > 2 ? hi[1] - lo[1] + 1 : 1;
+    const int ncand = n0 * n1;   // <= kNearSegMax (checked at launch)
+    // segment k: tiles (lo0 + k / n1, lo1 + k % n1, lo_last .. hi_last), its length, then an
+    // exclusive prefix over the lengths (block scans of 256 segments at a time)
+    __shared__ int wsum[kNearWarps];
+    int carry = 0;
+    if (threadIdx.x == 0) seg_pre[0] = 0;
+    for (int k0 = 0; k0 < ncand; k0 += kNearWarps * 32) {
+        const int k = k0 + threadIdx.x;
+        int len = 0;
+        if (k < ncand) {
+            const int t0 = lo[0] + k / n1, t1 = D > 2 ? lo[1] + k % n1 : 0;
+            const int base = D == 2 ? t0 * np.tpa : (t0 * np.tpa + t1) * np.tpa;
+            const int a0 = tile_start[base + lo[D - 1]], b0 = tile_start[base + hi[D - 1] + 1];
+            seg_a[k] = a0;
+            len = b0 - a0;
+        }
+        int v = len;
+        for (int o = 1; o < 32; o <<= 1) {
+            const int y = __shfl_up_sync(0xffffffffu, v, o);
+            if (lane >= o) v += y;
+        }
+        __syncthreads();   // wsum of the previous round consumed
+        if (lane == 31) wsum[warp] = v;
+        __syncthreads();
+        int off = carry, all = 0;
+        for (int q = 0; q < kNearWarps; ++q) {
+            if (q < warp) off += wsum[q];
+            all += wsum[q];
+        }
+        if (k < ncand) seg_pre[k + 1] = off + v;
+        carry += all;
+    }
+    __syncthreads();
+    const int total = seg_pre[ncand];
+    const double to_a = np.inv_n / np.a;   // grid units -> units of the radius
+    double xi[2][D], acc[2] = {0.0, 0.0};
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+        const int k = e * 32 + lane;
+#pragma unroll
+        for (int a = 0; a < D; ++a) xi[e][a] = k < it.count ? ut[a * nt + it.start + k] * to_a : 1e300;
+    }
+    const double lam_a = np.lam_p * np.a, r_scale = np.a * np.rho_inv;
+    const double* ki = np.ki;
+    for (int p0 = 0; p0 < total; p0 += kNearBlk) {
+        const int cnt = min(kNearBlk, total - p0);
+        __syncthreads();
+        for (int k = threadIdx.x; k < cnt; k += blockDim.x) {
+            const int p = p0 + k;
+            int L = 0, R = ncand;   // last segment with seg_pre <= p
+            while (R - L > 1) {
+                const int M = (L + R) >> 1;
+                if (seg_pre[M] <= p) L = M; else R = M;
+            }
+            const long long j = seg_a[L] + (p - seg_pre[L]);
+#pragma unroll
+            for (int a = 0; a < D; ++a) sy[a][k] = us[a * ns + j] * to_a;
+            sw[k] = w[j];
+        }
+        __syncthreads();
+        for (int k = warp; k < cnt; k += kNearWarps) {
+            double yk[D];
+#pragma unroll
+            for (int a = 0; a < D; ++a) yk[a] = sy[a][k];
+            const double wk = sw[k];
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+                double t2 = 0.0;
+#pragma unroll
+                for (int a = 0; a < D; ++a) {
+                    const double dx = xi[e][a] - yk[a];
+                    t2 = fma(dx, dx, t2);
+                }
+                if (t2 < 1.0) {
+                    const double r = sqrt(t2);   // |x - y| / a
+                    double kv = wk * exp(-lam_a * r);
+                    if (KERNEL == 1) kv *= r * r_scale;
+                    double q = ki[kNearKI - 1];
+#pragma unroll
+                    for (int c = kNearKI - 2; c >= 0; --c) q = fma(q, t2, ki[c]);
+                    acc[e] += fma(-wk, q, kv);
+                }
+            }
+        }
+    }
+#pragma unroll
+    for (int e = 0; e < 2; ++e) part[warp][e * 32 + lane] = acc[e];
+    __syncthreads();
+    if ((int)threadIdx.x < it.count) {
+        double sum = part[0][threadIdx.x];
+        for (int q = 1; q < kNearWarps; ++q) sum += part[q][threadIdx.x];
+        t[it.start + threadIdx.x] += sum;
+    }
+}
+
 int launch_nearfield(Plan& P, int src, int dst, int kernel, const double* w_sorted, double* t_sorted,
                      cudaStream_t s) {
     const NodeSet& S = P.side[src];
@@ -927,8 +1054,23 @@ int launch_nearfield(Plan& P, int src, int dst, int kernel, const double* w_sort
         kern<<<(unsigned)blocks, kNearWarps * 32, 0, s>>>(np, D.u, D.count, S.u, S.count, P.fine_shift, kmax,
                                                           w_sorted, t_sorted);
     } else {
-        nearfield_kernel<<<grid_for(D.count, 128), 128, 0, s>>>(np, D.u, D.count, S.u, S.count, S.tile_start,
-                                                                w_sorted, t_sorted);
+        // d >= 2: the tiled kernel when the item's source runs fit its shared list
+        const int span = 2 * ((P.near_cells + P.tile_cells - 1) / P.tile_cells) + 2;
+        int runs = 1;
+        for (int a = 0; a + 1 < P.d; ++a) runs *= span;
+        static const bool v1 = getenv("SK_NEARFIELD_V1") != nullptr;
+        if (!v1 && P.d >= 2 && D.n_near > 0 && runs <= kNearSegMax && P.ki_n <= kNearKI) {
+            const NearItem* it = (const NearItem*)D.near_items;
+            if (P.d == 2)
+                (kernel == 0 ? nearfield_tiled_kernel<2, 0> : nearfield_tiled_kernel<2, 1>)
+                    <<<D.n_near, kNearWarps * 32, 0, s>>>(np, it, D.u, D.count, S.u, S.count, S.tile_start, w_sorted, t_sorted);
+            else
+                (kernel == 0 ? nearfield_tiled_kernel<3, 0> : nearfield_tiled_kernel<3, 1>)
+                    <<<D.n_near, kNearWarps * 32, 0, s>>>(np, it, D.u, D.count, S.u, S.count, S.tile_start, w_sorted, t_sorted);
+        } else {
+            nearfield_kernel<<<grid_for(D.count, 128), 128, 0, s>>>(np, D.u, D.count, S.u, S.count, S.tile_start,
+                                                                    w_sorted, t_sorted);
+        }
     }
     SK_LAUNCH_CHECK();
     return SK_OK;

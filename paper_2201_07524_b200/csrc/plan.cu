@@ -232,6 +232,37 @@ static int choose_tile(int d, int n, bool tiled) {
     return T;
 }
 
+// r = 1, d >= 2 near-field work list: every non-empty tile's targets in chunks of
+// <= kNearChunk, so a CTA's targets share one tile and one neighbourhood of source tiles.
+static int build_near_items(Plan& P, NodeSet& S, cudaStream_t s) {
+    std::vector<int> ts(S.ntiles + 1);
+    SK_CUDA(cudaMemcpyAsync(ts.data(), S.tile_start, sizeof(int) * (S.ntiles + 1), cudaMemcpyDeviceToHost, s));
+    SK_CUDA(cudaStreamSynchronize(s));
+    // sparse tiles (a few targets each, e.g. d = 3 with 2^3-cell tiles) are merged along the
+    // last axis while they share the row and the item stays <= kNearChunk targets
+    std::vector<NearItem> items;
+    const int tpa = P.tiles_per_axis;
+    for (int t = 0; t < S.ntiles; ++t) {
+        const int cnt = ts[t + 1] - ts[t];
+        if (cnt <= 0) continue;
+        NearItem* last = items.empty() ? nullptr : &items.back();
+        if (last && last->tile_last / tpa == t / tpa && last->start + last->count == ts[t] &&
+            last->count + cnt <= kNearChunk) {
+            last->count += cnt;
+            last->tile_last = t;
+            continue;
+        }
+        for (int c = ts[t]; c < ts[t + 1]; c += kNearChunk)
+            items.push_back(NearItem{t, c, std::min(kNearChunk, ts[t + 1] - c), t});
+    }
+    S.n_near = (int)items.size();
+    SK_TRY(alloc(&S.near_items, sizeof(NearItem) * std::max<size_t>(items.size(), 1)));
+    if (!items.empty())
+        SK_CUDA(cudaMemcpyAsync(S.near_items, items.data(), sizeof(NearItem) * items.size(), cudaMemcpyHostToDevice, s));
+    SK_CUDA(cudaStreamSynchronize(s));
+    return SK_OK;
+}
+
 // Work list of the tiled kernels: one item per non-empty tile, dense tiles split into
 // balanced chunks of <= kItemMax nodes; sorted by size (largest first) so the static
 // round-robin over CTAs balances.
@@ -523,7 +554,7 @@ static int plan_side(Plan& P, int sidx, const double* pts, long long count, cuda
     long long Td = 1;
     for (int a = 0; a < P.d; ++a) Td *= P.tile_cells;
     const long long nkeys = P.fine_shift ? ((long long)S.ntiles * P.tile_cells << P.fine_shift)
-                                         : (P.dmma ? (long long)S.ntiles * Td : S.ntiles);
+                                         : ((P.dmma || P.near_cell_sort) ? (long long)S.ntiles * Td : S.ntiles);
     int end_bit = 1;
     while ((1LL << end_bit) < nkeys) ++end_bit;
     size_t tmp_bytes = 0;
@@ -543,11 +574,17 @@ static int plan_side(Plan& P, int sidx, const double* pts, long long count, cuda
         SK_TRY(alloc((void**)&S.taps, sizeof(double) * count * P.d * 2 * P.win.m));
         SK_TRY(launch_taps(P, sidx, s));
         plan_trace("side: taps", s);
+        if (P.rpow == 1) {   // the near field's tile CSR (keys are tile * T^d + cell; scratch now)
+            SK_TRY(launch_key_to_tile(P, S.cell_key, count, s));
+            SK_TRY(launch_tile_offsets(S.cell_key, count, S.ntiles, S.tile_start, s));
+            SK_TRY(build_near_items(P, S, s));
+        }
     } else {
-        if (P.fine_shift) SK_TRY(launch_fine_to_tile(P, S.cell_key, count, s));
+        if (P.fine_shift || P.near_cell_sort) SK_TRY(launch_key_to_tile(P, S.cell_key, count, s));
         SK_TRY(launch_tile_offsets(S.cell_key, count, S.ntiles, S.tile_start, s));
         SK_CUDA(cudaStreamSynchronize(s));
         if (P.tiled) SK_TRY(build_items(P, S, s));
+        if (P.rpow == 1 && P.d >= 2) SK_TRY(build_near_items(P, S, s));
     }
     sk_free(tmp);
     sk_free(key_in);
@@ -656,11 +693,13 @@ int build_plan(Ctx* ctx, Plan** out, int d, const double* x, long long n, const 
         WinPoly* wp = new WinPoly();
         const double err = build_winpoly(m_w, sigma, wp);
         P->winpoly = wp;
-        // r = 1 runs the plain v1 spread / interp: its near field walks the source tiles
-        P->tiled = (d == 3) && (m_w == 6 || m_w == 8) && err >= 0.0 && err <= 1e-14 && rpow == 2 &&
+        // r = 1 takes the same spread / interp (its near field walks the tile CSR, built for it
+        // on the DMMA path too); SK_R1_V1=1 keeps r = 1 on the plain v1 kernels
+        const bool fast = rpow == 2 || getenv("SK_R1_V1") == nullptr;
+        P->tiled = (d == 3) && (m_w == 6 || m_w == 8) && err >= 0.0 && err <= 1e-14 && fast &&
                    getenv("SK_FORCE_V1") == nullptr;
         P->dmma = ((P->tiled && m_w == 6) || (d == 2 && m_w == 8 && err >= 0.0 && err <= 1e-14)) &&
-                  rpow == 2 && getenv("SK_NO_DMMA") == nullptr && getenv("SK_FORCE_V1") == nullptr;
+                  fast && getenv("SK_NO_DMMA") == nullptr && getenv("SK_FORCE_V1") == nullptr;
         if (P->dmma && d == 2) P->tiled = false;
         // d = 3 spread: the padded DMMA spread on TMA-fed warp pairs, x-pair segments for
         // sparse sets (SK_NO_XPAIRS=1 disables them)
@@ -681,6 +720,7 @@ int build_plan(Ctx* ctx, Plan** out, int d, const double* x, long long n, const 
         while (((long long)ng << (shift + 1)) <= (1LL << 30)) ++shift;
         P->fine_shift = shift;
     }
+    P->near_cell_sort = d >= 2 && rpow == 1 && !P->dmma && getenv("SK_NEARFIELD_V1") == nullptr;
 
     auto fail = [&](int code) { destroy_plan(P); return code; };
 
@@ -831,6 +871,7 @@ int destroy_plan(Plan* P) {
     for (int sidx = 0; sidx < 2; ++sidx) {
         NodeSet& S = P->side[sidx];
         sk_free(S.u); sk_free(S.perm); sk_free(S.cell_key); sk_free(S.tile_start); sk_free(S.items);
+        sk_free(S.near_items);
         sk_free(S.batches); sk_free(S.segs); sk_free(S.sitems); sk_free(S.taps);
     }
     sk_free(P->grid); sk_free(P->spec);

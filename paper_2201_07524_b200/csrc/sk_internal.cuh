@@ -72,7 +72,13 @@ struct NodeSet {
     void* sitems = nullptr;      // SpreadItem[nsitems]: segments of one 2^3 super-tile (spread)
     int nsitems = 0;
     double* taps = nullptr;      // [count][d][2 m_w] window taps of every node (sorted order)
+    // r = 1, d >= 2: near-field work list, <= kNearChunk consecutive targets of one tile row each
+    void* near_items = nullptr;  // NearItem[n_near]
+    int n_near = 0;
 };
+// consecutive targets of tiles tile .. tile_last of one row along the last axis
+struct NearItem { int tile, start, count, tile_last; };
+constexpr int kNearChunk = 64;
 
 struct Ctx {
     int device = 0;
@@ -100,6 +106,9 @@ struct Plan {
     // d = 1 with a near field: nodes sorted by position (key = floor(u 2^fine_shift)), not only by
     // tile, so a chunk of consecutive targets has one contiguous source range (0 = tile sort)
     int fine_shift = 0;
+    // d >= 2 with a near field: nodes sorted by (tile, cell within the tile), so the 64 targets
+    // of a near-field item (and each warp's 32) sit in a few adjacent cells
+    bool near_cell_sort = false;
     int ki_n = 0;
     int p_smooth = 8;
     double centre[kMaxD] = {0, 0, 0};
@@ -308,7 +317,7 @@ int launch_finalize_partials(const double* red, int nparts, int nvals, double* o
 int build_plan(Ctx* ctx, Plan** out, int d, const double* x, long long n, const double* y,
                long long m, double lambda, int N, double sigma, int m_w, double eps_B, int p,
                int rpow, int near_cells);
-int launch_fine_to_tile(Plan& P, int* key, long long count, cudaStream_t s);
+int launch_key_to_tile(Plan& P, int* key, long long count, cudaStream_t s);
 int launch_nearfield(Plan& P, int src, int dst, int kernel, const double* w_sorted, double* t_sorted,
                      cudaStream_t s);
 int destroy_plan(Plan* P);

@@ -832,6 +832,27 @@ def test_r1_d1_nearfield_tiles(capi, ctx, lam, kernel):
     assert rel_linf(t, ref) <= 1e-12 and rel_linf(tt, reft) <= 1e-12, (rel_linf(t, ref), rel_linf(tt, reft))
 
 
+@pytest.mark.parametrize("d,N,kernel", [(2, 64, 0), (2, 64, 1), (3, 32, 0), (3, 32, 1)])
+def test_r1_tiled_nearfield(capi, ctx, d, N, kernel):
+    """d >= 2 near field (one CTA per <= 64 targets of a tile, source-tile runs streamed through
+    shared memory) at sizes spanning many items and several staged blocks per item, clustered
+    targets and a ragged tail: GPU = the oracle's statement of the method."""
+    from oracle import laplace_ref as LR
+    rng = np.random.default_rng(300 + d)
+    n, m = (6000 + 37, 5000 + 11) if d == 2 else (4000 + 37, 3000 + 11)
+    x = np.clip(rng.normal(0.5, 0.12, (n, d)), 0.0, 1.0)
+    y = rng.random((m, d))
+    wy, wx = rng.random(m), rng.random(n)
+    m_w = 8 if d == 2 else 6
+    P = capi.Plan(ctx, dev(x), dev(y), 20.0, N, 2.0, m_w, 1 / 16, 8, r=1, near_cells=16)
+    t = capi.fastsum_apply(P, dev(wy), 0, kernel).cpu().numpy()
+    tt = capi.fastsum_apply(P, dev(wx), 1, kernel).cpu().numpy()
+    ref = LR.fastsum_ndft(x, y, wy, 20.0, N, 1 / 16, 8, 16, kernel=kernel)
+    reft = LR.fastsum_ndft(y, x, wx, 20.0, N, 1 / 16, 8, 16, kernel=kernel)
+    window = 1e-12 if d < 3 else 1e-9
+    assert rel_linf(t, ref) <= window and rel_linf(tt, reft) <= window, (rel_linf(t, ref), rel_linf(tt, reft))
+
+
 @pytest.mark.parametrize("d,seed", [(1, 0), (1, 1), (2, 0), (2, 1), (3, 0)])
 def test_random_r1_configs_match_method_statement(capi, ctx, d, seed):
     """r = 1 plans with seeded random sizes, lambda, N and near-field radius: GPU = the oracle's
