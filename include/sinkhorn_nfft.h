@@ -112,9 +112,11 @@ int fastsum_plan(sk_ctx_t ctx, sk_plan_t* plan, int d,
  * the Fourier series is built from K_I | K | K_B, and every fast summation adds the near field
  *   t_i += sum over |x'_i - y'_j| < a of w_j (K - K_I)(|x'_i - y'_j|)
  * (direct sum over the source tiles around each target). The divergence kernel c K uses
- * c = |x - y| in original units. r = 1 runs the plain spread / interp kernels.
- * Errors: SK_EINVAL for r not in {1, 2}, near_cells < 1, p_smooth > 8 (r = 1; the monomial K_I system is ill-conditioned beyond) or
- * a >= 1/2 - eps_B; otherwise as fastsum_plan. */
+ * c = |x - y| in original units. r = 1 runs the same spread / interp kernels as r = 2.
+ * r = 1 plans are single-rank: the near field needs every source within the radius of a
+ * target, which a sharded source set does not hold (an all-gather of the sources is not built).
+ * Errors: SK_EINVAL for r not in {1, 2}, near_cells < 1, p_smooth > 8 (r = 1; the monomial K_I system is ill-conditioned beyond),
+ * a >= 1/2 - eps_B, or r = 1 on a context with world_size > 1; otherwise as fastsum_plan. */
 typedef struct {
     double lambda;
     int    r;             /* 1 or 2 */

@@ -639,6 +639,9 @@ int build_plan(Ctx* ctx, Plan** out, int d, const double* x, long long n, const 
     if (rpow != 1 && rpow != 2) return set_error(SK_EINVAL, "r must be 1 or 2");
     if (rpow == 1 && (near_cells < 1 || p > 8))
         return set_error(SK_EINVAL, "r = 1 needs near_cells >= 1 and p_smooth <= 8 (K_I monomial system)");
+    if (rpow == 1 && ctx && ctx->world > 1)
+        return set_error(SK_EINVAL, "r = 1 plans are single-rank (the near field needs every source near a "
+                                    "target; sharded sources are not gathered)");
     if (N < 2 || (N & 1)) return set_error(SK_EINVAL, "N must be even and >= 2");
     if (!(lambda > 0.0) || !isfinite(lambda)) return set_error(SK_EINVAL, "lambda must be > 0");
     if (m_w < 2 || m_w > 8) return set_error(SK_EINVAL, "m_w must be in [2, 8]");

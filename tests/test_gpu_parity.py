@@ -614,6 +614,21 @@ def test_emulated_two_rank_world(capi):
         c.close()
 
 
+def test_r1_multi_rank_is_rejected(capi):
+    """r = 1 plans are single-rank (include/sinkhorn_nfft.h): with world_size > 1 the near field
+    would miss the other ranks' sources, so fastsum_plan_ex returns SK_EINVAL."""
+    os.environ["SK_EMULATE_WORLD"] = "2"
+    try:
+        c2 = capi.Context(0)
+    finally:
+        del os.environ["SK_EMULATE_WORLD"]
+    x = dev(np.random.default_rng(0).random((100, 1)))
+    with pytest.raises(capi.SkError) as e:
+        capi.Plan(c2, x, x, 20.0, 64, 2.0, 8, r=1, near_cells=16)
+    assert e.value.code == 1 and "single-rank" in str(e.value)
+    c2.close()
+
+
 def test_nccl_one_rank_path(capi):
     """world_size 1 with an ncclUniqueId: a real one-rank NCCL communicator, so the bbox min/max,
     the box exchange of every fast summation and the scalar sums all run through ncclAllReduce
