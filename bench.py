@@ -59,9 +59,12 @@ def parse():
 
 def workload_config(cfg):
     """The `config` keys both arms report for a workload."""
-    return {"workload": cfg.name, "n": cfg.n, "m": cfg.m, "d": cfg.d, "lambda": cfg.lam, "N": cfg.N,
-            "sigma": cfg.sigma, "m_w": cfg.m_w, "eps_B": cfg.eps_B, "iters_per_step": cfg.iters,
-            "step": "plan + iters x (K v, K^T u) + divergence (2 applies)"}
+    out = {"workload": cfg.name, "n": cfg.n, "m": cfg.m, "d": cfg.d, "lambda": cfg.lam, "N": cfg.N,
+           "sigma": cfg.sigma, "m_w": cfg.m_w, "eps_B": cfg.eps_B, "iters_per_step": cfg.iters,
+           "step": "plan + iters x (K v, K^T u) + divergence (2 applies)"}
+    if cfg.r != 2:   # cost |x - y|^r: r = 1 is the Laplace kernel with its near field
+        out.update({"r": cfg.r, "near_cells": cfg.near_cells})
+    return out
 
 
 def peaks():
