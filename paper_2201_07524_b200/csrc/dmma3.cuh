@@ -409,6 +409,103 @@ constexpr int kSparsePairs = SK_TP_NPAIR_SPARSE;   // warp pairs per CTA of the 
 using SpreadTPCfgSparse = SpreadTPCfg<kSegTmaPMax, kSparsePairs>;
 using SpreadTPCfgDense = SpreadTPCfg<kSegTmaPDense, 2>;
 
+// ------------------------------------------------------------------------------ 28-tile cover
+// A node's 12^3 contributions w phi_x[tx] phi_y[ty] phi_z[tz] tiled by m8n8k4 DMMA tiles instead
+// of 12 -> 16 padded rows (36 DMMA.8x8x4 per 4-node k-step, 75 % useful): 1728 = 27 x 64, and
+// with each tile's rows and columns products of whole axes the cover needs 28 tiles (96 %):
+//   F1 (18): rows tx = g (0..7),                 cols (ty, tz) = flat 8 jn + c      A = w phi_x,  B = phi_y phi_z
+//   F2  (6): rows (tx, ty) = (8 + g%4, 2p + g/4), cols tz = c (0..7)                 A = w phi_x phi_y, B = phi_z
+//   F3  (2): rows ty = g (0..7),                 cols (tx, tz) = (8 + 2t + c/4, 8 + c%4)  A = phi_y, B = w phi_x phi_z
+//   F4  (2): rows as F2 with p = 4, 5,           cols tz = 8 + c (c < 4; c >= 4 zero)
+// (F1 tx 0..7 x all (ty, tz): 1152; F2 tx 8..11 x ty 0..11 x tz 0..7: 384; F3 tx 8..11 x ty 0..7 x
+// tz 8..11: 128; F4 tx 8..11 x ty 8..11 x tz 8..11: 64.) Warp h of the pair takes 14 tiles:
+// h = 0: F1 jn 0..8, F2 p 0..4;  h = 1: F1 jn 9..17, F2 p 5, F3 t 0, 1, F4 p 4, 5 (16 DMULs each).
+// acc index: 0..8 F1; h = 0: 9..13 F2 p; h = 1: 9 F2 p5, 10..11 F3, 12..13 F4.
+#ifndef SK_SPREAD3_T28
+#define SK_SPREAD3_T28 1
+#endif
+template <int H, int kSU>
+__device__ __forceinline__ void spread3_t28_ksteps(double (&acc)[14][2], const double* __restrict__ T0,
+                                                   const double* __restrict__ W0, int count, int nks, int g,
+                                                   int q) {
+    constexpr int W = 12, TS = 3 * W;
+    const int z1 = (8 + g) % W;
+#pragma unroll kSU
+    for (int s = 0; s < nks; ++s) {
+        const int jr = 4 * s + q;
+        const bool ok = jr < count;
+        const double* tr = T0 + (ok ? jr : 0) * TS;
+        const double wu = ok ? W0[jr] : 0.0;
+        const double wx0 = wu * tr[g];
+        const double wx1 = wu * tr[8 + (g & 3)];
+        double yv[6];
+        {
+            const double2* y2 = reinterpret_cast<const double2*>(tr + W + 6 * H);
+#pragma unroll
+            for (int i = 0; i < 3; ++i) { const double2 v2 = y2[i]; yv[2 * i] = v2.x; yv[2 * i + 1] = v2.y; }
+        }
+        const double zv[3] = {tr[2 * W + g], tr[2 * W + z1], tr[2 * W + 4 + g]};
+#pragma unroll
+        for (int j = 0; j < 9; ++j) {   // F1: f = 8 (9H + j) + g -> ty = 6H + 2 (j / 3) + {0, g >= 4, 1}
+            const int k3 = j / 3, r3 = j % 3;
+            const double yvv = (r3 == 0) ? yv[2 * k3]
+                             : ((r3 == 1) ? (g >= 4 ? yv[2 * k3 + 1] : yv[2 * k3]) : yv[2 * k3 + 1]);
+            dmma884(acc[j][0], acc[j][1], wx0, yvv * zv[r3]);
+        }
+        const int gy = g >> 2;
+        if constexpr (H == 0) {
+#pragma unroll
+            for (int p = 0; p < 5; ++p) dmma884(acc[9 + p][0], acc[9 + p][1], wx1 * tr[W + 2 * p + gy], zv[0]);
+        } else {
+            const double a5 = wx1 * tr[W + 10 + gy], a4 = wx1 * tr[W + 8 + gy];
+            dmma884(acc[9][0], acc[9][1], a5, zv[0]);
+            const double wz = wu * tr[2 * W + 8 + (g & 3)];
+            const double ay = tr[W + g];
+            dmma884(acc[10][0], acc[10][1], ay, wz * tr[8 + gy]);
+            dmma884(acc[11][0], acc[11][1], ay, wz * tr[10 + gy]);
+            const double bz = g < 4 ? zv[1] : 0.0;   // zv[1] = phi_z[8 + g] for g < 4
+            dmma884(acc[12][0], acc[12][1], a4, bz);
+            dmma884(acc[13][0], acc[13][1], a5, bz);
+        }
+    }
+}
+// Adds the 14 tiles' C fragments (c_e = C[g][2q + e]) into the region at rc (the cell's (0,0,0)
+// tap; strides S^2, S, 1).
+template <int H>
+__device__ __forceinline__ void spread3_t28_update(double (&acc)[14][2], double* rc, int g, int q) {
+    constexpr int W = 12, S = W + 1;
+#pragma unroll
+    for (int j = 0; j < 9; ++j)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+            const int f = 8 * (9 * H + j) + 2 * q + e;
+            rc[g * S * S + (f / W) * S + (f % W)] += acc[j][e];
+        }
+    const int tx1 = 8 + (g & 3), gy = g >> 2;
+    if constexpr (H == 0) {
+#pragma unroll
+        for (int p = 0; p < 5; ++p)
+#pragma unroll
+            for (int e = 0; e < 2; ++e) rc[tx1 * S * S + (2 * p + gy) * S + 2 * q + e] += acc[9 + p][e];
+    } else {
+#pragma unroll
+        for (int e = 0; e < 2; ++e) rc[tx1 * S * S + (10 + gy) * S + 2 * q + e] += acc[9][e];
+#pragma unroll
+        for (int t = 0; t < 2; ++t)
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+                const int c = 2 * q + e;
+                rc[(8 + 2 * t + (c >> 2)) * S * S + g * S + 8 + (c & 3)] += acc[10 + t][e];
+            }
+        if (q < 2) {
+#pragma unroll
+            for (int p = 0; p < 2; ++p)
+#pragma unroll
+                for (int e = 0; e < 2; ++e) rc[tx1 * S * S + (8 + 2 * p + gy) * S + 8 + 2 * q + e] += acc[12 + p][e];
+        }
+    }
+}
+
 // XP: segments may hold the nodes of an x-pair of cells (seg.cell is the x-digit-0 cell, its
 // seg.pad nodes come first, the rest sit one row lower): 13 of the 16 padded DMMA rows, so a
 // sparse pair costs one accumulator flush instead of two at no extra DMMA work.
@@ -463,6 +560,10 @@ spread3_tmapad_kernel(const SpreadItem* __restrict__ items, int nitems, const Ce
         for (int i = plane; i < C::REG; i += 64) REGm[i] = 0.0;
         double acc[NTH][4];   // m16n8k4 C: rows g (0, 1) and 8 + g (2, 3), columns 2q, 2q+1
         bool fresh = true;
+#if SK_SPREAD3_T28
+        double acc28[14][2];  // 14 m8n8k4 tiles of the 28-tile cover (spread3_t28_ksteps)
+        bool fresh28 = true;
+#endif
         for (int sg = it.seg_begin; sg < it.seg_end; ++sg, ++t) {
             const int b = t & 1;
             const CellBatch seg = segs[sg];
@@ -483,6 +584,25 @@ spread3_tmapad_kernel(const SpreadItem* __restrict__ items, int nitems, const Ce
                 fresh = false;
             }
             const int nks = (seg.count + 3) >> 2;
+#if SK_SPREAD3_T28
+            if constexpr (!XP) {
+                if (fresh28) {
+#pragma unroll
+                    for (int j = 0; j < 14; ++j) acc28[j][0] = acc28[j][1] = 0.0;
+                    fresh28 = false;
+                }
+                if (half == 0) spread3_t28_ksteps<0, kSU>(acc28, T0, W0, seg.count, nks, g, q);
+                else spread3_t28_ksteps<1, kSU>(acc28, T0, W0, seg.count, nks, g, q);
+                const bool flush28 = (sg + 1 >= it.seg_end) || (segs[sg + 1].cell != seg.cell);
+                if (flush28) {
+                    double* rc = REGm + ox * S * S + oy * S + oz;
+                    if (half == 0) spread3_t28_update<0>(acc28, rc, g, q);
+                    else spread3_t28_update<1>(acc28, rc, g, q);
+                    fresh28 = true;
+                }
+                continue;
+            }
+#endif
 #pragma unroll kSU
             for (int s = 0; s < nks; ++s) {
                 const int jr = 4 * s + q;
