@@ -79,8 +79,10 @@ constexpr int kSegTmaPMax = SK_TP_SEG_MAX;   // spread3_tmapad_kernel segments (
 #define SK_SPREAD3_PRODFIRST 0
 #endif
 constexpr int kSegTmaPDense = SK_TP_SEG_DENSE;   // spread3_tmapad_kernel segments (dense cells)
-constexpr int kSegDenseMinMean = 200;         // mean nodes per occupied cell for the dense shape
-                                              // (measured: c5 x 1793 / y 278 gain, c3 y 136 loses)
+constexpr int kSegDenseMinMean = 1 << 30;     // mean nodes per occupied cell for the dense shape:
+                                              // off since the 28-tile cover (162 registers fit 12
+                                              // warps per SM; c5 spread 12.46 -> 12.13 ms (y),
+                                              // 15.01 -> 14.91 ms (x)); round 1's 200 gained c5 x/y
 #ifndef SK_SPREAD_ITEM_MAX
 #define SK_SPREAD_ITEM_MAX 4096
 #endif
