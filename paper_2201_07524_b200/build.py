@@ -19,7 +19,7 @@ CSRC = os.path.join(PKG, "csrc")
 LIBDIR = os.path.join(PKG, "lib")
 LIB = os.path.join(LIBDIR, "libsk_nfft.so")
 BUILD = os.path.join(ROOT, "build")
-UNITS = ["api.cu", "kernels.cu", "plan.cu", "pruned_fft.cu"]
+UNITS = ["api.cu", "kernels.cu", "plan.cu", "pruned_fft.cu", "fftconv2.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 CUDA_HOME = os.environ.get("CUDA_HOME", "/usr/local/cuda")
 

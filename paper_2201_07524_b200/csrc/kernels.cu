@@ -1174,7 +1174,8 @@ __global__ void grid_fix_convert_kernel(const GridAcc ga, int d, long long grid_
     }
 }
 
-int launch_spread(Plan& P, int side, const double* w_sorted, double* grid, cudaStream_t s) {
+int launch_spread(Plan& P, int side, const double* w_sorted, double* grid, cudaStream_t s, GridAcc* keep,
+                  unsigned** keep_slot) {
     const NodeSet& S = P.side[side];
     if (S.count <= 0 || !P.deterministic) SK_CUDA(cudaMemsetAsync(grid, 0, sizeof(double) * P.grid_size, s));
     if (S.count <= 0) return SK_OK;
@@ -1198,6 +1199,11 @@ int launch_spread(Plan& P, int side, const double* w_sorted, double* grid, cudaS
         ga.wmax = slot;
     }
     SK_TRY(spread_dispatch(P, S, w_sorted, ga, s));
+    if (keep) {
+        *keep = ga;
+        *keep_slot = slot;
+        return SK_OK;
+    }
     if (P.deterministic) {
         grid_fix_convert_kernel<<<grid_for(P.grid_size, 256), 256, 0, s>>>(ga, P.d, P.grid_size, P.det_wmax + kWSlots,
                                                                            slot);

@@ -853,6 +853,15 @@ int build_plan(Ctx* ctx, Plan** out, int d, const double* x, long long n, const 
     P->box_exchange = ctx->world > 1 || ctx->nccl_comm || getenv("SK_FORCE_BOX_EXCHANGE") != nullptr;
     if (P->box_exchange && (st = alloc((void**)&P->box_buf, sizeof(double) * std::max(P->box_size, 1LL))))
         return fail(st);
+    P->fftconv2 = !P->box_exchange && !P->pruned && fftconv2_supported(d, P->n, P->N);
+    if (P->fftconv2) {
+        std::vector<double> tw((size_t)P->n);
+        fftconv2_twiddles(P->n, tw.data());
+        if ((st = alloc((void**)&P->fc_tw, sizeof(double) * P->n))) return fail(st);
+        if (cudaMemcpyAsync(P->fc_tw, tw.data(), sizeof(double) * P->n, cudaMemcpyHostToDevice, s) != cudaSuccess ||
+            cudaStreamSynchronize(s) != cudaSuccess)
+            return fail(set_error(SK_ECUDA, "fftconv2 twiddles"));
+    }
     if ((st = alloc((void**)&P->red, sizeof(double) * 4096))) return fail(st);
     if ((st = alloc((void**)&P->red_out, sizeof(double) * 8192))) return fail(st);
     if ((st = alloc((void**)&P->flag, sizeof(int) * 16))) return fail(st);
@@ -886,6 +895,7 @@ int destroy_plan(Plan* P) {
     sk_free(P->w_sorted); sk_free(P->t_sorted);
     sk_free(P->a_s); sk_free(P->b_s); sk_free(P->u_s); sk_free(P->v_s);
     sk_free(P->red); sk_free(P->red_out); sk_free(P->flag); sk_free(P->box_buf); sk_free(P->det_acc);
+    sk_free(P->fc_tw);
     pinned_release(P->host_red);
     delete (WinPoly*)P->winpoly;
     delete P;
@@ -898,7 +908,10 @@ int apply_sorted(Plan& P, int transpose, int kernel, const double* w_sorted, dou
     cudaStream_t s = P.ctx->stream;
     const int src = transpose ? 0 : 1, dst = transpose ? 1 : 0;
     prof_begin(ST_SPREAD, s);
-    SK_TRY(launch_spread(P, src, w_sorted, P.grid, s));   // writes every grid cell
+    GridAcc ga;
+    unsigned* slot = nullptr;
+    if (P.fftconv2) SK_TRY(launch_spread(P, src, w_sorted, P.grid, s, &ga, &slot));   // conversion in K1
+    else SK_TRY(launch_spread(P, src, w_sorted, P.grid, s));   // writes every grid cell
     prof_end(ST_SPREAD, s);
     if (P.box_exchange) {
         // a3: sum the partial grids of all ranks over the touched box only (pack, NCCL
@@ -911,7 +924,11 @@ int apply_sorted(Plan& P, int transpose, int kernel, const double* w_sorted, dou
         SK_TRY(launch_box_copy(P, P.grid, P.box_buf, 1, s));
         prof_end(ST_ALLREDUCE, s);
     }
-    if (P.pruned) {
+    if (P.fftconv2) {
+        prof_begin(ST_FFT_FWD, s);
+        SK_TRY(fftconv2_apply(P, kernel, ga, slot, s));
+        prof_end(ST_FFT_FWD, s);
+    } else if (P.pruned) {
         SK_TRY(pruned_fft_apply(P, kernel, s));
     } else {
         prof_begin(ST_FFT_FWD, s);

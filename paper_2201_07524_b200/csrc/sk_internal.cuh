@@ -131,6 +131,10 @@ struct Plan {
     double* pr_A = nullptr;
     void *pr_Z = nullptr, *pr_Y = nullptr, *pr_X = nullptr;   // cufftDoubleComplex buffers
     cufftHandle pr_fz = 0, pr_iz = 0, pr_y = 0, pr_x = 0;
+    // d = 2 shared-memory FFT convolution (fftconv2.cu): replaces D2Z / multiply / Z2D and the
+    // deterministic conversion; twiddle table [n/2] complex
+    bool fftconv2 = false;
+    double* fc_tw = nullptr;
     // scratch
     double* w_sorted = nullptr;   // [max count]
     double* t_sorted = nullptr;   // [max count]
@@ -281,7 +285,13 @@ int launch_gather_coords(Plan& P, const double* pts, const int* perm, long long 
                          cudaStream_t s);   // rescales the caller's points in sorted order
 int launch_tile_offsets(const int* sorted_keys, long long count, int ntiles, int* tile_start,
                         cudaStream_t s);
-int launch_spread(Plan& P, int side, const double* w_sorted, double* grid, cudaStream_t s);
+// keep != nullptr: the deterministic conversion is left to the caller (fftconv2_apply), which
+// gets the accumulator descriptor and the source vector's bound slot
+int launch_spread(Plan& P, int side, const double* w_sorted, double* grid, cudaStream_t s,
+                  GridAcc* keep = nullptr, unsigned** keep_slot = nullptr);
+bool fftconv2_supported(int d, int n, int N);
+void fftconv2_twiddles(int n, double* out);
+int fftconv2_apply(Plan& P, int kernel, const GridAcc& ga, unsigned* slot, cudaStream_t s);
 int launch_taps(Plan& P, int side, cudaStream_t s);
 int launch_interp(Plan& P, int side, const double* grid, double* t_sorted, cudaStream_t s,
                   const FusedUpd& fu = FusedUpd());   // fu.x only on the DMMA interps (P.dmma)

@@ -975,3 +975,44 @@ def test_deterministic_emulated_two_ranks_reproducible(capi):
         P.close()
     assert out[0][0] == out[1][0] and np.array_equal(out[0][1], out[1][1]) and np.array_equal(out[0][2], out[1][2])
     c2.close()
+
+
+@pytest.mark.parametrize("N,sigma,det", [(16, 4.0, "1"), (32, 2.0, "1"), (64, 2.0, "0"), (64, 2.0, "1"),
+                                         (128, 2.0, "1"), (128, 4.0, "0"), (256, 4.0, "1"), (48, 2.0, "1")])
+def test_fftconv2_equals_cufft_path(capi, ctx, N, sigma, det):
+    """d = 2 shared-memory FFT convolution (fftconv2.cu: box rows -> band columns x D -> box rows,
+    the deterministic conversion fused into the first pass) against the cuFFT D2Z / multiply /
+    Z2D path of the same plan (SK_NO_FFTCONV2), both kernels and directions, deterministic and
+    atomic spreads, grid edges n = 64 .. 1024 (48 x 2 = 96 is not a power of two: both plans take
+    cuFFT); and against the oracle's exact-NDFT statement of the method where it is
+    cheap. Clustered x and a narrow y keep the touched box smaller than the grid."""
+    rng = np.random.default_rng(N + int(10 * sigma))
+    n, m = 3001, 2503
+    x = np.concatenate([0.3 + 0.05 * rng.normal(size=(n // 2, 2)), rng.random((n - n // 2, 2))])
+    y = 0.2 + 0.6 * rng.random((m, 2)) ** 1.5
+    wy, wx = rng.random(m), rng.random(n)
+    lam = 0.5 * N
+    old = {k: os.environ.get(k) for k in ("SK_DETERMINISTIC", "SK_NO_FFTCONV2")}
+    res = {}
+    try:
+        os.environ["SK_DETERMINISTIC"] = det
+        for path in ("fc", "cufft"):
+            if path == "cufft":
+                os.environ["SK_NO_FFTCONV2"] = "1"
+            P = capi.Plan(ctx, dev(x), dev(y), lam, N, sigma, 8)
+            res[path] = [capi.fastsum_apply(P, dev(w), tr, k).cpu().numpy()
+                         for k in (0, 1) for tr, w in ((0, wy), (1, wx))]
+            P.close()
+    finally:
+        for k, v in old.items():
+            if v is None:
+                os.environ.pop(k, None)
+            else:
+                os.environ[k] = v
+    for i, (a, b) in enumerate(zip(res["fc"], res["cufft"])):
+        assert rel_linf(a, b) <= 1e-13, (N, sigma, det, i, rel_linf(a, b))
+    if N <= 64:
+        for i, (k, tr) in enumerate([(0, 0), (0, 1), (1, 0), (1, 1)]):
+            xs, ys, w = (x, y, wy) if tr == 0 else (y, x, wx)
+            ref = nfft_ref.fastsum_ndft(xs, ys, w, lam, N, 1 / 16, 8, k)
+            assert rel_linf(res["fc"][i], ref) <= 2e-13, (N, sigma, k, tr, rel_linf(res["fc"][i], ref))

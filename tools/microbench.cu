@@ -186,6 +186,32 @@ __global__ void __launch_bounds__(128, 2) spreadmix_kernel(double* out, int iter
     out[blockIdx.x * blockDim.x + threadIdx.x] = s;
 }
 
+// the 28-tile spread3 mix (dmma3.cuh spread3_t28_ksteps): per warp and k-step 14 DMMA.8x8x4 into
+// 14 accumulators fed by 16 DMUL products; useful work 1728 of 1792 issued FMAs per node
+template <int MINB>
+__global__ void __launch_bounds__(192, MINB) t28mix_kernel(double* out, int iters) {
+    double acc[14][2];
+#pragma unroll
+    for (int j = 0; j < 14; ++j) acc[j][0] = acc[j][1] = 0.0;
+    double y = 1.0 + threadIdx.x * 1e-6, z = 1.0 - threadIdx.x * 1e-6, w = 1e-3;
+    for (int it = 0; it < iters; ++it) {
+        const double a0 = w * y, a1 = w * z;
+#pragma unroll
+        for (int j = 0; j < 14; ++j) {
+            const double b = j < 9 ? y * (z + j) : (z + j);
+            const double a = j < 9 ? a0 : a1 * (y + j);
+            asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+                : "+d"(acc[j][0]), "+d"(acc[j][1]) : "d"(a), "d"(b));
+        }
+        y *= 0.9999999;
+        z *= 1.0000001;
+    }
+    double s = 0;
+#pragma unroll
+    for (int j = 0; j < 14; ++j) s += acc[j][0] + acc[j][1];
+    out[blockIdx.x * blockDim.x + threadIdx.x] = s;
+}
+
 // operand-order variants of the spread mix: ORDER 0 = (a0,b_j),(a1,b_j) pairs; 1 = all a0 then
 // all a1 (A reused, B changes every DMMA); 2 = b_j varies but computed without DMUL chains
 template <int ORDER>
@@ -440,6 +466,12 @@ int main() {
         printf("spread mix m16n8k4 without DMUL: %.2f TFLOP/s issued\n", fl / ms / 1e9);
         ms = timeit([&] { spreadmix_grouped_kernel<<<g2, 128>>>(out, iters); });
         printf("spread mix, 18 DMUL grouped in one asm block: %.2f TFLOP/s issued, USEFUL %.2f\n", fl / ms / 1e9, 0.75 * fl / ms / 1e9);
+        {   // 28-tile cover: 14 DMMA + 16 DMUL per warp and k-step, 12 warps/SM (2 CTAs x 6 warps)
+            const double fl28 = 2.0 * 256 * 14 * (double)iters * g2 * 6;
+            ms = timeit([&] { t28mix_kernel<2><<<g2, 192>>>(out, iters); });
+            printf("t28 mix (14 DMMA + 16 DMUL, 12 warps/SM): %.2f TFLOP/s issued, USEFUL %.2f\n", fl28 / ms / 1e9,
+                   fl28 * 1728.0 / 1792.0 / ms / 1e9);
+        }
         double flu = 2.0 * 12 * 8 * 18 * 4 * (double)iters * g2 * 4;
         ms = timeit([&] { hybrid_kernel<18><<<g2, 128>>>(out, iters); });
         printf("hybrid 18 DMMA + 72 DFMA + 22 DMUL, 8 warps/SM, USEFUL: %.2f TFLOP/s\n", flu / ms / 1e9);
