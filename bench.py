@@ -38,6 +38,7 @@ SMI_MS = int(os.environ.get("SK_BENCH_SMI_MS", "200"))          # clock sampling
 STAGE_PROFILE = os.environ.get("SK_BENCH_STAGE_PROFILE", "1") != "0"
 FP64_FMA_PER_CLK_PER_SM = 64      # B200 FP64 vector rate
 N_SM = 148
+MIX_CEILING = {"spread": 31.4, "interp": 31.2}   # TF/s, DESIGN.md §6
 
 
 def parse():
@@ -467,15 +468,16 @@ def main():
                      "peak_source": f"{N_SM} SMs x {FP64_FMA_PER_CLK_PER_SM} FP64 FMA/clk x 2 x sm_max_mhz "
                                     f"{pk.get('sm_max_mhz')} (DESIGN.md)",
                      "hbm_frac": bytes_alg / (avg_ms * 1e-3) / (pk["hbm_gbs"] * 1e9),
-                     # what the kernel's FP64 instruction mix allows on this chip (microbenchmarks of
-                     # the same mix with operands in shared memory): the spread pads the
-                     # 12-tap axis to 16 DMMA rows and forms 144 DMUL products per node, the interp
-                     # pays one DFMA per E value; d = 3, m_w = 6 only
-                     "mix_ceiling_tflops": ({"spread": 22.3, "interp": 31.2}.get(dom)
-                                            if (cfg.d == 3 and cfg.m_w == 6) else None),
-                     "frac_of_mix_ceiling": ((achieved / {"spread": 22.3, "interp": 31.2}[dom])
-                                             if (cfg.d == 3 and cfg.m_w == 6) else None),
-                     "mix_ceiling_source": "profiles/r1_microbench.txt, profiles/r1_interp_mix.txt",
+                     # what the kernel's FP64 instruction mix allows on this chip: the
+                     # spread's 28-tile m8n8k4 cover issues 1792 DMMA FMAs + 256 DMUL lane products per
+                     # node for 1728 useful FMAs on the one shared FP64 pipe (pipe model: 0.844 x
+                     # 37.2 TF); the interp pays one DFMA per E value (microbenchmark of the same mix);
+                     # d = 3, m_w = 6 only
+                     "mix_ceiling_tflops": (MIX_CEILING.get(dom) if (cfg.d == 3 and cfg.m_w == 6) else None),
+                     "frac_of_mix_ceiling": ((achieved / MIX_CEILING[dom])
+                                             if (cfg.d == 3 and cfg.m_w == 6 and dom in MIX_CEILING) else None),
+                     "mix_ceiling_source": "spread: pipe model 1728 / (1792 + 256) x 37.2 TF (DESIGN.md §6); "
+                                           "interp: profiles/r1_interp_mix.txt (measured)",
                      "avg_launch_ms": avg_ms,
                      "timing": "CUDA events around the kernel's stage on the library stream, averaged "
                                "over its launches in the profiled step (stage_profile)"},

@@ -27,6 +27,10 @@ int set_error(int code, const std::string& msg) {
     return code;
 }
 void count_launch(long long k) { g_launches += k; }
+bool pdl_enabled() {
+    static const bool on = getenv("SK_NO_PDL") == nullptr;
+    return on;
+}
 
 // ---------------------------------------------------------------- caching device allocator
 // Plans allocate tens of GB (c5: sorted nodes, 52 GB of window taps, grids); cudaMalloc /

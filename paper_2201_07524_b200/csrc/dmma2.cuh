@@ -90,6 +90,8 @@ interp2_dmma_kernel(const CellBatch* __restrict__ batches, int nbatches, const d
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int g = lane >> 2, q = lane & 3;
     const int gw = blockIdx.x * C::NWARP + warp, nw = gridDim.x * C::NWARP;
+    pdl_trigger();
+    pdl_wait();   // the grid (and the fused update's p, x) come from the preceding kernels
     for (int bi = gw; bi < nbatches; bi += nw) {
         const CellBatch B = batches[bi];
         const int ntn = (B.count + 7) >> 3;   // warp-uniform
@@ -113,6 +115,8 @@ spread2_dmma_kernel(const SpreadItem* __restrict__ items, int nitems, const Cell
                     const double* __restrict__ taps, const double* __restrict__ w, const GridAcc ga) {
     using C = Spread2Cfg;
     const int n = ga.n;
+    pdl_trigger();
+    pdl_wait();   // w, its bound slot and the cleared accumulator come from the preceding kernels
     const double gscale = grid_scale(ga);
     constexpr int W = C::W, S = C::S, m = W / 2, TS = C::TS;
     extern __shared__ __align__(16) double smem[];

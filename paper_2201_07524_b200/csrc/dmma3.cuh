@@ -324,6 +324,8 @@ interp3_dmma_kernel(const CellBatch* __restrict__ batches, int nbatches, const d
     const long long ry[3] = {STAGE ? g * W : (long long)g * n, STAGE ? ty1 * W : (long long)ty1 * n,
                              STAGE ? (4 + g) * W : (long long)(4 + g) * n};
 
+    pdl_trigger();
+    pdl_wait();   // the grid (and the fused update's p, x) come from the preceding kernels
     CellBatch Bnext = b_lo < b_hi ? batches[b_lo] : CellBatch{0, 0, 0, 0};
     for (int bi = b_lo; bi < b_hi; ++bi) {
         const CellBatch B = Bnext;   // descriptor loaded one batch ahead
@@ -531,6 +533,8 @@ spread3_tmapad_kernel(const SpreadItem* __restrict__ items, int nitems, const Ce
     double* TB0 = base + 2 + C::REGP;
     double* WB0 = TB0 + 2 * C::TBUF;
     const int n = ga.n, ns = n / 2;
+    pdl_trigger();
+    pdl_wait();   // w, its bound slot and the cleared accumulator come from the preceding kernels
     const double gscale = grid_scale(ga);
     const int gp = blockIdx.x * C::NPAIR + pair, np = gridDim.x * C::NPAIR;
     const int z1 = (8 + g) % W;

@@ -75,6 +75,8 @@ __global__ void __launch_bounds__(T) fc2_rows_fwd_kernel(const FcGeom g, const G
     __shared__ double2 buf[2][NN];
     __shared__ double2 tws[NN / 2];
     load_twiddles<NN, T>(tws, tw);
+    pdl_trigger();
+    pdl_wait();
     const int r = blockIdx.x;   // box row
     const int i0 = g.lo0 + r;
     double inv = 1.0;
@@ -125,6 +127,8 @@ __global__ void __launch_bounds__(T) fc2_cols_kernel(const FcGeom g, const doubl
     __shared__ double2 buf[2][NN];
     __shared__ double2 tws[NN / 2];
     load_twiddles<NN, T>(tws, tw);
+    pdl_trigger();
+    pdl_wait();
     const int kl = blockIdx.x;
     for (int i = threadIdx.x; i < NN; i += T) {
         const int ib = i - g.lo0;
@@ -154,6 +158,8 @@ __global__ void __launch_bounds__(T) fc2_rows_inv_kernel(const FcGeom g, const d
     __shared__ double2 buf[2][NN];
     __shared__ double2 tws[NN / 2];
     load_twiddles<NN, T>(tws, tw);
+    pdl_trigger();
+    pdl_wait();
     const int i0 = g.lo0 + blockIdx.x;
     const double2* row = S + (long long)i0 * g.ld;
     for (int k = threadIdx.x; k < NN; k += T) {
@@ -171,11 +177,11 @@ template <int NN>
 int run(const FcGeom& g, const GridAcc& ga, const double* grid_in, const double* Dk, const double2* tw,
         double2* S, double* grid_out, unsigned* done, unsigned* slot, cudaStream_t s) {
     constexpr int T = NN / 2 < 256 ? NN / 2 : 256;
-    fc2_rows_fwd_kernel<NN, T><<<g.bn0, T, 0, s>>>(g, ga, grid_in, tw, S, done, slot);
-    fc2_cols_kernel<NN, T><<<g.h + 1, T, 0, s>>>(g, Dk, tw, S);
-    fc2_rows_inv_kernel<NN, T><<<g.bn0, T, 0, s>>>(g, tw, S, grid_out);
+    cudaError_t e = launch_pdl(fc2_rows_fwd_kernel<NN, T>, g.bn0, T, 0, s, g, ga, grid_in, tw, S, done, slot);
+    if (e == cudaSuccess) e = launch_pdl(fc2_cols_kernel<NN, T>, g.h + 1, T, 0, s, g, Dk, tw, S);
+    if (e == cudaSuccess) e = launch_pdl(fc2_rows_inv_kernel<NN, T>, g.bn0, T, 0, s, g, tw, S, grid_out);
     count_launch(3);
-    const cudaError_t e = cudaGetLastError();
+    if (e == cudaSuccess) e = cudaGetLastError();
     if (e != cudaSuccess) return set_error(SK_ECUDA, std::string("fftconv2 launch: ") + cudaGetErrorString(e));
     return SK_OK;
 }

@@ -704,10 +704,11 @@ int build_plan(Ctx* ctx, Plan** out, int d, const double* x, long long n, const 
         P->dmma = ((P->tiled && m_w == 6) || (d == 2 && m_w == 8 && err >= 0.0 && err <= 1e-14)) &&
                   fast && getenv("SK_NO_DMMA") == nullptr && getenv("SK_FORCE_V1") == nullptr;
         if (P->dmma && d == 2) P->tiled = false;
-        // d = 3 spread: the padded DMMA spread on TMA-fed warp pairs, x-pair segments for
-        // sparse sets (SK_NO_XPAIRS=1 disables them)
+        // d = 3 spread: the DMMA spread on TMA-fed warp pairs. x-pair segments for sparse sets
+        // (16-row padded tiles) are opt-in (SK_XPAIRS=1): the 28-tile cover without them is faster
+        // on c3 (924 -> 945 it/s, tools/ab_env.sh)
         P->spread_tmapad = P->dmma && d == 3;
-        P->spread_xpairs = P->dmma && d == 3 && getenv("SK_NO_XPAIRS") == nullptr;
+        P->spread_xpairs = P->dmma && d == 3 && getenv("SK_XPAIRS") != nullptr;
     }
     {   // phi(0)^d bounds one node's spread contribution |w| prod_a phi (deterministic mode)
         const double bm = P->win.beta * m_w;

@@ -36,6 +36,38 @@ int set_error(int code, const std::string& msg);
 
 void count_launch(long long k = 1);
 
+// Programmatic dependent launch (sm_90+) on the per-apply kernel chain (spread -> FFT stages ->
+// interp): a kernel launched with launch_pdl may be scheduled while its predecessor in the stream
+// still runs; it must call pdl_wait() before touching memory the predecessor writes or reads, and
+// triggers its own successor's launch with pdl_trigger(). Kernels launched without the attribute
+// see both as no-ops. SK_NO_PDL=1 launches plainly (A/B).
+bool pdl_enabled();
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                              Args&&... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
+}
+#ifdef __CUDACC__
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+#ifndef SK_PDL_EARLY
+#define SK_PDL_EARLY 0   // 1: trigger at kernel start (measured slower on c2 / images: the waiting
+                         // successor CTAs take SM slots); 0: implicit trigger at block exit
+#endif
+__device__ __forceinline__ void pdl_trigger() {
+    if (SK_PDL_EARLY) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+#endif
+
 // Caching device allocator (api.cu): stream-ordered reuse of freed blocks.
 int dev_alloc(void** out, size_t bytes, cudaStream_t s);
 void dev_free(void* p, cudaStream_t s);

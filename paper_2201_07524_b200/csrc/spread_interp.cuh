@@ -255,9 +255,10 @@ inline int spread_dispatch(Plan& P, const NodeSet& S, const double* w, const Gri
             const bool cta = S.count <= cta_nodes;
             const auto kern = cta ? spread2_dmma_kernel<true> : spread2_dmma_kernel<false>;
             const int g = persistent_grid(kern, C::NT, C::SMEM_BYTES, cta ? S.nsitems : (S.nsitems + C::NWARP - 1) / C::NWARP);
-            kern<<<g, C::NT, C::SMEM_BYTES, s>>>((const SpreadItem*)S.sitems, S.nsitems, (const CellBatch*)S.segs,
-                                                 S.taps, w, ga);
+            const cudaError_t le = launch_pdl(kern, g, C::NT, C::SMEM_BYTES, s, (const SpreadItem*)S.sitems,
+                                              S.nsitems, (const CellBatch*)S.segs, S.taps, w, ga);
             count_launch();
+            if (le != cudaSuccess) return set_error(SK_ECUDA, std::string("spread2_dmma: ") + cudaGetErrorString(le));
         }
         cudaError_t e = cudaGetLastError();
         if (e != cudaSuccess) return set_error(SK_ECUDA, std::string("spread2_dmma: ") + cudaGetErrorString(e));
@@ -281,8 +282,10 @@ inline int spread_dispatch(Plan& P, const NodeSet& S, const double* w, const Gri
             const int nt = S.seg_dense ? SpreadTPCfgDense::NT : SpreadTPCfgSparse::NT;
             const size_t sm = S.seg_dense ? SpreadTPCfgDense::SMEM_BYTES : SpreadTPCfgSparse::SMEM_BYTES;
             const int g = persistent_grid(kern, nt, sm, (S.nsitems + np - 1) / np);
-            kern<<<g, nt, sm, s>>>((const SpreadItem*)S.sitems, S.nsitems, (const CellBatch*)S.segs, S.taps, w, ga);
+            const cudaError_t le = launch_pdl(kern, g, nt, sm, s, (const SpreadItem*)S.sitems, S.nsitems,
+                                              (const CellBatch*)S.segs, S.taps, w, ga);
             count_launch();
+            if (le != cudaSuccess) return set_error(SK_ECUDA, std::string("spread3_tmapad: ") + cudaGetErrorString(le));
         }
         cudaError_t e = cudaGetLastError();
         if (e != cudaSuccess) return set_error(SK_ECUDA, std::string("spread3_tmapad: ") + cudaGetErrorString(e));
@@ -335,8 +338,10 @@ inline int interp_dispatch(Plan& P, const NodeSet& S, const double* grid, double
         }
         if (S.nbatches > 0) {
             const int g = persistent_grid(interp2_dmma_kernel, C::NT, C::SMEM_BYTES, (S.nbatches + C::NWARP - 1) / C::NWARP);
-            interp2_dmma_kernel<<<g, C::NT, C::SMEM_BYTES, s>>>((const CellBatch*)S.batches, S.nbatches, S.taps, grid, P.n, t, fu);
+            const cudaError_t le = launch_pdl(interp2_dmma_kernel, g, C::NT, C::SMEM_BYTES, s,
+                                              (const CellBatch*)S.batches, S.nbatches, S.taps, grid, P.n, t, fu);
             count_launch();
+            if (le != cudaSuccess) return set_error(SK_ECUDA, std::string("interp2_dmma: ") + cudaGetErrorString(le));
         }
         cudaError_t e = cudaGetLastError();
         if (e != cudaSuccess) return set_error(SK_ECUDA, std::string("interp2_dmma: ") + cudaGetErrorString(e));
@@ -355,8 +360,10 @@ inline int interp_dispatch(Plan& P, const NodeSet& S, const double* grid, double
             const auto kern = stage ? interp3_dmma_kernel<true> : interp3_dmma_kernel<false>;
             const size_t sm = stage ? C::SMEM_BYTES : C::SMEM_BYTES_NOSTAGE;
             const int g = persistent_grid(kern, C::NT, sm, (S.nbatches + C::NWARP - 1) / C::NWARP);
-            kern<<<g, C::NT, sm, s>>>((const CellBatch*)S.batches, S.nbatches, S.taps, grid, P.n, t, fu);
+            const cudaError_t le = launch_pdl(kern, g, C::NT, sm, s, (const CellBatch*)S.batches, S.nbatches, S.taps,
+                                              grid, P.n, t, fu);
             count_launch();
+            if (le != cudaSuccess) return set_error(SK_ECUDA, std::string("interp3_dmma: ") + cudaGetErrorString(le));
         }
         cudaError_t e = cudaGetLastError();
         if (e != cudaSuccess) return set_error(SK_ECUDA, std::string("interp3_dmma: ") + cudaGetErrorString(e));

@@ -194,11 +194,11 @@ def _variant_sets():
 
 
 @pytest.mark.parametrize("env", [{}, {"SK_SEG_DENSE_MIN": "0"}, {"SK_SEG_DENSE_MIN": "1000000000"},
-                                 {"SK_NO_XPAIRS": "1"}, {"SK_NO_DMMA": "1"}, {"SK_DETERMINISTIC": "1"},
+                                 {"SK_XPAIRS": "1"}, {"SK_NO_DMMA": "1"}, {"SK_DETERMINISTIC": "1"},
                                  {"SK_DETERMINISTIC": "1", "SK_NO_DMMA": "1"}, {"SK_DETERMINISTIC": "0"}])
 def test_kernel_variants_match_gridding_definition(capi, ctx, env):
     """Every d = 3 spread/interp variant the plan can select (default shapes, forced dense or
-    32-node segments, no x-pairs, the vector path without tensor cores, the deterministic
+    32-node segments, x-pair segments, the vector path without tensor cores, the deterministic
     fixed-point accumulation on both) on dense, mid and sparse cells against the gridding
     definition."""
     sets = _variant_sets()
@@ -942,12 +942,20 @@ def test_deterministic_spread_properties(capi, ctx):
         mk = lambda: capi.Plan(ctx, dev(x), dev(y), 20.0, N, 2.0, m_w)  # noqa: E731
         Pd = _with_env({"SK_DETERMINISTIC": "1"}, mk)
         Pa = _with_env({"SK_DETERMINISTIC": "0"}, mk)
+        Px = _with_env({"SK_DETERMINISTIC": "1", "SK_XPAIRS": "1"}, mk) if d == 3 else None
         for w in (rng.random(cnt), rng.random(cnt) * 10.0 ** rng.uniform(-30, 30, cnt)):
             g1 = capi.nfft_spread(Pd, 0, dev(w)).cpu().numpy()
             g2 = capi.nfft_spread(Pd, 0, dev(w)).cpu().numpy()
             ga = capi.nfft_spread(Pa, 0, dev(w)).cpu().numpy()
             assert np.array_equal(g1, g2), d
             assert np.abs(g1 - ga).max() <= 1e-14 * np.abs(ga).max(), (d, np.abs(g1 - ga).max() / np.abs(ga).max())
+            if Px is not None:   # x-pair segments (opt-in)
+                gx1 = capi.nfft_spread(Px, 0, dev(w)).cpu().numpy()
+                gx2 = capi.nfft_spread(Px, 0, dev(w)).cpu().numpy()
+                assert np.array_equal(gx1, gx2)
+                assert np.abs(gx1 - ga).max() <= 1e-14 * np.abs(ga).max()
+        if Px is not None:
+            Px.close()
         assert not np.any(capi.nfft_spread(Pd, 0, dev(np.zeros(cnt))).cpu().numpy())
         wn = rng.random(cnt)
         wn[cnt // 2] = np.nan
