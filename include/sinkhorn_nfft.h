@@ -113,10 +113,13 @@ int fastsum_plan(sk_ctx_t ctx, sk_plan_t* plan, int d,
  *   t_i += sum over |x'_i - y'_j| < a of w_j (K - K_I)(|x'_i - y'_j|)
  * (direct sum over the source tiles around each target). The divergence kernel c K uses
  * c = |x - y| in original units. r = 1 runs the same spread / interp kernels as r = 2.
- * r = 1 plans are single-rank: the near field needs every source within the radius of a
- * target, which a sharded source set does not hold (an all-gather of the sources is not built).
+ * Across ranks (world_size > 1) the near field of a target needs every source within the radius,
+ * wherever it lives: the plan all-gathers each side's scaled coordinates once (ncclBroadcast per
+ * rank, rank-major) and every r = 1 fast summation all-gathers the source weights; the far field
+ * stays the grid all-reduce. Memory: every rank holds all nodes' coordinates for the near field.
  * Errors: SK_EINVAL for r not in {1, 2}, near_cells < 1, p_smooth > 8 (r = 1; the monomial K_I system is ill-conditioned beyond),
- * a >= 1/2 - eps_B, or r = 1 on a context with world_size > 1; otherwise as fastsum_plan. */
+ * a >= 1/2 - eps_B, or r = 1 with more than 64 ranks; SK_ENCCL if libnccl lacks ncclBroadcast;
+ * otherwise as fastsum_plan. */
 typedef struct {
     double lambda;
     int    r;             /* 1 or 2 */

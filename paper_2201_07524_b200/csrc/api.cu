@@ -120,6 +120,9 @@ struct NcclApi {
                               cudaStream_t) = nullptr;
     ncclResult_t (*commDestroy)(ncclComm_t) = nullptr;
     const char* (*errStr)(ncclResult_t) = nullptr;
+    ncclResult_t (*broadcast)(const void*, void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*groupStart)() = nullptr;
+    ncclResult_t (*groupEnd)() = nullptr;
 };
 static NcclApi g_nccl;
 static std::mutex g_nccl_mu;
@@ -135,6 +138,9 @@ static int nccl_load() {
     g_nccl.allReduce = (decltype(g_nccl.allReduce))dlsym(h, "ncclAllReduce");
     g_nccl.commDestroy = (decltype(g_nccl.commDestroy))dlsym(h, "ncclCommDestroy");
     g_nccl.errStr = (decltype(g_nccl.errStr))dlsym(h, "ncclGetErrorString");
+    g_nccl.broadcast = (decltype(g_nccl.broadcast))dlsym(h, "ncclBroadcast");
+    g_nccl.groupStart = (decltype(g_nccl.groupStart))dlsym(h, "ncclGroupStart");
+    g_nccl.groupEnd = (decltype(g_nccl.groupEnd))dlsym(h, "ncclGroupEnd");
     if (!g_nccl.getUniqueId || !g_nccl.commInitRank || !g_nccl.allReduce || !g_nccl.commDestroy)
         return set_error(SK_ENCCL, "libnccl is missing a required symbol");
     g_nccl.loaded = true;
@@ -161,6 +167,52 @@ int allreduce_sum(Ctx* c, double* buf, long long count) {
                              c->stream));
     count_launch();
     return SK_OK;
+}
+
+int allgather_concat(Ctx* c, const double* local, long long count, const long long* counts, double* out) {
+    if (c->emulated || !c->nccl_comm) {   // identical shards (emulated) or one rank
+        const int copies = c->emulated ? c->world : 1;
+        for (int r = 0; r < copies; ++r)
+            if (count > 0)
+                SK_CUDA(cudaMemcpyAsync(out + (long long)r * count, local, sizeof(double) * count,
+                                        cudaMemcpyDeviceToDevice, c->stream));
+        return SK_OK;
+    }
+    if (!g_nccl.broadcast || !g_nccl.groupStart || !g_nccl.groupEnd)
+        return set_error(SK_ENCCL, "libnccl lacks ncclBroadcast / ncclGroupStart / ncclGroupEnd");
+    long long off = 0;
+    SK_NCCL(g_nccl.groupStart());
+    for (int r = 0; r < c->world; ++r) {
+        if (counts[r] > 0)
+            SK_NCCL(g_nccl.broadcast(r == c->rank ? (const void*)local : (const void*)(out + off), out + off,
+                                     (size_t)counts[r], ncclFloat64, r, (ncclComm_t)c->nccl_comm, c->stream));
+        off += counts[r];
+    }
+    SK_NCCL(g_nccl.groupEnd());
+    count_launch();
+    return SK_OK;
+}
+
+int gather_counts(Ctx* c, long long local, long long* counts) {
+    if (c->world > kMaxRanks) return set_error(SK_EINVAL, "r = 1 across ranks: at most 64 ranks");
+    if (c->emulated || !c->nccl_comm) {
+        for (int r = 0; r < c->world; ++r) counts[r] = local;
+        return SK_OK;
+    }
+    std::vector<double> h((size_t)c->world, 0.0);
+    h[(size_t)c->rank] = (double)local;
+    double* d = nullptr;
+    SK_TRY(dev_alloc((void**)&d, sizeof(double) * c->world, c->stream));
+    int st = SK_OK;
+    if (cudaMemcpyAsync(d, h.data(), sizeof(double) * c->world, cudaMemcpyHostToDevice, c->stream) != cudaSuccess)
+        st = set_error(SK_ECUDA, "gather_counts copy");
+    if (!st) st = allreduce_sum(c, d, c->world);
+    if (!st && (cudaMemcpyAsync(h.data(), d, sizeof(double) * c->world, cudaMemcpyDeviceToHost, c->stream) != cudaSuccess ||
+                cudaStreamSynchronize(c->stream) != cudaSuccess))
+        st = set_error(SK_ECUDA, "gather_counts copy back");
+    dev_free(d, c->stream);
+    for (int r = 0; r < c->world && !st; ++r) counts[r] = (long long)llround(h[(size_t)r]);
+    return st;
 }
 
 int allreduce_minmax(Ctx* c, double* mins, double* maxs, int count) {

@@ -1028,9 +1028,67 @@ __global__ void __launch_bounds__(kNearWarps * 32, 2) nearfield_tiled_kernel(
     }
 }
 
+// Near-field sources across ranks (plan.cu, build_near_global): sort keys of gathered grid
+// coordinates, the same keys a local side sorts by (d = 1 near field: position keys; otherwise
+// the tile index -- the near-field kernels read sources per tile)
+__global__ void near_key_kernel(const double* __restrict__ U, long long total, int d, int T, int tpa, int fine_shift,
+                                int fine_max, int* __restrict__ key, int* __restrict__ idx) {
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
+         i += (long long)gridDim.x * blockDim.x) {
+        int k = 0;
+        if (fine_shift) {
+            k = fine_key(U[i], fine_shift, fine_max);
+        } else {
+            for (int a = 0; a < d; ++a) {
+                int tc = (int)floor(U[a * total + i]) / T;
+                tc = tc < 0 ? 0 : (tc >= tpa ? tpa - 1 : tc);
+                k = k * tpa + tc;
+            }
+        }
+        key[i] = k;
+        idx[i] = (int)i;
+    }
+}
+
+int launch_near_keys(Plan& P, const double* U, long long total, int* key, int* idx, cudaStream_t s) {
+    if (total <= 0) return SK_OK;
+    const int fine_max = (int)(((long long)P.tiles_per_axis * P.tile_cells << P.fine_shift) - 1);
+    near_key_kernel<<<grid_for(total, 256), 256, 0, s>>>(U, total, P.d, P.tile_cells, P.tiles_per_axis, P.fine_shift,
+                                                          fine_max, key, idx);
+    SK_LAUNCH_CHECK();
+    return SK_OK;
+}
+
+__global__ void gather_rows_kernel(const double* __restrict__ in, long long in_ld, const int* __restrict__ perm,
+                                   long long count, int rows, double* __restrict__ out) {
+    for (long long j = blockIdx.x * (long long)blockDim.x + threadIdx.x; j < count;
+         j += (long long)gridDim.x * blockDim.x) {
+        const long long pj = perm[j];
+        for (int r = 0; r < rows; ++r) out[r * count + j] = in[r * in_ld + pj];
+    }
+}
+
+int launch_gather_rows(const double* in, long long in_ld, const int* perm, long long count, int rows, double* out,
+                       cudaStream_t s) {
+    if (count <= 0) return SK_OK;
+    gather_rows_kernel<<<grid_for(count, 256), 256, 0, s>>>(in, in_ld, perm, count, rows, out);
+    SK_LAUNCH_CHECK();
+    return SK_OK;
+}
+
 int launch_nearfield(Plan& P, int src, int dst, int kernel, const double* w_sorted, double* t_sorted,
                      cudaStream_t s) {
-    const NodeSet& S = P.side[src];
+    // across ranks the sources are every rank's nodes of the side (build_near_global), weights
+    // gathered into their order by the caller
+    NodeSet Sg;
+    const NodeSet* Sp = &P.side[src];
+    if (P.side[src].g_u) {
+        Sg.u = P.side[src].g_u;
+        Sg.count = P.side[src].g_total;
+        Sg.tile_start = P.side[src].g_tile_start;
+        Sp = &Sg;
+    }
+    const NodeSet& S = *Sp;
     const NodeSet& D = P.side[dst];
     if (D.count <= 0 || S.count <= 0) return SK_OK;
     NearParams np;

@@ -593,6 +593,55 @@ static int plan_side(Plan& P, int sidx, const double* pts, long long count, cuda
     return SK_OK;
 }
 
+// r = 1 across ranks (world > 1, an emulated world, or a one-rank NCCL communicator): the near
+// field of a target needs every source within the radius, wherever it lives. Each side's sorted
+// grid coordinates are all-gathered (rank-major concatenation), sorted by the key a local side
+// uses, and kept with the sorted -> concatenation map; each fast summation all-gathers the source
+// weights into the same order (apply_sorted). The far field is unchanged (grid all-reduce).
+static int build_near_global(Plan& P, NodeSet& S, cudaStream_t s) {
+    Ctx* C = P.ctx;
+    SK_TRY(gather_counts(C, S.count, S.g_counts));
+    long long total = 0;
+    for (int r = 0; r < C->world; ++r) total += S.g_counts[r];
+    S.g_total = total;
+    const int d = P.d;
+    SK_TRY(alloc((void**)&S.g_u, sizeof(double) * std::max(1LL, d * total)));
+    SK_TRY(alloc((void**)&S.g_tile_start, sizeof(int) * (S.ntiles + 1)));
+    SK_TRY(alloc((void**)&S.g_perm, sizeof(int) * std::max(1LL, total)));
+    SK_TRY(alloc((void**)&S.g_wcat, sizeof(double) * std::max(1LL, total)));
+    SK_TRY(alloc((void**)&S.g_w, sizeof(double) * std::max(1LL, total)));
+    double* ucat = nullptr;
+    int *key_in = nullptr, *idx_in = nullptr, *key_out = nullptr;
+    SK_TRY(alloc((void**)&ucat, sizeof(double) * std::max(1LL, d * total)));
+    SK_TRY(alloc((void**)&key_in, sizeof(int) * 3 * std::max(1LL, total)));
+    idx_in = key_in + std::max(1LL, total);
+    key_out = idx_in + std::max(1LL, total);
+    int st = SK_OK;
+    for (int a = 0; a < d && !st; ++a) st = allgather_concat(C, S.u + a * S.count, S.count, S.g_counts, ucat + a * total);
+    if (!st) st = launch_near_keys(P, ucat, total, key_in, idx_in, s);
+    if (!st && total > 0) {
+        const long long nkeys = P.fine_shift ? ((long long)S.ntiles * P.tile_cells << P.fine_shift) : S.ntiles;
+        int end_bit = 1;
+        while ((1LL << end_bit) < nkeys) ++end_bit;
+        size_t tb = 0;
+        cub::DeviceRadixSort::SortPairs(nullptr, tb, key_in, key_out, idx_in, S.g_perm, (int)total, 0, end_bit, s);
+        void* tmp = nullptr;
+        st = alloc(&tmp, tb);
+        if (!st && cub::DeviceRadixSort::SortPairs(tmp, tb, key_in, key_out, idx_in, S.g_perm, (int)total, 0, end_bit,
+                                                   s) != cudaSuccess)
+            st = set_error(SK_ECUDA, "near-field sort across ranks");
+        count_launch(4);
+        sk_free(tmp);
+        if (!st) st = launch_gather_rows(ucat, total, S.g_perm, total, d, S.g_u, s);
+        if (!st && P.fine_shift) st = launch_key_to_tile(P, key_out, total, s);
+    }
+    if (!st) st = launch_tile_offsets(key_out, total, S.ntiles, S.g_tile_start, s);
+    if (!st && cudaStreamSynchronize(s) != cudaSuccess) st = set_error(SK_ECUDA, "near-field gather sync");
+    sk_free(ucat);
+    sk_free(key_in);
+    return st;
+}
+
 static int plan_coefficients(Plan& P, cudaStream_t s) {
     const int M = 2 * P.N;  // sampling grid of K~_per (reading Q9)
     long long Md = 1, Bsz = 1;
@@ -639,9 +688,6 @@ int build_plan(Ctx* ctx, Plan** out, int d, const double* x, long long n, const 
     if (rpow != 1 && rpow != 2) return set_error(SK_EINVAL, "r must be 1 or 2");
     if (rpow == 1 && (near_cells < 1 || p > 8))
         return set_error(SK_EINVAL, "r = 1 needs near_cells >= 1 and p_smooth <= 8 (K_I monomial system)");
-    if (rpow == 1 && ctx && ctx->world > 1)
-        return set_error(SK_EINVAL, "r = 1 plans are single-rank (the near field needs every source near a "
-                                    "target; sharded sources are not gathered)");
     if (N < 2 || (N & 1)) return set_error(SK_EINVAL, "N must be even and >= 2");
     if (!(lambda > 0.0) || !isfinite(lambda)) return set_error(SK_EINVAL, "lambda must be > 0");
     if (m_w < 2 || m_w > 8) return set_error(SK_EINVAL, "m_w must be in [2, 8]");
@@ -815,6 +861,11 @@ int build_plan(Ctx* ctx, Plan** out, int d, const double* x, long long n, const 
     } else if (st) {
         return fail(st);
     }
+    if (rpow == 1 && (ctx->world > 1 || ctx->nccl_comm)) {   // every rank reaches this point together
+        st = build_near_global(*P, P->side[0], s);
+        if (!st) st = build_near_global(*P, P->side[1], s);
+        if (st) return fail(st);
+    }
     // ---- a1: coefficients
     if ((st = alloc((void**)&P->D[0], sizeof(double) * P->band_size))) return fail(st);
     if ((st = alloc((void**)&P->D[1], sizeof(double) * P->band_size))) return fail(st);
@@ -885,6 +936,7 @@ int destroy_plan(Plan* P) {
         NodeSet& S = P->side[sidx];
         sk_free(S.u); sk_free(S.perm); sk_free(S.cell_key); sk_free(S.tile_start); sk_free(S.items);
         sk_free(S.near_items);
+        sk_free(S.g_u); sk_free(S.g_tile_start); sk_free(S.g_perm); sk_free(S.g_wcat); sk_free(S.g_w);
         sk_free(S.batches); sk_free(S.segs); sk_free(S.sitems); sk_free(S.taps);
     }
     sk_free(P->grid); sk_free(P->spec);
@@ -946,7 +998,14 @@ int apply_sorted(Plan& P, int transpose, int kernel, const double* w_sorted, dou
     }
     auto nearfield = [&]() -> int {   // r = 1: the near-field correction, its own profiled stage
         prof_begin(ST_NEARFIELD, s);
-        SK_TRY(launch_nearfield(P, src, dst, kernel, w_sorted, t_sorted, s));
+        const double* wn = w_sorted;
+        const NodeSet& Ssrc = P.side[src];
+        if (Ssrc.g_u) {   // across ranks: every rank's source weights, in the gathered sources' order
+            SK_TRY(allgather_concat(P.ctx, w_sorted, Ssrc.count, Ssrc.g_counts, Ssrc.g_wcat));
+            SK_TRY(launch_gather_rows(Ssrc.g_wcat, Ssrc.g_total, Ssrc.g_perm, Ssrc.g_total, 1, Ssrc.g_w, s));
+            wn = Ssrc.g_w;
+        }
+        SK_TRY(launch_nearfield(P, src, dst, kernel, wn, t_sorted, s));
         prof_end(ST_NEARFIELD, s);
         return SK_OK;
     };

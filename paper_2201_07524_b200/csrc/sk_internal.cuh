@@ -12,6 +12,7 @@
 namespace sk {
 
 constexpr int kMaxD = 3;
+constexpr int kMaxRanks = 64;        // r = 1 across ranks: per-rank node counts kept on the host
 constexpr int kMaxW = 16;            // 2 * m_w taps per axis, m_w <= 8
 constexpr int kXPairMaxDensity = 96; // x-pair spread segments when nodes per cell < this
 constexpr double kLampDegenerate = 1e-16;   // lambda' of a zero-diameter geometry (reading Q6b)
@@ -107,6 +108,16 @@ struct NodeSet {
     // r = 1, d >= 2: near-field work list, <= kNearChunk consecutive targets of one tile row each
     void* near_items = nullptr;  // NearItem[n_near]
     int n_near = 0;
+    // r = 1 across ranks: every rank's nodes of this side as near-field sources (plan.cu,
+    // build_near_global): gathered grid coordinates sorted like a local side, the sorted ->
+    // concatenated (rank-major, each rank's sorted order) map, and per-apply weight buffers
+    long long g_total = 0;
+    double* g_u = nullptr;         // [d][g_total]
+    int* g_tile_start = nullptr;   // [ntiles + 1]
+    int* g_perm = nullptr;         // [g_total] position in the concatenation
+    double* g_wcat = nullptr;      // [g_total] all-gathered weights (concatenation)
+    double* g_w = nullptr;         // [g_total] weights in g_u's order
+    long long g_counts[kMaxRanks] = {};   // nodes per rank
 };
 // consecutive targets of tiles tile .. tile_last of one row along the last axis
 struct NearItem { int tile, start, count, tile_last; };
@@ -360,6 +371,9 @@ int build_plan(Ctx* ctx, Plan** out, int d, const double* x, long long n, const 
                long long m, double lambda, int N, double sigma, int m_w, double eps_B, int p,
                int rpow, int near_cells);
 int launch_key_to_tile(Plan& P, int* key, long long count, cudaStream_t s);
+int launch_near_keys(Plan& P, const double* U, long long total, int* key, int* idx, cudaStream_t s);
+int launch_gather_rows(const double* in, long long in_ld, const int* perm, long long count, int rows, double* out,
+                       cudaStream_t s);   // out[r][j] = in[r * in_ld + perm[j]]
 int launch_nearfield(Plan& P, int src, int dst, int kernel, const double* w_sorted, double* t_sorted,
                      cudaStream_t s);
 int destroy_plan(Plan* P);
@@ -384,6 +398,11 @@ void prof_harvest();
 
 // ---- comm (api.cu) ----
 int allreduce_sum(Ctx* c, double* buf, long long count);           // in-place, device
+// every rank's `count` local doubles, concatenated in rank order into out (counts[r] per rank);
+// emulated world: world copies of the local buffer; one rank: a copy
+int allgather_concat(Ctx* c, const double* local, long long count, const long long* counts, double* out);
+// per-rank counts of a local quantity (host), via a sum all-reduce of one slot per rank
+int gather_counts(Ctx* c, long long local, long long* counts);
 int allreduce_minmax(Ctx* c, double* mins, double* maxs, int count); // in-place, device
 
 }  // namespace sk

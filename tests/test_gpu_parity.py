@@ -614,19 +614,46 @@ def test_emulated_two_rank_world(capi):
         c.close()
 
 
-def test_r1_multi_rank_is_rejected(capi):
-    """r = 1 plans are single-rank (include/sinkhorn_nfft.h): with world_size > 1 the near field
-    would miss the other ranks' sources, so fastsum_plan_ex returns SK_EINVAL."""
+@pytest.mark.parametrize("d,N", [(1, 128), (2, 64), (3, 32)])
+def test_r1_across_ranks(capi, d, N):
+    """r = 1 across ranks (include/sinkhorn_nfft.h): the near field gathers every rank's sources.
+    SK_EMULATE_WORLD=2 (two identical shards, every atom duplicated): K_global v = 2 K v for both
+    kernels and directions, exactly as the far field's grid all-reduce; a one-rank NCCL
+    communicator runs the coordinate and weight all-gathers (ncclBroadcast) as the identity and
+    equals the communicator-free plan. d = 1 takes the position-sorted near-field kernel, d = 2, 3
+    the tiled one."""
+    rng = np.random.default_rng(40 + d)
+    n, m = 3000, 2500
+    x = 0.5 + 0.2 * rng.normal(size=(n, d))
+    y = rng.random((m, d))
+    wy, wx = rng.random(m), rng.random(n)
+    kw = dict(r=1, near_cells=16 if d < 3 else 6)
+
+    a, b = np.full(n, 1.0 / n), np.full(m, 1.0 / m)
+
+    def applies(c, scale=1.0):
+        P = capi.Plan(c, dev(x), dev(y), 20.0, N, 2.0, 8 if d < 3 else 6, **kw)
+        out = [capi.fastsum_apply(P, dev(w), tr, k).cpu().numpy() for k in (0, 1) for tr, w in ((0, wy), (1, wx))]
+        u, v, _ = capi.sinkhorn_run(P, dev(a * scale), dev(b * scale), 8)   # graph-captured gathers
+        out += [u.cpu().numpy(), v.cpu().numpy()]
+        P.close()
+        return out
+    c1 = capi.Context(0)
+    ref = applies(c1)
     os.environ["SK_EMULATE_WORLD"] = "2"
     try:
         c2 = capi.Context(0)
     finally:
         del os.environ["SK_EMULATE_WORLD"]
-    x = dev(np.random.default_rng(0).random((100, 1)))
-    with pytest.raises(capi.SkError) as e:
-        capi.Plan(c2, x, x, 20.0, 64, 2.0, 8, r=1, near_cells=16)
-    assert e.value.code == 1 and "single-rank" in str(e.value)
-    c2.close()
+    emu = applies(c2, 0.5)   # every atom duplicated with half its mass: U = u / 4, V = v
+    for i, (t2, t1) in enumerate(zip(emu[:4], ref[:4])):
+        assert rel_linf(t2, 2 * t1) <= 1e-13, (d, i, rel_linf(t2, 2 * t1))
+    assert rel_linf(4 * emu[4], ref[4]) <= 1e-11 and rel_linf(emu[5], ref[5]) <= 1e-11
+    c3 = capi.Context(0, 0, 1, capi.sk_nccl_unique_id())
+    for i, (t3, t1) in enumerate(zip(applies(c3), ref)):
+        assert rel_linf(t3, t1) <= (1e-13 if i < 4 else 1e-11), (d, i, rel_linf(t3, t1))
+    for c in (c3, c2, c1):
+        c.close()
 
 
 def test_nccl_one_rank_path(capi):
