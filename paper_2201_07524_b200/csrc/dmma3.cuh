@@ -403,7 +403,7 @@ struct SpreadTPCfg {
     static constexpr int REGP = REG + 1;
     static constexpr int TBUF = SEG * TS;
     static constexpr int WBUF = SEG + 4;
-    static constexpr int PAIR = 2 + REGP + 2 * TBUF + 2 * WBUF;
+    static constexpr int PAIR = 4 + REGP + 2 * TBUF + 2 * WBUF;   // 4 mbarrier words (full / empty)
     static constexpr size_t SMEM_BYTES = sizeof(double) * NPAIR * PAIR;
 };
 #ifndef SK_TP_NPAIR_SPARSE
@@ -507,6 +507,116 @@ __device__ __forceinline__ void spread3_t28_update(double (&acc)[14][2], double*
 #pragma unroll
                 for (int e = 0; e < 2; ++e) rc[tx1 * S * S + (8 + 2 * p + gy) * S + 8 + 2 * q + e] += acc[12 + p][e];
         }
+    }
+}
+
+// The 28-tile spread on a full / empty mbarrier pipeline (non-x-pair segments): the producer
+// (lane 0 of the pair's first warp) refills a segment buffer once both warps have released it
+// (empty[b], two arrivals) instead of a pair barrier at every segment, so neither warp waits for
+// its partner's k-loop; the next segment's descriptor is loaded one segment ahead. The warps meet
+// only before each cell's region update (consecutive cells' regions overlap: one barrier per cell
+// instead of per segment, c5 x: 56 segments per cell) and around the item flush (which also
+// zeroes the region for the next item).
+#ifndef SK_SPREAD3_PIPE
+#define SK_SPREAD3_PIPE 1
+#endif
+template <int SEG, int NPAIR_>
+__global__ void __launch_bounds__(64 * NPAIR_, 2)
+spread3_t28_kernel(const SpreadItem* __restrict__ items, int nitems, const CellBatch* __restrict__ segs,
+                   const double* __restrict__ taps, const double* __restrict__ w, const GridAcc ga) {
+    using C = SpreadTPCfg<SEG, NPAIR_>;
+    constexpr int kSU = SK_SPREAD3_SUNROLL > 0 ? SK_SPREAD3_SUNROLL : (SEG >= 64 ? 4 : 8);
+    constexpr int W = C::W, S = C::S, m = W / 2, TS = C::TS;
+    extern __shared__ __align__(16) double smem[];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int pair = warp >> 1, half = warp & 1;
+    const int g = lane >> 2, q = lane & 3;
+    const int plane = half * 32 + lane;
+    double* base = smem + pair * C::PAIR;
+    unsigned long long* full = reinterpret_cast<unsigned long long*>(base);   // [2]
+    unsigned long long* empty = full + 2;                                       // [2]
+    double* REGm = base + 4;
+    double* TB0 = base + 4 + C::REGP;
+    double* WB0 = TB0 + 2 * C::TBUF;
+    const int n = ga.n, ns = n / 2;
+    pdl_trigger();
+    pdl_wait();   // w, its bound slot and the cleared accumulator come from the preceding kernels
+    const double gscale = grid_scale(ga);
+    const int gp = blockIdx.x * C::NPAIR + pair, np = gridDim.x * C::NPAIR;
+    const bool producer = half == 0 && lane == 0;
+    if (producer) {
+        mbar_init(&full[0], 1);
+        mbar_init(&full[1], 1);
+        mbar_init(&empty[0], 2);
+        mbar_init(&empty[1], 2);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    for (int i = plane; i < C::REG; i += 64) REGm[i] = 0.0;
+    pair_barrier(pair);
+    auto issue = [&](const CellBatch& sq, int b) {
+        const long long st = sq.start;
+        const long long w0 = st & ~1LL, w1 = (st + sq.count + 1) & ~1LL;
+        const unsigned tbytes = (unsigned)sq.count * TS * 8u, wbytes = (unsigned)(w1 - w0) * 8u;
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        mbar_expect_tx(&full[b], tbytes + wbytes);
+        tma_load_1d(TB0 + b * C::TBUF, taps + st * TS, tbytes, &full[b]);
+        tma_load_1d(WB0 + b * C::WBUF, w + w0, wbytes, &full[b]);
+    };
+    int t = 0;   // segments of this pair so far (buffer t & 1, its (t >> 1)-th use)
+    CellBatch seg_next = gp < nitems ? segs[items[gp].seg_begin] : CellBatch{0, 0, 0, 0};
+    if (producer && gp < nitems) issue(seg_next, 0);
+    for (int ii = gp; ii < nitems; ii += np) {
+        const SpreadItem it = items[ii];
+        const int sz = it.stile % ns, sy = (it.stile / ns) % ns, sx = it.stile / ns / ns;
+        double acc28[14][2];
+        bool fresh = true;
+        for (int sg = it.seg_begin; sg < it.seg_end; ++sg, ++t) {
+            const int b = t & 1;
+            const CellBatch seg = seg_next;
+            // the pair's next segment: this item's, or the first of its next item
+            const bool more = sg + 1 < it.seg_end;
+            const int nxt_item = ii + np;
+            if (more) seg_next = segs[sg + 1];
+            else if (nxt_item < nitems) seg_next = segs[items[nxt_item].seg_begin];
+            if (producer && (more || nxt_item < nitems)) {
+                if (t >= 1) mbar_wait(&empty[b ^ 1], (unsigned)((t - 1) >> 1) & 1u);   // both warps released it
+                issue(seg_next, b ^ 1);
+            }
+            mbar_wait(&full[b], (unsigned)(t >> 1) & 1u);
+            const double* T0 = TB0 + b * C::TBUF;
+            const double* W0 = WB0 + b * C::WBUF + (seg.start & 1LL);
+            if (fresh) {
+#pragma unroll
+                for (int j = 0; j < 14; ++j) acc28[j][0] = acc28[j][1] = 0.0;
+                fresh = false;
+            }
+            const int nks = (seg.count + 3) >> 2;
+            if (half == 0) spread3_t28_ksteps<0, kSU>(acc28, T0, W0, seg.count, nks, g, q);
+            else spread3_t28_ksteps<1, kSU>(acc28, T0, W0, seg.count, nks, g, q);
+            __syncwarp();
+            if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&empty[b])) : "memory");
+            if (!more || seg_next.cell != seg.cell) {
+                // the warps may drift apart by a segment; consecutive cells' regions overlap, so
+                // the update of this cell waits until the partner finished the previous one
+                pair_barrier(pair);
+                const int cz = seg.cell % n, cy = (seg.cell / n) % n, cx = seg.cell / n / n;
+                double* rc = REGm + (cx - 2 * sx) * S * S + (cy - 2 * sy) * S + (cz - 2 * sz);
+                if (half == 0) spread3_t28_update<0>(acc28, rc, g, q);
+                else spread3_t28_update<1>(acc28, rc, g, q);
+                fresh = true;
+            }
+        }
+        pair_barrier(pair);
+        const int gx0 = 2 * sx - (m - 1), gy0 = 2 * sy - (m - 1), gz0 = 2 * sz - (m - 1);
+        for (int i = plane; i < C::REG; i += 64) {   // flush, and zero the region for the next item
+            const double v = REGm[i];
+            if (v != 0.0) {
+                const int rz = i % S, rest = i / S, ry = rest % S, rxx = rest / S;
+                grid_add<3>(ga, gscale, gx0 + rxx, gy0 + ry, gz0 + rz, v);
+                REGm[i] = 0.0;
+            }
+        }
+        pair_barrier(pair);
     }
 }
 

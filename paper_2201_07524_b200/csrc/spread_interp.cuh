@@ -273,11 +273,18 @@ inline int spread_dispatch(Plan& P, const NodeSet& S, const double* w, const Gri
                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SpreadTPCfgSparse::SMEM_BYTES);
             cudaFuncSetAttribute(spread3_tmapad_kernel<kSegTmaPDense, 2, false>,
                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SpreadTPCfgDense::SMEM_BYTES);
+            cudaFuncSetAttribute(spread3_t28_kernel<kSegTmaPMax, kSparsePairs>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SpreadTPCfgSparse::SMEM_BYTES);
+            cudaFuncSetAttribute(spread3_t28_kernel<kSegTmaPDense, 2>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SpreadTPCfgDense::SMEM_BYTES);
         }
+        static const bool pipe = SK_SPREAD3_PIPE && SK_SPREAD3_T28 && getenv("SK_SPREAD3_NOPIPE") == nullptr;
         if (S.nsitems > 0) {
-            const auto kern = S.seg_dense ? spread3_tmapad_kernel<kSegTmaPDense, 2, false>
+            const auto kern = S.seg_dense ? (pipe ? spread3_t28_kernel<kSegTmaPDense, 2>
+                                                  : spread3_tmapad_kernel<kSegTmaPDense, 2, false>)
                               : (S.xpairs ? spread3_tmapad_kernel<kSegTmaPMax, kSparsePairs, true>
-                                          : spread3_tmapad_kernel<kSegTmaPMax, kSparsePairs, false>);
+                                          : (pipe ? spread3_t28_kernel<kSegTmaPMax, kSparsePairs>
+                                                  : spread3_tmapad_kernel<kSegTmaPMax, kSparsePairs, false>));
             const int np = S.seg_dense ? SpreadTPCfgDense::NPAIR : SpreadTPCfgSparse::NPAIR;
             const int nt = S.seg_dense ? SpreadTPCfgDense::NT : SpreadTPCfgSparse::NT;
             const size_t sm = S.seg_dense ? SpreadTPCfgDense::SMEM_BYTES : SpreadTPCfgSparse::SMEM_BYTES;
