@@ -754,6 +754,7 @@ int build_plan(Ctx* ctx, Plan** out, int d, const double* x, long long n, const 
         // (16-row padded tiles) are opt-in (SK_XPAIRS=1): the 28-tile cover without them is faster
         // on c3 (924 -> 945 it/s, tools/ab_env.sh)
         P->spread_tmapad = P->dmma && d == 3;
+        P->spread_pipe = getenv("SK_SPREAD3_NOPIPE") == nullptr;
         P->spread_xpairs = P->dmma && d == 3 && getenv("SK_XPAIRS") != nullptr;
     }
     {   // phi(0)^d bounds one node's spread contribution |w| prod_a phi (deterministic mode)

@@ -202,6 +202,7 @@ struct Plan {
     bool tiled = false;       // v2 tiled spread/interp usable (d = 3, 2 m_w in {12, 16})
     bool dmma = false;        // FP64 tensor-core spread/interp (d = 3, 2 m_w = 12)
     bool spread_tmapad = false;  // d = 3 spread: the padded DMMA spread on TMA-fed warp pairs
+    bool spread_pipe = true;     // its full / empty mbarrier pipeline (SK_SPREAD3_NOPIPE=1: pair barriers)
     // deterministic spread (GridAcc): fixed-point box accumulator [box_size][2] + 1 word max |w|
     bool deterministic = false;
     unsigned long long* det_acc = nullptr;   // [2 box_size] accumulator, then 8 uint: 4 bound slots,

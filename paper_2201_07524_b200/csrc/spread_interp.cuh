@@ -278,7 +278,7 @@ inline int spread_dispatch(Plan& P, const NodeSet& S, const double* w, const Gri
             cudaFuncSetAttribute(spread3_t28_kernel<kSegTmaPDense, 2>,
                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SpreadTPCfgDense::SMEM_BYTES);
         }
-        static const bool pipe = SK_SPREAD3_PIPE && SK_SPREAD3_T28 && getenv("SK_SPREAD3_NOPIPE") == nullptr;
+        const bool pipe = SK_SPREAD3_PIPE && SK_SPREAD3_T28 && P.spread_pipe;
         if (S.nsitems > 0) {
             const auto kern = S.seg_dense ? (pipe ? spread3_t28_kernel<kSegTmaPDense, 2>
                                                   : spread3_tmapad_kernel<kSegTmaPDense, 2, false>)

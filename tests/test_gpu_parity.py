@@ -195,10 +195,11 @@ def _variant_sets():
 
 @pytest.mark.parametrize("env", [{}, {"SK_SEG_DENSE_MIN": "0"}, {"SK_SEG_DENSE_MIN": "1000000000"},
                                  {"SK_XPAIRS": "1"}, {"SK_NO_DMMA": "1"}, {"SK_DETERMINISTIC": "1"},
-                                 {"SK_DETERMINISTIC": "1", "SK_NO_DMMA": "1"}, {"SK_DETERMINISTIC": "0"}])
+                                 {"SK_DETERMINISTIC": "1", "SK_NO_DMMA": "1"}, {"SK_DETERMINISTIC": "0"},
+                                 {"SK_SPREAD3_NOPIPE": "1"}])
 def test_kernel_variants_match_gridding_definition(capi, ctx, env):
     """Every d = 3 spread/interp variant the plan can select (default shapes, forced dense or
-    32-node segments, x-pair segments, the vector path without tensor cores, the deterministic
+    32-node segments, x-pair segments, the pair-barrier form of the pipelined spread, the vector path without tensor cores, the deterministic
     fixed-point accumulation on both) on dense, mid and sparse cells against the gridding
     definition."""
     sets = _variant_sets()
