@@ -8,4 +8,4 @@ python bench.py --impl reference --steps 3 --warmup 1 > gpurun_out/fin_ref.jsonl
 bash tools/bench_all.sh > gpurun_out/fin_all.jsonl 2>&1
 SK_DETERMINISTIC=0 bash tools/bench_all.sh > gpurun_out/fin_all_atomic.jsonl 2>&1
 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/fin_launches_c5.csv python bench.py --steps 1 --warmup 0 --no-e2e --no-cpu-baseline > gpurun_out/fin_ncu.log 2>&1; echo ncu_rc=$?
-ncu --set full --clock-control none --import-source on -k regex:"spread3_tmapad|interp3" -c 4 -o gpurun_out/fin_kern python tools/profile_apply.py --config c5 --reps 1 --per-dir > gpurun_out/fin_ncu_kern.log 2>&1; tail -1 gpurun_out/fin_ncu_kern.log
+ncu --set full --clock-control none --import-source on -k regex:"spread3_t28|interp3" -c 6 -o gpurun_out/fin_kern python tools/profile_apply.py --config c5 --reps 1 --per-dir > gpurun_out/fin_ncu_kern.log 2>&1; tail -1 gpurun_out/fin_ncu_kern.log
