@@ -518,7 +518,7 @@ def main():
                                      "source range in the radius, factored exp (DESIGN.md §9b)"}
     if e2e:
         line["e2e"] = e2e
-    if rank == 0 and not args.no_cpu_baseline:
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:   # the oracle baseline: rank 0 at N = 1 only
         v, desc, cores, _ = cpu_oracle_rate(cfg, args.cpu_seconds)
         line["cpu_baseline"] = {"value": v, "unit": "it/s", "cores": cores, "kind": "oracle", "sample": desc,
                                 "cpu_model": cpu_model(), "nproc": os.cpu_count(),
