@@ -186,15 +186,26 @@ __device__ __forceinline__ void cp_async8(void* smem_dst, const void* gmem_src) 
     asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(sa), "l"(gmem_src));
 }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+__device__ __forceinline__ void cp_async16(void* smem_dst, const void* gmem_src) {
+    const unsigned sa = (unsigned)__cvta_generic_to_shared(smem_dst);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sa), "l"(gmem_src));
+}
+#ifndef SK_INTERP_XT_ASYNC
+#define SK_INTERP_XT_ASYNC 1   // phi_x staging of the next batch during this batch's epilogue
+#endif
 
 // One batch (<= 32 nodes of one cell) with NT_ n-tiles of 8 nodes: ragged tail batches of sparse
 // cells run ceil(count / 8) n-tiles instead of 4 (c3 x nodes: 29 % fewer DMMAs).
 // Hb: the cell's 12^3 block (+ q), row strides sxs (tx) and ry[] (the lane's 3 ty rows).
-template <int NT_, bool STAGE>
+struct NoHook {
+    __device__ __forceinline__ void operator()() const {}
+};
+template <int NT_, bool STAGE, typename Hook = NoHook>
 __device__ __forceinline__ void interp3_batch(const CellBatch& B, const double* __restrict__ taps,
                                               const double* XT, const double* Hb, long long sxs,
                                               const long long (&ry)[3], int ty1, int txo1, int g, int q,
-                                              double* __restrict__ t_out, const FusedUpd& fu) {
+                                              double* __restrict__ t_out, const FusedUpd& fu,
+                                              const Hook& after_kloop = Hook()) {
     using C = InterpDCfg;
     constexpr int W = C::W, KS = C::KS, TS = C::TS;
     const double* T0 = taps + (long long)B.start * TS;
@@ -261,6 +272,7 @@ __device__ __forceinline__ void interp3_batch(const CellBatch& B, const double* 
                 acc3[nt][e][2] = fma(xx.y, d[2][nt][e], acc3[nt][e][2]);
             }
     }
+    after_kloop();   // XT is free from here on (the epilogue reads phi_y from the taps)
     double acc[NT_][2];
 #pragma unroll
     for (int nt = 0; nt < NT_; ++nt)
@@ -346,6 +358,16 @@ interp3_dmma_kernel(const CellBatch* __restrict__ batches, int nbatches, const d
         }
         if (bi + 1 < b_hi)   // next batch of this warp: stream its taps into L2
             if (SK_INTERP_PREFETCH) prefetch_range(taps + (long long)Bnext.start * TS, (long long)Bnext.count * TS * 8, lane);
+#if SK_INTERP_XT_ASYNC
+        // phi_x rows of this batch: issued with cp.async during the previous batch's epilogue
+        // (first batch: here)
+        if (bi == b_lo && lane < NB) {
+            const double* src = T0 + min(lane, last) * TS;
+#pragma unroll
+            for (int i = 0; i < W / 2; ++i) cp_async16(XT + lane * C::XS + 2 * i, src + 2 * i);
+        }
+        cp_async_wait_all();
+#else
         if (lane < NB) {   // stage the batch's phi_x rows (lane = node) in this warp's shared table
             const double2* src = reinterpret_cast<const double2*>(T0 + min(lane, last) * TS);
             double2* dst = reinterpret_cast<double2*>(XT + lane * C::XS);
@@ -353,14 +375,30 @@ interp3_dmma_kernel(const CellBatch* __restrict__ batches, int nbatches, const d
             for (int i = 0; i < W / 2; ++i) dst[i] = __ldg(src + i);
         }
         if (new_cell) cp_async_wait_all();
+#endif
         __syncwarp();
         const double* Hb = STAGE ? GB + q
                                  : grid + (long long)(cx - m + 1) * n2 + (long long)(cy - m + 1) * n + (cz - m + 1) + q;
         const int ntn = min(NTN, (B.count + 7) >> 3);   // warp-uniform
-        if (ntn >= 4 && NTN >= 4) interp3_batch<(NTN >= 4 ? 4 : 1), STAGE>(B, taps, XT, Hb, sxs, ry, ty1, txo1, g, q, t_out, fu);
-        else if (ntn == 3 && NTN >= 3) interp3_batch<(NTN >= 3 ? 3 : 1), STAGE>(B, taps, XT, Hb, sxs, ry, ty1, txo1, g, q, t_out, fu);
-        else if (ntn == 2 && NTN >= 2) interp3_batch<(NTN >= 2 ? 2 : 1), STAGE>(B, taps, XT, Hb, sxs, ry, ty1, txo1, g, q, t_out, fu);
-        else interp3_batch<1, STAGE>(B, taps, XT, Hb, sxs, ry, ty1, txo1, g, q, t_out, fu);
+#if SK_INTERP_XT_ASYNC
+        const bool has_next = bi + 1 < b_hi;
+        const double* Tn = taps + (long long)Bnext.start * TS;
+        const int lastn = Bnext.count - 1;
+        auto hook = [&]() {   // next batch's phi_x rows, overlapping this batch's epilogue
+            __syncwarp();
+            if (has_next && lane < NB) {
+                const double* src = Tn + min(lane, lastn) * TS;
+#pragma unroll
+                for (int i = 0; i < W / 2; ++i) cp_async16(XT + lane * C::XS + 2 * i, src + 2 * i);
+            }
+        };
+#else
+        const NoHook hook;
+#endif
+        if (ntn >= 4 && NTN >= 4) interp3_batch<(NTN >= 4 ? 4 : 1), STAGE>(B, taps, XT, Hb, sxs, ry, ty1, txo1, g, q, t_out, fu, hook);
+        else if (ntn == 3 && NTN >= 3) interp3_batch<(NTN >= 3 ? 3 : 1), STAGE>(B, taps, XT, Hb, sxs, ry, ty1, txo1, g, q, t_out, fu, hook);
+        else if (ntn == 2 && NTN >= 2) interp3_batch<(NTN >= 2 ? 2 : 1), STAGE>(B, taps, XT, Hb, sxs, ry, ty1, txo1, g, q, t_out, fu, hook);
+        else interp3_batch<1, STAGE>(B, taps, XT, Hb, sxs, ry, ty1, txo1, g, q, t_out, fu, hook);
         __syncwarp();   // XT is rewritten by the next batch
     }
 }
