@@ -193,6 +193,9 @@ __device__ __forceinline__ void cp_async16(void* smem_dst, const void* gmem_src)
 #ifndef SK_INTERP_XT_ASYNC
 #define SK_INTERP_XT_ASYNC 1   // phi_x staging of the next batch during this batch's epilogue
 #endif
+#ifndef SK_INTERP_BF_AHEAD
+#define SK_INTERP_BF_AHEAD 0   // 1: the next batch's phi_z B fragments loaded during this batch's epilogue (measured slower)
+#endif
 
 // One batch (<= 32 nodes of one cell) with NT_ n-tiles of 8 nodes: ragged tail batches of sparse
 // cells run ceil(count / 8) n-tiles instead of 4 (c3 x nodes: 29 % fewer DMMAs).
@@ -200,24 +203,28 @@ __device__ __forceinline__ void cp_async16(void* smem_dst, const void* gmem_src)
 struct NoHook {
     __device__ __forceinline__ void operator()() const {}
 };
+// B fragments of a batch: phi_z of node 8 nt + g at tz = 4 s + q
+__device__ __forceinline__ void load_bf(double (&bf)[3][4], const double* __restrict__ T0, int last, int g, int q) {
+    constexpr int W = 12, TS = 3 * W;
+#pragma unroll
+    for (int nt = 0; nt < 4; ++nt) {
+        const double* tz = T0 + min(8 * nt + g, last) * TS + 2 * W;
+#pragma unroll
+        for (int s = 0; s < 3; ++s) bf[s][nt] = __ldg(tz + 4 * s + q);
+    }
+}
+// bfio: this batch's B fragments on entry (load_bf); after_kloop may overwrite them with the next
+// batch's (they are dead once the k loop is done)
 template <int NT_, bool STAGE, typename Hook = NoHook>
 __device__ __forceinline__ void interp3_batch(const CellBatch& B, const double* __restrict__ taps,
                                               const double* XT, const double* Hb, long long sxs,
                                               const long long (&ry)[3], int ty1, int txo1, int g, int q,
                                               double* __restrict__ t_out, const FusedUpd& fu,
-                                              const Hook& after_kloop = Hook()) {
+                                              double (&bf)[3][4], const Hook& after_kloop = Hook()) {
     using C = InterpDCfg;
     constexpr int W = C::W, KS = C::KS, TS = C::TS;
     const double* T0 = taps + (long long)B.start * TS;
     const int last = B.count - 1;
-    // B fragments: phi_z of node 8 nt + g at tz = 4 s + q
-    double bf[KS][NT_];
-#pragma unroll
-    for (int nt = 0; nt < NT_; ++nt) {
-        const double* tz = T0 + min(8 * nt + g, last) * TS + 2 * W;
-#pragma unroll
-        for (int s = 0; s < KS; ++s) bf[s][nt] = __ldg(tz + 4 * s + q);
-    }
     // per (node, ty) partial sums over tx: phi_y is applied once after the k loop, so each
     // E value costs one DFMA in the loop (24 per k-step at 4 n-tiles)
     double acc3[NT_][2][3];
@@ -339,6 +346,10 @@ interp3_dmma_kernel(const CellBatch* __restrict__ batches, int nbatches, const d
     pdl_trigger();
     pdl_wait();   // the grid (and the fused update's p, x) come from the preceding kernels
     CellBatch Bnext = b_lo < b_hi ? batches[b_lo] : CellBatch{0, 0, 0, 0};
+    double bf[3][4];   // B fragments of the batch about to run (loaded one batch ahead)
+#if SK_INTERP_BF_AHEAD
+    if (b_lo < b_hi) load_bf(bf, taps + (long long)Bnext.start * TS, Bnext.count - 1, g, q);
+#endif
     for (int bi = b_lo; bi < b_hi; ++bi) {
         const CellBatch B = Bnext;   // descriptor loaded one batch ahead
         if (bi + 1 < b_hi) Bnext = batches[bi + 1];
@@ -380,25 +391,29 @@ interp3_dmma_kernel(const CellBatch* __restrict__ batches, int nbatches, const d
         const double* Hb = STAGE ? GB + q
                                  : grid + (long long)(cx - m + 1) * n2 + (long long)(cy - m + 1) * n + (cz - m + 1) + q;
         const int ntn = min(NTN, (B.count + 7) >> 3);   // warp-uniform
-#if SK_INTERP_XT_ASYNC
         const bool has_next = bi + 1 < b_hi;
         const double* Tn = taps + (long long)Bnext.start * TS;
         const int lastn = Bnext.count - 1;
-        auto hook = [&]() {   // next batch's phi_x rows, overlapping this batch's epilogue
+        auto hook = [&]() {   // the next batch's operands, overlapping this batch's epilogue
+#if SK_INTERP_XT_ASYNC
             __syncwarp();
-            if (has_next && lane < NB) {
+            if (has_next && lane < NB) {   // phi_x rows
                 const double* src = Tn + min(lane, lastn) * TS;
 #pragma unroll
                 for (int i = 0; i < W / 2; ++i) cp_async16(XT + lane * C::XS + 2 * i, src + 2 * i);
             }
-        };
-#else
-        const NoHook hook;
 #endif
-        if (ntn >= 4 && NTN >= 4) interp3_batch<(NTN >= 4 ? 4 : 1), STAGE>(B, taps, XT, Hb, sxs, ry, ty1, txo1, g, q, t_out, fu, hook);
-        else if (ntn == 3 && NTN >= 3) interp3_batch<(NTN >= 3 ? 3 : 1), STAGE>(B, taps, XT, Hb, sxs, ry, ty1, txo1, g, q, t_out, fu, hook);
-        else if (ntn == 2 && NTN >= 2) interp3_batch<(NTN >= 2 ? 2 : 1), STAGE>(B, taps, XT, Hb, sxs, ry, ty1, txo1, g, q, t_out, fu, hook);
-        else interp3_batch<1, STAGE>(B, taps, XT, Hb, sxs, ry, ty1, txo1, g, q, t_out, fu, hook);
+#if SK_INTERP_BF_AHEAD
+            if (has_next) load_bf(bf, Tn, lastn, g, q);   // B fragments
+#endif
+        };
+#if !SK_INTERP_BF_AHEAD
+        load_bf(bf, T0, last, g, q);
+#endif
+        if (ntn >= 4 && NTN >= 4) interp3_batch<(NTN >= 4 ? 4 : 1), STAGE>(B, taps, XT, Hb, sxs, ry, ty1, txo1, g, q, t_out, fu, bf, hook);
+        else if (ntn == 3 && NTN >= 3) interp3_batch<(NTN >= 3 ? 3 : 1), STAGE>(B, taps, XT, Hb, sxs, ry, ty1, txo1, g, q, t_out, fu, bf, hook);
+        else if (ntn == 2 && NTN >= 2) interp3_batch<(NTN >= 2 ? 2 : 1), STAGE>(B, taps, XT, Hb, sxs, ry, ty1, txo1, g, q, t_out, fu, bf, hook);
+        else interp3_batch<1, STAGE>(B, taps, XT, Hb, sxs, ry, ty1, txo1, g, q, t_out, fu, bf, hook);
         __syncwarp();   // XT is rewritten by the next batch
     }
 }
